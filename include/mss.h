@@ -1,0 +1,181 @@
+/*
+ * mss.h — C ABI of the B200-native recursive multi-scale PCG (Lackner & Menikoff,
+ * arXiv math/9809043) for the cell-centred porous-flow operator -div(K grad p) = f.
+ *
+ * Citations "P:n" are PAPER.md line numbers (the paper's LaTeX source); DESIGN.md
+ * §2 lists every reading taken where the paper is silent (Q1..Q22).
+ *
+ * Conventions shared by every entry point
+ *   - All floating point is fp64.  Cell fields are contiguous, cell-centred, with
+ *     linear index c = i + n_x (j + n_y k) (x fastest); 2-D problems use n_z = 1.
+ *   - Pointers documented "device" are CUDA device pointers on the context's device
+ *     (PyTorch-allocated tensors in the Python binding); "host" pointers are plain
+ *     host memory.  The library never keeps a caller pointer after a call returns.
+ *   - Every call returns an int: 0 = MSS_OK; a positive value is a soft status; a
+ *     negative value is an error (see below).  No exception crosses the ABI.
+ *   - A context belongs to one host thread, one device and one CUDA stream at a time.
+ *   - All work is enqueued on the context's stream; calls that return host data
+ *     synchronise that stream before returning.
+ */
+#ifndef MSS_H
+#define MSS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------ */
+#define MSS_OK               0
+#define MSS_NOT_CONVERGED    1   /* some level hit max_iter; x holds the last iterate */
+#define MSS_EINVAL          -1   /* bad dims / K <= 0 or non-finite / scale < 2 / bad BC / bad level */
+#define MSS_ENOMEM          -2   /* device allocation failed */
+#define MSS_ECUDA           -3   /* CUDA runtime error (message via mss_last_error) */
+#define MSS_ENCCL           -4   /* NCCL error (distributed contexts) */
+#define MSS_ESINGULAR       -5   /* all-Neumann operator, isolated cell, or coarsest matrix not SPD */
+#define MSS_EBREAKDOWN      -6   /* rho <= 0 or p.Ap <= 0 inside a PCG call (DESIGN Q16) */
+#define MSS_EUNSUPPORTED    -7   /* option not built into this library */
+
+#define MSS_MAX_LEVELS      12
+
+/* Opaque context: owns every device buffer it allocates (faces, level vectors,
+ * coarsest factor); released by mss_free. */
+typedef struct mss_ctx mss_ctx;
+
+/* Boundary condition of one side.  kind 0 = Neumann: value = inward
+ * flux per unit area (0 = no flow); kind 1 = Dirichlet: value = pressure. */
+typedef struct { int kind; double value; } mss_bc;
+
+/* Method parameters.  mss_default_params fills the paper's choices. */
+typedef struct {
+  int     scale;        /* coarsening factor per axis; default 4                    */
+  int     m;            /* smoothing degree (SGS steps per side); default = scale    */
+  double  f;            /* per-level tolerance factor; default 0.1                   */
+  int     interp;       /* 0 = linear extension (default), 1 = piecewise constant */
+  int     max_iter;     /* PCG iteration cap per call per level; default 500 (paper silent, Q16) */
+  int     coarse_min;   /* stop coarsening once N_k <= coarse_min; default 512 (Q10)            */
+  int     use_lift;     /* 1 = x0 = P_bf (default); 0 = x0 = 0                       */
+  int64_t tail_cells;   /* levels with N_k <= tail_cells run inside one persistent cluster
+                           kernel per call (device-resident control); default 65536; 0 = off  */
+  int64_t gather_below; /* distributed: levels with N_k < gather_below are replicated; 64^3     */
+} mss_params;
+
+/* Per-solve report (the schema of the paper's Tables 1-2). */
+typedef struct {
+  int     levels;                        /* L+1 */
+  int64_t dims[MSS_MAX_LEVELS][3];       /* n_x, n_y, n_z per level (global) */
+  int64_t iters[MSS_MAX_LEVELS];         /* iterations summed over all calls; coarsest = solves */
+  int64_t calls[MSS_MAX_LEVELS];         /* PCG calls per level */
+  int     not_converged;                 /* 1 if any call hit max_iter */
+  int     breakdown_level;               /* -1 or the level of an EBREAKDOWN */
+  double  true_rel_res;                  /* ||b - A x|| / ||b|| after the solve */
+  double  bnorm2;                        /* ||b||^2 of the full RHS (O5) */
+  int64_t kernel_launches;               /* library kernels launched during the solve */
+} mss_info;
+
+int         mss_default_params(mss_params* p);
+const char* mss_strerror(int code);
+const char* mss_last_error(void);        /* thread-local detail of the last error */
+
+/*
+ * mss_setup — build the level hierarchy on the device (setup is excluded from the
+ * paper's timings).
+ *   ndim      2 or 3 (5-point / 7-point stencil).
+ *   n         cells per axis (n[2] ignored in 2-D).  With scale s every coarsened axis
+ *             must divide by s (DESIGN O8); otherwise coarsening stops there (auto
+ *             depth) or MSS_EINVAL (explicit depth).
+ *   extent    domain lengths per axis (host, NULL = unit box [0,1]^d).
+ *   K         device, k_comp * N doubles: per-cell permeability; k_comp = 1 (scalar) or
+ *             ndim (diagonal tensor K_xx, K_yy[, K_zz], each a full cell field).
+ *             Must be finite and > 0 (else MSS_EINVAL).
+ *   bc        host, 2*ndim entries in the order x-, x+, y-, y+, z-, z+.
+ *   depth     number of coarsenings, < 0 = automatic (until N_k <= coarse_min).
+ *   p         host, NULL = defaults.
+ *   stream    cudaStream_t (NULL = legacy default stream).
+ * Builds: face transmissibilities with harmonic-mean K,
+ * Reading-B coarse faces on every level, the dense coarsest matrix and
+ * its hand-written Cholesky factor.  Errors: MSS_EINVAL, MSS_ENOMEM,
+ * MSS_ECUDA, MSS_ESINGULAR.  On error *out is NULL.
+ */
+int mss_setup(mss_ctx** out, int ndim, const int64_t n[3], const double extent[3],
+              const double* K, int k_comp, const mss_bc bc[6], int depth,
+              const mss_params* p, void* stream);
+
+int mss_free(mss_ctx* ctx);
+int mss_num_levels(const mss_ctx* ctx, int* L1);                 /* L+1 */
+int mss_level_dims(const mss_ctx* ctx, int level, int64_t n[3]); /* local dims */
+
+/*
+ * mss_solve — solve A x = b where b_c = f_c V_c + boundary sources (O5).
+ *   f        device, N doubles: source density per cell (BASELINE's -div(K grad p) = f).
+ *   x        device, N doubles: out = pressure (lift included).  With use_lift = 0 its
+ *            input value is the initial guess (pass zeros for x0 = 0).
+ *   rel_tol  stop when ||r||^2 / N_0 < rel_tol^2 ||b||^2 / N_0 on level 0, and with the
+ *            per-level criterion ||r||^2/N_k < f^k eps^2 below.
+ *   iters_per_level  host, length >= L+1, nullable: iterations summed per level.
+ *   true_rel_res     host, nullable: ||b - A x|| / ||b||.
+ * Returns MSS_OK, MSS_NOT_CONVERGED, MSS_EBREAKDOWN, MSS_ECUDA.
+ */
+int mss_solve(mss_ctx* ctx, const double* f, double* x, double rel_tol,
+              int64_t* iters_per_level, double* true_rel_res);
+
+/* As mss_solve with HOST f and x; the host<->device copies happen inside the call
+ * (through pinned staging buffers) — the end-to-end path the bench's e2e leg times. */
+int mss_solve_host(mss_ctx* ctx, const double* f_host, double* x_host, double rel_tol,
+                   int64_t* iters_per_level, double* true_rel_res);
+
+int mss_get_info(const mss_ctx* ctx, mss_info* info);            /* last solve's report */
+
+/* ---- kernel-level hooks (parity tests; level-local compact device vectors) ---- */
+int mss_get_faces(const mss_ctx* ctx, int level, int dir, double* T);        /* device out */
+int mss_apply_A(mss_ctx* ctx, int level, const double* x, double* y);        /* y = A_k x   */
+int mss_dot(mss_ctx* ctx, int level, const double* a, const double* b, double* out /*host*/);
+/* n_half alternating half-sweeps on z starting with colour first_color (0 = red, the
+ * (i+j+k)-even cells); z_is_zero = 1 takes z = 0 on entry (O12). */
+int mss_smooth(mss_ctx* ctx, int level, const double* r, double* z, int n_half,
+               int first_color, int z_is_zero);
+/* coarse_b = R (r - A z) on level+1 (R = E^T).  Full residual, every colour. */
+int mss_residual_restrict(mss_ctx* ctx, int level, const double* r, const double* z,
+                          double* coarse_b);
+/* z += E y on the cells of colour `color` (-1 = all cells). */
+int mss_prolong_add(mss_ctx* ctx, int level, const double* coarse_y, double* z, int color);
+/* z = M_level^{-1} r, Eq. 2.10 with the recursive coarse PCG.  The
+ * tolerance of the inner solves uses eps^2 = rel_tol^2 ||r||^2 / N_level. */
+int mss_precond(mss_ctx* ctx, int level, const double* r, double* z, double rel_tol,
+                int64_t* iters_per_level);
+int mss_coarse_solve(mss_ctx* ctx, const double* b, double* x);   /* x = A_L^{-1} b */
+/* b (O5) and x0 = P_bf (O6) for a source density f. */
+int mss_rhs_lift(mss_ctx* ctx, const double* f, double* b, double* x0);
+
+/* ---- distributed (z-slabs across ranks; NCCL over NVLink) ------------------------ */
+int mss_nccl_unique_id(unsigned char id[128]);
+/* Rank r owns global planes [z_begin, z_end) given by mss_slab_range; K_local, and the
+ * f / x passed to mss_solve, are that rank's slab.  Levels with N_k < gather_below are
+ * replicated on every rank (allgather of the restricted RHS). */
+int mss_slab_range(const int64_t n_global[3], int ndim, int scale, int depth, int rank,
+                   int nranks, int64_t* z_begin, int64_t* z_end);
+int mss_setup_dist(mss_ctx** out, int rank, int nranks, const unsigned char id[128],
+                   int ndim, const int64_t n_global[3], const double extent[3],
+                   const double* K_local, int k_comp, const mss_bc bc[6], int depth,
+                   const mss_params* p, void* stream);
+
+/* ---- live per-kernel timing (bench.py's roofline) ----------------------------------
+ * With profiling on, every launch of a kernel class on a level <= max_level is
+ * bracketed by CUDA events on the context's stream; mss_profile_read returns, per
+ * (class, level), the launch count, summed device milliseconds and the algorithmic
+ * bytes those launches must move (DESIGN.md §6 per-cell figures x cells).
+ * Classes: 0 half-sweep (generic), 1 half-sweep from z = 0, 2 residual, 3 restrict,
+ * 4 prolong-add, 5 direction+SpMV+dot, 6 axpy+norm, 7 dot, 8 coarsest solve, 9 other. */
+#define MSS_NUM_KCLASS 10
+int mss_profile(mss_ctx* ctx, int enable, int max_level);      /* enable also resets */
+int mss_profile_read(const mss_ctx* ctx, int kclass, int level, int64_t* count,
+                     double* ms, double* bytes);
+
+/* Number of library kernels launched since the context was created. */
+int mss_kernel_launches(const mss_ctx* ctx, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSS_H */

@@ -1,0 +1,118 @@
+// internal.cuh — context / level structures of the B200 multi-scale PCG library.
+//
+// Memory layout in HBM:
+//   * cell vectors: x-fastest, contiguous; every level vector is allocated with one
+//     ghost xy-plane below and above the interior (zeroed, or filled by a halo
+//     exchange in distributed mode) so z-neighbour loads need no branch.  The
+//     interior pointer (base + plane) is what kernels index with c = i + nx (j + ny k).
+//   * faces: Tx (nz, ny, nx+1), Ty (nz, ny+1, nx), Tz (nz+1, ny, nx); face i along d
+//     lies between cells i-1 and i (the oracle's layout, so parity compares arrays).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/mss.h"
+
+#define MSS_DIRICHLET_KIND 1
+
+namespace mss {
+
+constexpr int kBlock = 256;           // threads per CTA for the streaming kernels
+constexpr int kSMs = 148;             // B200
+constexpr int kMaxGrid = kSMs * 16;   // grid-stride cap: 16 CTAs of 256 per SM in flight
+
+// Per-level CG scalars, resident on the device (one 64-byte record per level).
+struct Scal {
+  double rho;       // r.z of the current iteration
+  double rho_prev;  // r.z of the previous iteration
+  double pq;        // p.Ap
+  double rr;        // ||r||^2
+  double bb;        // ||b||^2 (level 0) / scratch
+  double aux;
+  double pad[2];
+};
+
+// Plain-pointer view of one level handed to kernels by value.
+struct LevelDev {
+  int nx, ny, nz;     // local dims (nz = 1 in 2-D)
+  int z0;             // global z offset of this slab (colour parity)
+  int64_t plane;      // nx * ny
+  int64_t N;          // nx * ny * nz
+  const double* Tx;
+  const double* Ty;
+  const double* Tz;   // nullptr in 2-D
+};
+
+struct Level {
+  int nx = 0, ny = 0, nz = 0;
+  int z0 = 0;
+  int64_t N = 0, plane = 0;
+  double h[3] = {1, 1, 1};
+  double *Tx = nullptr, *Ty = nullptr, *Tz = nullptr;
+  // ghosted cell vectors (interior pointers)
+  double *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *b = nullptr, *s = nullptr;
+  double *p[2] = {nullptr, nullptr};
+  double *t1 = nullptr, *t2 = nullptr;   // restriction temporaries (to level+1)
+  int pcur = 0;
+  double thr = 0;                          // N_k f^k eps^2 for the current solve
+  LevelDev dev() const {
+    LevelDev d;
+    d.nx = nx; d.ny = ny; d.nz = nz; d.z0 = z0; d.plane = plane; d.N = N;
+    d.Tx = Tx; d.Ty = Ty; d.Tz = Tz;
+    return d;
+  }
+};
+
+}  // namespace mss
+
+struct mss_ctx {
+  int ndim = 3;
+  mss_params prm;
+  mss_bc bc[6];
+  double extent[3] = {1, 1, 1};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int L = 0;                               // coarsest level index
+  std::vector<mss::Level> lv;
+  // coarsest dense solve
+  int NL = 0;
+  double* Achol = nullptr;                 // Cholesky factor (lower, row-major) of A_L
+  double* Ainv = nullptr;                  // A_L^{-1} formed from the factor (symmetrised)
+  // device scalars and reduction scratch
+  mss::Scal* dscal = nullptr;              // [MSS_MAX_LEVELS]
+  mss::Scal* hscal = nullptr;              // pinned mirror
+  double* partials = nullptr;              // [kMaxGrid]
+  unsigned* counter = nullptr;
+  int* dflag = nullptr;                    // setup validation flags
+  double* hbuf = nullptr;                  // pinned scratch (8 doubles)
+  // host staging for mss_solve_host
+  double* stage = nullptr;
+  size_t stage_bytes = 0;
+  double* dev_f = nullptr;                 // device f / x for mss_solve_host
+  double* dev_x = nullptr;
+  // lift
+  int lift_mode = 0;                       // 0 zero, 1 constant, 2 ramp in x
+  double lift_a = 0, lift_b = 0;
+  // solve state
+  double eps2 = 0;
+  int64_t launches = 0;
+  mss_info info;
+  std::vector<void*> allocs;
+  // live per-kernel timing (mss_profile)
+  struct ProfRec {
+    int cls, lvl;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  bool prof_on = false;
+  int prof_max_level = 0;
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<ProfRec> prof_pend;
+  double prof_ms[MSS_NUM_KCLASS][MSS_MAX_LEVELS] = {};
+  double prof_bytes[MSS_NUM_KCLASS][MSS_MAX_LEVELS] = {};
+  int64_t prof_cnt[MSS_NUM_KCLASS][MSS_MAX_LEVELS] = {};
+  // distributed (rank/nranks == 0/1 single GPU)
+  int rank = 0, nranks = 1;
+};

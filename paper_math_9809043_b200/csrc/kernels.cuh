@@ -1,0 +1,531 @@
+// kernels.cuh — fp64 CUDA kernels (sm_100a) of the multi-scale PCG hot path.
+//
+// Every kernel here is HBM-streaming stencil or vector work (≈0.3 flop/B): no tensor
+// cores.  Per-cell arithmetic follows the paper's definitions:
+//   operator  (A p)_c = sum_f T_f (p_c - p_nbr(f))           P:335-350, O4
+//   half-sweep z_c = (r_c + sum_f T_f z_nbr(f)) / sum_f T_f   P:353-357 (red-black SGS)
+//   extension  tensor product of 1-D linear (or constant) interpolation, R = E^T
+//   CG         Templates Fig. 2.5, Fletcher-Reeves beta.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace mss {
+
+// ------------------------------------------------------------------ reductions (K10)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum, fixed order (warp shuffles, then warp 0 over the warp partials); the
+// result is valid in thread 0.
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  if (w == 0) v = warp_sum(v);
+  return v;
+}
+
+// Where a grid reduction lands.  mode 0: *out = sum.  mode 1: *out = sum and
+// scal->rho_prev = scal->rho (end of a CG iteration).
+struct RedOut {
+  double* out;
+  double* partials;
+  unsigned* counter;
+  Scal* scal;
+  int mode;
+};
+
+// Single-pass grid reduction: every block writes its partial, the last block to
+// arrive sums the partials in block order (deterministic for a fixed grid).
+__device__ __forceinline__ void grid_sum_finish(double v, const RedOut& ro) {
+  __shared__ int s_last;
+  double bsum = block_sum(v);
+  if (threadIdx.x == 0) {
+    ro.partials[blockIdx.x] = bsum;
+    __threadfence();
+    unsigned t = atomicAdd(ro.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) acc += __ldcg(&ro.partials[i]);
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) {
+      *ro.out = acc;
+      if (ro.mode == 1) ro.scal->rho_prev = ro.scal->rho;
+      *ro.counter = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ cell geometry
+struct Cell {
+  int i, j, k;
+  int64_t c;
+};
+
+__device__ __forceinline__ Cell cell_of(const LevelDev& L, int64_t c) {
+  Cell e;
+  e.c = c;
+  const uint32_t uc = (uint32_t)c;
+  const uint32_t row = uc / (uint32_t)L.nx;
+  e.i = (int)(uc - row * (uint32_t)L.nx);
+  e.k = (int)(row / (uint32_t)L.ny);
+  e.j = (int)(row - (uint32_t)e.k * (uint32_t)L.ny);
+  return e;
+}
+
+// t[0..1] x-lower/upper, t[2..3] y-lower/upper, t[4..5] z-lower/upper.
+template <int NDIM>
+__device__ __forceinline__ void load_faces(const LevelDev& L, const Cell& e, double t[6]) {
+  const int64_t row = e.j + (int64_t)L.ny * e.k;
+  const int64_t fx = e.c + row;                 // i + (nx+1)(j + ny k)
+  const int64_t fy = e.c + (int64_t)L.nx * e.k; // i + nx (j + (ny+1) k)
+  t[0] = __ldg(L.Tx + fx);
+  t[1] = __ldg(L.Tx + fx + 1);
+  t[2] = __ldg(L.Ty + fy);
+  t[3] = __ldg(L.Ty + fy + L.nx);
+  if (NDIM == 3) {
+    t[4] = __ldg(L.Tz + e.c);
+    t[5] = __ldg(L.Tz + e.c + L.plane);
+  } else {
+    t[4] = 0.0;
+    t[5] = 0.0;
+  }
+}
+
+template <int NDIM>
+__device__ __forceinline__ double diag_of(const double t[6]) {
+  double d = t[0] + t[1] + t[2] + t[3];
+  if (NDIM == 3) d += t[4] + t[5];
+  return d;
+}
+
+// sum_f T_f v_nbr(f); v has zeroed ghost planes, x/y boundaries are masked.
+template <int NDIM, class Get>
+__device__ __forceinline__ double nbr_sum(const LevelDev& L, const Cell& e, const double t[6], Get v) {
+  const double xl = (e.i > 0) ? v(e.c - 1) : 0.0;
+  const double xh = (e.i < L.nx - 1) ? v(e.c + 1) : 0.0;
+  const double yl = (e.j > 0) ? v(e.c - L.nx) : 0.0;
+  const double yh = (e.j < L.ny - 1) ? v(e.c + L.nx) : 0.0;
+  double s = t[0] * xl + t[1] * xh + t[2] * yl + t[3] * yh;
+  if (NDIM == 3) s += t[4] * v(e.c - L.plane) + t[5] * v(e.c + L.plane);
+  return s;
+}
+
+__device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+// ------------------------------------------------------------------ setup kernels (a1-a3)
+__global__ void k_validate_K(const double* __restrict__ K, int64_t n, int* flag) {
+  for (int64_t t = gtid(); t < n; t += gstride()) {
+    const double v = K[t];
+    if (!(v > 0.0) || !isfinite(v)) atomicOr(flag, 1);
+  }
+}
+
+// a1: faces along direction d from the cell K_d (P:341-346 harmonic mean; P:366-371
+// boundary types; P:381-383 T = (A/h) K).  Face dims: n + e_d.
+__global__ void k_assemble_faces(const double* __restrict__ Kd, double* __restrict__ T,
+                                 int nx, int ny, int nz, int d, double coef,
+                                 int dir_lo, int dir_hi) {
+  const int Dx = nx + (d == 0), Dy = ny + (d == 1), Dz = nz + (d == 2);
+  const int64_t total = (int64_t)Dx * Dy * Dz;
+  const int nd = (d == 0) ? nx : (d == 1) ? ny : nz;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int fi = (int)(t % Dx);
+    const int64_t rr = t / Dx;
+    const int fj = (int)(rr % Dy);
+    const int fk = (int)(rr / Dy);
+    const int f = (d == 0) ? fi : (d == 1) ? fj : fk;   // face index along d
+    // cells on either side: f-1 and f along d
+    int ci = fi, cj = fj, ck = fk;
+    double val;
+    if (f == 0) {
+      val = dir_lo ? 2.0 * coef * Kd[ci + (int64_t)nx * (cj + (int64_t)ny * ck)] : 0.0;
+    } else if (f == nd) {
+      if (d == 0) ci -= 1; else if (d == 1) cj -= 1; else ck -= 1;
+      val = dir_hi ? 2.0 * coef * Kd[ci + (int64_t)nx * (cj + (int64_t)ny * ck)] : 0.0;
+    } else {
+      const double kb = Kd[ci + (int64_t)nx * (cj + (int64_t)ny * ck)];
+      if (d == 0) ci -= 1; else if (d == 1) cj -= 1; else ck -= 1;
+      const double ka = Kd[ci + (int64_t)nx * (cj + (int64_t)ny * ck)];
+      val = coef * (2.0 * ka * kb / (ka + kb));
+    }
+    T[t] = val;
+  }
+}
+
+// a2: Reading B coarse faces:  1/T^c_F = sum_i w_i / sum_{rows} T_d(i, rows),
+// w_i = |CV_i ∩ CV_F| / |CV_i| over the staggered control volumes; a zero column sum
+// blocks the face.  One thread per coarse face.
+__global__ void k_coarsen_faces(const double* __restrict__ Tf, double* __restrict__ Tc,
+                                int nfx, int nfy, int nfz,   // fine cell dims
+                                int ncx, int ncy, int ncz,   // coarse cell dims
+                                int d, int s, int ndim) {
+  const int Cx = ncx + (d == 0), Cy = ncy + (d == 1), Cz = ncz + (d == 2);
+  const int Fx = nfx + (d == 0), Fy = nfy + (d == 1);
+  const int64_t total = (int64_t)Cx * Cy * Cz;
+  const int nf_d = (d == 0) ? nfx : (d == 1) ? nfy : nfz;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    int c3[3];
+    c3[0] = (int)(t % Cx);
+    const int64_t rr = t / Cx;
+    c3[1] = (int)(rr % Cy);
+    c3[2] = (int)(rr / Cy);
+    const int F = c3[d];
+    const double a = fmax(s * (double)F - 0.5 * s, 0.0);
+    const double b = fmin(s * (double)F + 0.5 * s, (double)nf_d);
+    // the two transverse axes (in 2-D the z axis is a single row)
+    const int e1 = (d == 0) ? 1 : 0;
+    const int e2 = (d == 2) ? 1 : 2;
+    const int r1_lo = c3[e1] * s, r1_n = s;
+    const int r2_lo = (ndim == 3) ? c3[e2] * s : 0, r2_n = (ndim == 3) ? s : 1;
+    double inv = 0.0;
+    bool blocked = false;
+    const int ilo = max(0, s * F - s), ihi = min(nf_d, s * F + s);
+    for (int i = ilo; i <= ihi; ++i) {
+      const double lo = fmax(i - 0.5, 0.0), hi = fmin(i + 0.5, (double)nf_d);
+      const double ov = fmin(b, hi) - fmax(a, lo);
+      if (!(ov > 0.0)) continue;
+      const double w = ov / (hi - lo);
+      double cs = 0.0;
+      for (int q2 = 0; q2 < r2_n; ++q2) {
+        for (int q1 = 0; q1 < r1_n; ++q1) {
+          int f3[3];
+          f3[d] = i;
+          f3[e1] = r1_lo + q1;
+          f3[e2] = r2_lo + q2;
+          cs += Tf[f3[0] + (int64_t)Fx * (f3[1] + (int64_t)Fy * f3[2])];
+        }
+      }
+      if (cs == 0.0) blocked = true;
+      else inv += w / cs;
+    }
+    Tc[t] = blocked ? 0.0 : 1.0 / inv;
+  }
+}
+
+// a3: dense coarsest matrix, row c: diag and -T to in-domain neighbours.
+template <int NDIM>
+__global__ void k_dense_assemble(LevelDev L, double* __restrict__ A) {
+  const int64_t n = L.N;
+  for (int64_t c = gtid(); c < n; c += gstride()) {
+    const Cell e = cell_of(L, c);
+    double t[6];
+    load_faces<NDIM>(L, e, t);
+    A[c * n + c] = diag_of<NDIM>(t);
+    if (e.i > 0) A[c * n + c - 1] = -t[0];
+    if (e.i < L.nx - 1) A[c * n + c + 1] = -t[1];
+    if (e.j > 0) A[c * n + c - L.nx] = -t[2];
+    if (e.j < L.ny - 1) A[c * n + c + L.nx] = -t[3];
+    if (NDIM == 3) {
+      if (e.k > 0) A[c * n + c - L.plane] = -t[4];
+      if (e.k < L.nz - 1) A[c * n + c + L.plane] = -t[5];
+    }
+  }
+}
+
+// Hand-written unblocked right-looking Cholesky, A = L L^T, in place on the lower
+// triangle (row-major), one CTA.  flag = 1 if a pivot is not positive.
+__global__ void k_cholesky(double* __restrict__ A, int n, int* flag) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double dj = A[(int64_t)j * n + j];
+      if (!(dj > 0.0)) bad = 1;
+      else A[(int64_t)j * n + j] = sqrt(dj);
+    }
+    __syncthreads();
+    if (bad) {
+      if (threadIdx.x == 0) *flag = 1;
+      return;
+    }
+    const double ljj = A[(int64_t)j * n + j];
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + j] /= ljj;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) {
+      const int ii = (int)(idx / m), kk = (int)(idx % m);
+      if (kk > ii) continue;
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      A[(int64_t)i * n + k] -= A[(int64_t)i * n + j] * A[(int64_t)k * n + j];
+    }
+    __syncthreads();
+  }
+}
+
+// X = (L L^T)^{-1}: thread j solves L y = e_j then L^T x = y (column j of X).
+__global__ void k_chol_inverse(const double* __restrict__ Lf, double* __restrict__ X, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int i = 0; i < j; ++i) X[(int64_t)i * n + j] = 0.0;
+  for (int i = j; i < n; ++i) {
+    double acc = (i == j) ? 1.0 : 0.0;
+    for (int k = j; k < i; ++k) acc -= Lf[(int64_t)i * n + k] * X[(int64_t)k * n + j];
+    X[(int64_t)i * n + j] = acc / Lf[(int64_t)i * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = X[(int64_t)i * n + j];
+    for (int k = i + 1; k < n; ++k) acc -= Lf[(int64_t)k * n + i] * X[(int64_t)k * n + j];
+    X[(int64_t)i * n + j] = acc / Lf[(int64_t)i * n + i];
+  }
+}
+
+__global__ void k_symmetrize(const double* __restrict__ X, double* __restrict__ S, int n) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int64_t i = t / n, j = t % n;
+    S[t] = 0.5 * (X[i * n + j] + X[j * n + i]);
+  }
+}
+
+// ------------------------------------------------------------------ a4: RHS and lift
+struct BCDev {
+  int kind[6];
+  double val[6];
+  double area[3];
+  int lift_mode;       // 0 zero, 1 constant lift_a, 2 ramp lift_a + (lift_b - lift_a) x_c
+  double lift_a, lift_b;
+};
+
+template <int NDIM>
+__global__ void k_rhs_lift(LevelDev L, const double* __restrict__ f, double* __restrict__ b,
+                           double* __restrict__ x0, double V, BCDev bc) {
+  for (int64_t c = gtid(); c < L.N; c += gstride()) {
+    const Cell e = cell_of(L, c);
+    double t[6];
+    load_faces<NDIM>(L, e, t);
+    double v = f[c] * V;
+    const int idx[3] = {e.i, e.j, e.k};
+    const int nn[3] = {L.nx, L.ny, L.nz};
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) {
+      if (idx[d] == 0) {
+        v += (bc.kind[2 * d] == MSS_DIRICHLET_KIND) ? t[2 * d] * bc.val[2 * d] : bc.area[d] * bc.val[2 * d];
+      }
+      if (idx[d] == nn[d] - 1) {
+        v += (bc.kind[2 * d + 1] == MSS_DIRICHLET_KIND) ? t[2 * d + 1] * bc.val[2 * d + 1]
+                                                         : bc.area[d] * bc.val[2 * d + 1];
+      }
+    }
+    b[c] = v;
+    if (x0) {
+      double l = 0.0;
+      if (bc.lift_mode == 1) l = bc.lift_a;
+      else if (bc.lift_mode == 2) {
+        const double xc = (e.i + 0.5) / (double)L.nx;
+        l = bc.lift_a + (bc.lift_b - bc.lift_a) * xc;
+      }
+      x0[c] = l;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ operator (K08 part) & residual
+// r = b - A x, with ||r||^2 reduced when ro.out != nullptr.
+template <int NDIM>
+__global__ void k_residual(LevelDev L, const double* __restrict__ b, const double* __restrict__ x,
+                           double* __restrict__ r, RedOut ro) {
+  double acc = 0.0;
+  for (int64_t c = gtid(); c < L.N; c += gstride()) {
+    const Cell e = cell_of(L, c);
+    double t[6];
+    load_faces<NDIM>(L, e, t);
+    const double ax = diag_of<NDIM>(t) * x[c] - nbr_sum<NDIM>(L, e, t, [&](int64_t q) { return x[q]; });
+    const double rv = b[c] - ax;
+    r[c] = rv;
+    acc += rv * rv;
+  }
+  if (ro.out) grid_sum_finish(acc, ro);
+}
+
+template <int NDIM>
+__global__ void k_apply_A(LevelDev L, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t c = gtid(); c < L.N; c += gstride()) {
+    const Cell e = cell_of(L, c);
+    double t[6];
+    load_faces<NDIM>(L, e, t);
+    y[c] = diag_of<NDIM>(t) * x[c] - nbr_sum<NDIM>(L, e, t, [&](int64_t q) { return x[q]; });
+  }
+}
+
+// ------------------------------------------------------------------ a5/a9: red-black half-sweep (K05)
+// Cells of colour `colour` ((i + j + k + z0) % 2): z_c = (r_c + sum_f T_f z_nbr) / diag_c.
+// FIRST: z = 0 on entry, so z_c = r_c / diag_c (only T and r are read).
+// Threads walk the colour's cells: thread t -> row = t / hx, i = 2 (t % hx) + parity(row).
+template <int NDIM, bool FIRST>
+__global__ void k_halfsweep(LevelDev L, const double* __restrict__ r, double* __restrict__ z, int colour) {
+  const uint32_t hx = (uint32_t)(L.nx + 1) >> 1;
+  const int64_t total = (int64_t)hx * L.ny * L.nz;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const uint32_t ut = (uint32_t)t;
+    const uint32_t row = ut / hx;
+    const uint32_t m = ut - row * hx;
+    const uint32_t k = row / (uint32_t)L.ny;
+    const uint32_t j = row - k * (uint32_t)L.ny;
+    const int i = 2 * (int)m + (int)((j + k + (uint32_t)L.z0 + (uint32_t)colour) & 1u);
+    if (i >= L.nx) continue;
+    Cell e;
+    e.i = i; e.j = (int)j; e.k = (int)k;
+    e.c = i + (int64_t)L.nx * row;
+    double tf[6];
+    load_faces<NDIM>(L, e, tf);
+    double acc = r[e.c];
+    if (!FIRST) acc += nbr_sum<NDIM>(L, e, tf, [&](int64_t q) { return z[q]; });
+    z[e.c] = acc / diag_of<NDIM>(tf);
+  }
+}
+
+// ------------------------------------------------------------------ a6/a8: transfer
+// 1-D weights of fine cell i onto coarse cells: (I0, w0) + (I1, w1).
+__device__ __forceinline__ void interp_w(int i, int nc, int s, int kind, int& I0, double& w0, int& I1, double& w1) {
+  if (kind == 1 || nc == 1) {   // piecewise constant
+    I0 = min(i / s, nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
+    return;
+  }
+  const double x = i + 0.5;                   // fine centre in fine-cell units
+  const double X0 = 0.5 * s, Xl = s * (nc - 0.5);
+  if (x <= X0) { I0 = 0; w0 = 1.0; I1 = 0; w1 = 0.0; return; }          // zero slope
+  if (x >= Xl) { I0 = nc - 1; w0 = 1.0; I1 = nc - 1; w1 = 0.0; return; }
+  const int I = (int)floor((x - X0) / s);
+  const double tt = (x - s * (I + 0.5)) / s;
+  I0 = I; w0 = 1.0 - tt; I1 = I + 1; w1 = tt;
+}
+
+// out = R_axis in along one axis: (n0,n1,n2) -> same with n_axis -> nc.  Gather form.
+__global__ void k_restrict_axis(const double* __restrict__ in, double* __restrict__ out,
+                                int n0, int n1, int n2, int axis, int nc, int s, int kind) {
+  const int o0 = (axis == 0) ? nc : n0, o1 = (axis == 1) ? nc : n1, o2 = (axis == 2) ? nc : n2;
+  const int64_t total = (int64_t)o0 * o1 * o2;
+  const int nf = (axis == 0) ? n0 : (axis == 1) ? n1 : n2;
+  const int64_t stride_ax = (axis == 0) ? 1 : (axis == 1) ? (int64_t)n0 : (int64_t)n0 * n1;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    int q[3];
+    q[0] = (int)(t % o0);
+    const int64_t rr = t / o0;
+    q[1] = (int)(rr % o1);
+    q[2] = (int)(rr / o1);
+    const int I = q[axis];
+    q[axis] = 0;
+    const int64_t base = q[0] + (int64_t)n0 * (q[1] + (int64_t)n1 * q[2]);
+    double acc = 0.0;
+    const int ilo = max(0, s * (I - 1)), ihi = min(nf, s * (I + 2));
+    for (int i = ilo; i < ihi; ++i) {
+      int I0, I1; double w0, w1;
+      interp_w(i, nc, s, kind, I0, w0, I1, w1);
+      double w = 0.0;
+      if (I0 == I) w += w0;
+      if (I1 == I && I1 != I0) w += w1;
+      if (w != 0.0) acc += w * in[base + i * stride_ax];
+    }
+    out[t] = acc;
+  }
+}
+
+// z_c += (E y)_c on cells of colour `colour` (-1 = all).  y is the coarse level's
+// compact vector.
+template <int NDIM>
+__global__ void k_prolong_add(LevelDev L, int ncx, int ncy, int ncz, int s, int kind,
+                              const double* __restrict__ y, double* __restrict__ z, int colour) {
+  for (int64_t c = gtid(); c < L.N; c += gstride()) {
+    const Cell e = cell_of(L, c);
+    if (colour >= 0 && (((e.i + e.j + e.k + L.z0) & 1) != colour)) continue;
+    int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
+    double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
+    interp_w(e.i, ncx, s, kind, X0, wx0, X1, wx1);
+    interp_w(e.j, ncy, s, kind, Y0, wy0, Y1, wy1);
+    if (NDIM == 3) interp_w(e.k, ncz, s, kind, Z0, wz0, Z1, wz1);
+    const int64_t cp = (int64_t)ncx * ncy;
+    auto Y = [&](int a, int bb, int cc) { return y[a + (int64_t)ncx * bb + cp * cc]; };
+    double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
+                 wy1 * (wx0 * Y(X0, Y1, Z0) + wx1 * Y(X1, Y1, Z0));
+    if (NDIM == 3) {
+      acc *= wz0;
+      acc += wz1 * (wy0 * (wx0 * Y(X0, Y0, Z1) + wx1 * Y(X1, Y0, Z1)) +
+                    wy1 * (wx0 * Y(X0, Y1, Z1) + wx1 * Y(X1, Y1, Z1)));
+    }
+    z[c] += acc;
+  }
+}
+
+// ------------------------------------------------------------------ a10: direction + SpMV + dot (K08)
+// p_out = z + beta p_in (beta = rho / rho_prev; p = z on the first iteration);
+// q = A p_out; reduces p_out . q into scal->pq.  The neighbours' p_out are formed on
+// the fly from z and p_in, so the update and the SpMV are one pass.
+template <int NDIM>
+__global__ void k_pdir_spmv_dot(LevelDev L, const double* __restrict__ z, const double* __restrict__ pin,
+                                double* __restrict__ pout, double* __restrict__ q, const Scal* sc,
+                                int first, RedOut ro) {
+  const double beta = first ? 0.0 : sc->rho / sc->rho_prev;
+  double acc = 0.0;
+  for (int64_t c = gtid(); c < L.N; c += gstride()) {
+    const Cell e = cell_of(L, c);
+    double t[6];
+    load_faces<NDIM>(L, e, t);
+    auto P = [&](int64_t idx) { return first ? z[idx] : z[idx] + beta * pin[idx]; };
+    const double pc = P(c);
+    const double qc = diag_of<NDIM>(t) * pc - nbr_sum<NDIM>(L, e, t, P);
+    pout[c] = pc;
+    q[c] = qc;
+    acc += pc * qc;
+  }
+  grid_sum_finish(acc, ro);
+}
+
+// a11: alpha = rho / pq; x += alpha p; r -= alpha q; ||r||^2 -> scal->rr; rho_prev = rho.
+__global__ void k_axpy_norm(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                            const double* __restrict__ p, const double* __restrict__ q,
+                            const Scal* sc, RedOut ro) {
+  const double alpha = sc->rho / sc->pq;
+  double acc = 0.0;
+  for (int64_t c = gtid(); c < n; c += gstride()) {
+    x[c] += alpha * p[c];
+    const double rv = r[c] - alpha * q[c];
+    r[c] = rv;
+    acc += rv * rv;
+  }
+  grid_sum_finish(acc, ro);
+}
+
+__global__ void k_dot(int64_t n, const double* __restrict__ a, const double* __restrict__ b, RedOut ro) {
+  double acc = 0.0;
+  for (int64_t c = gtid(); c < n; c += gstride()) acc += a[c] * b[c];
+  grid_sum_finish(acc, ro);
+}
+
+__global__ void k_axpy(int64_t n, double* __restrict__ x, const double* __restrict__ y) {
+  for (int64_t c = gtid(); c < n; c += gstride()) x[c] += y[c];
+}
+
+// ------------------------------------------------------------------ a7 coarsest: x = A_L^{-1} b (K11)
+// One warp per row of the symmetrised inverse, lanes stride the row (coalesced).
+__global__ void k_coarse_solve(const double* __restrict__ Ainv, const double* __restrict__ b,
+                               double* __restrict__ x, int n) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int row = warp; row < n; row += nwarps) {
+    double acc = 0.0;
+    for (int k = lane; k < n; k += 32) acc += Ainv[(int64_t)row * n + k] * b[k];
+    acc = warp_sum(acc);
+    if (lane == 0) x[row] = acc;
+  }
+}
+
+}  // namespace mss

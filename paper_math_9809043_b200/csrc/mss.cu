@@ -1,0 +1,872 @@
+// mss.cu — setup, recursive PCG driver and C ABI (include/mss.h).
+//
+// The driver implements Eq. 2.10 as the sequence the survey derived and
+// the oracle pins (P6): z = 0; 2m+1 red/black half-sweeps; coarse correction
+// z += E A_c^{-1} R (r - A z) with A_c^{-1} applied by PCG on the coarser level
+// (recursively; exact Cholesky-based solve on the coarsest); 2m+1 more
+// half-sweeps.  Every level runs conventional PCG (Templates Fig. 2.5) with
+// the per-level stop ||r||^2 < N_k f^k eps^2, so the depth of each
+// excursion is decided dynamically.
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+#include "tail.cuh"
+
+using namespace mss;
+
+static thread_local std::string g_err;
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(_e);             \
+      return MSS_ECUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    int _rc = (expr);             \
+    if (_rc < 0) return _rc;      \
+  } while (0)
+
+static int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+static int grid_for(int64_t work) {
+  int64_t g = (work + kBlock - 1) / kBlock;
+  if (g < 1) g = 1;
+  if (g > kMaxGrid) g = kMaxGrid;
+  return (int)g;
+}
+
+static int dalloc(mss_ctx* ctx, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
+  if (e != cudaSuccess) {
+    g_err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+    return MSS_ENOMEM;
+  }
+  ctx->allocs.push_back(*p);
+  return MSS_OK;
+}
+
+// ghosted cell vector: (nz + 2) planes, zeroed; returns the interior pointer.
+static int valloc(mss_ctx* ctx, const Level& l, double** out) {
+  void* p = nullptr;
+  TRY(dalloc(ctx, &p, sizeof(double) * (size_t)(l.N + 2 * l.plane)));
+  CK(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)(l.N + 2 * l.plane), ctx->stream));
+  *out = reinterpret_cast<double*>(p) + l.plane;
+  return MSS_OK;
+}
+
+static RedOut red_to(mss_ctx* ctx, double* out, int level, int mode) {
+  RedOut ro;
+  ro.out = out;
+  ro.partials = ctx->partials;
+  ro.counter = ctx->counter;
+  ro.scal = ctx->dscal + level;
+  ro.mode = mode;
+  return ro;
+}
+
+#define LAUNCH(kern, grid, ...)                                       \
+  do {                                                                \
+    kern<<<(grid), kBlock, 0, ctx->stream>>>(__VA_ARGS__);            \
+    ctx->launches++;                                                  \
+  } while (0)
+
+#define DISPATCH(ndim, kern, grid, ...)                               \
+  do {                                                                \
+    if ((ndim) == 3) LAUNCH(kern<3>, grid, __VA_ARGS__);              \
+    else LAUNCH(kern<2>, grid, __VA_ARGS__);                          \
+  } while (0)
+
+// ============================================================================ live kernel timing
+enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_OTHER };
+
+static cudaEvent_t ev_get(mss_ctx* ctx) {
+  if (!ctx->ev_free.empty()) {
+    cudaEvent_t e = ctx->ev_free.back();
+    ctx->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+static void prof_flush(mss_ctx* ctx) {
+  for (auto& r : ctx->prof_pend) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    ctx->prof_ms[r.cls][r.lvl] += ms;
+    ctx->prof_cnt[r.cls][r.lvl] += 1;
+    ctx->prof_bytes[r.cls][r.lvl] += r.bytes;
+    ctx->ev_free.push_back(r.a);
+    ctx->ev_free.push_back(r.b);
+  }
+  ctx->prof_pend.clear();
+}
+
+// Brackets the launches issued in its scope with events (when profiling this level).
+struct ProfScope {
+  mss_ctx* c;
+  mss_ctx::ProfRec r;
+  bool on;
+  ProfScope(mss_ctx* ctx, int cls, int lvl, double bytes) : c(ctx), on(false) {
+    if (ctx->prof_on && lvl <= ctx->prof_max_level) {
+      on = true;
+      r.cls = cls;
+      r.lvl = lvl;
+      r.bytes = bytes;
+      r.a = ev_get(ctx);
+      cudaEventRecord(r.a, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (!on) return;
+    r.b = ev_get(c);
+    cudaEventRecord(r.b, c->stream);
+    c->prof_pend.push_back(r);
+    if (c->prof_pend.size() > 8192) prof_flush(c);
+  }
+};
+
+// Algorithmic bytes per cell (fp64 words x 8) of each kernel with the interleaved
+// layout (SURVEY §8(d) "interleaved" column): T = ndim words per cell.
+static double cell_bytes(const mss_ctx* ctx, int cls) {
+  const double T = ctx->ndim;
+  switch (cls) {
+    case KC_SWEEP: return 8.0 * (T + 3);    // T + r + z(nbr lines) + z write
+    case KC_SWEEP0: return 8.0 * (T + 2);   // T + r + z write
+    case KC_RESID: return 8.0 * (T + 3);    // T + r + z + s write
+    case KC_PROLONG: return 8.0 * 2;        // z read + write (coarse y from L2)
+    case KC_SPMV: return 8.0 * (T + 4);     // T + z + p_in + p_out + q
+    case KC_AXPY: return 8.0 * 6;           // x, r, p, q read; x, r write
+    case KC_DOT: return 8.0 * 2;
+    default: return 0.0;
+  }
+}
+
+// ============================================================================ kernels wrappers
+static int op_dot(mss_ctx* ctx, int level, int64_t n, const double* a, const double* b, double* out) {
+  ProfScope ps(ctx, KC_DOT, level, cell_bytes(ctx, KC_DOT) * n);
+  LAUNCH(k_dot, grid_for(n), n, a, b, red_to(ctx, out, level, 0));
+  return MSS_OK;
+}
+
+static int op_residual(mss_ctx* ctx, int k, const double* b, const double* x, double* r, double* rr_out) {
+  Level& l = ctx->lv[k];
+  RedOut ro = red_to(ctx, rr_out, k, 0);
+  ProfScope ps(ctx, KC_RESID, k, cell_bytes(ctx, KC_RESID) * l.N);
+  DISPATCH(ctx->ndim, k_residual, grid_for(l.N), l.dev(), b, x, r, ro);
+  return MSS_OK;
+}
+
+static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int colour, bool first) {
+  Level& l = ctx->lv[k];
+  const int64_t work = (int64_t)((l.nx + 1) / 2) * l.ny * l.nz;
+  const int g = grid_for(work);
+  ProfScope ps(ctx, first ? KC_SWEEP0 : KC_SWEEP, k, cell_bytes(ctx, first ? KC_SWEEP0 : KC_SWEEP) * l.N);
+  if (ctx->ndim == 3) {
+    if (first) LAUNCH((k_halfsweep<3, true>), g, l.dev(), r, z, colour);
+    else LAUNCH((k_halfsweep<3, false>), g, l.dev(), r, z, colour);
+  } else {
+    if (first) LAUNCH((k_halfsweep<2, true>), g, l.dev(), r, z, colour);
+    else LAUNCH((k_halfsweep<2, false>), g, l.dev(), r, z, colour);
+  }
+  return MSS_OK;
+}
+
+// n_half alternating half-sweeps starting with `first_colour`.
+static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero) {
+  for (int h = 0; h < n_half; ++h) {
+    const int col = (first_colour + h) & 1;
+    TRY(op_halfsweep(ctx, k, r, z, col, z_zero && h == 0));
+  }
+  return MSS_OK;
+}
+
+// coarse r_{k+1} = R s_k where s_k is the level-k vector `s` (ghost-free use).
+static int op_restrict(mss_ctx* ctx, int k, const double* s, double* coarse) {
+  Level& f = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  const int S = ctx->prm.scale, kind = ctx->prm.interp;
+  const double rb = (ctx->ndim == 3)
+      ? 8.0 * ((double)f.N + 2.0 * c.nx * f.ny * f.nz + 2.0 * c.nx * c.ny * f.nz + c.N)
+      : 8.0 * ((double)f.N + 2.0 * c.nx * f.ny + c.N);
+  ProfScope ps(ctx, KC_RESTRICT, k, rb);
+  if (ctx->ndim == 3) {
+    // x: (nx,ny,nz) -> (ncx,ny,nz) ; y: -> (ncx,ncy,nz) ; z: -> (ncx,ncy,ncz)
+    LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * f.ny * f.nz), s, f.t1, f.nx, f.ny, f.nz, 0, c.nx, S, kind);
+    LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * c.ny * f.nz), f.t1, f.t2, c.nx, f.ny, f.nz, 1, c.ny, S, kind);
+    LAUNCH(k_restrict_axis, grid_for(c.N), f.t2, coarse, c.nx, c.ny, f.nz, 2, c.nz, S, kind);
+  } else {
+    LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * f.ny), s, f.t1, f.nx, f.ny, 1, 0, c.nx, S, kind);
+    LAUNCH(k_restrict_axis, grid_for(c.N), f.t1, coarse, c.nx, f.ny, 1, 1, c.ny, S, kind);
+  }
+  return MSS_OK;
+}
+
+static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int colour) {
+  Level& f = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
+  DISPATCH(ctx->ndim, k_prolong_add, grid_for(f.N), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
+           ctx->prm.interp, y, z, colour);
+  return MSS_OK;
+}
+
+static int op_coarse_solve(mss_ctx* ctx, const double* b, double* x) {
+  const int n = ctx->NL;
+  const int blocks = (n * 32 + kBlock - 1) / kBlock;
+  ProfScope ps(ctx, KC_COARSE, ctx->L, 8.0 * ((double)n * n + 2.0 * n));
+  LAUNCH(k_coarse_solve, blocks < 1 ? 1 : blocks, ctx->Ainv, b, x, n);
+  return MSS_OK;
+}
+
+static int read_scal(mss_ctx* ctx, int k) {
+  CK(cudaMemcpyAsync(ctx->hscal + k, ctx->dscal + k, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+// ============================================================================ recursion
+static int pcg_level(mss_ctx* ctx, int k);
+
+// z_k = M_k^{-1} r_k  (Eq. 2.10 as the smoothing / coarse-correction sequence)
+static int precond(mss_ctx* ctx, int k) {
+  Level& l = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  const int nh = 2 * ctx->prm.m + 1;
+  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));                 // pre-smoothing (a5)
+  TRY(op_residual(ctx, k, l.r, l.z, l.s, nullptr));              // s = r - A z (a6)
+  TRY(op_restrict(ctx, k, l.s, c.r));                            // b_{k+1} = R s
+  if (k + 1 == ctx->L) {                                         // coarsest: exact (a7)
+    TRY(op_coarse_solve(ctx, c.r, c.x));
+    ctx->info.iters[k + 1] += 1;
+    ctx->info.calls[k + 1] += 1;
+  } else if (c.N <= ctx->prm.tail_cells && tail_supported(ctx, k + 1)) {
+    TRY(tail_pcg(ctx, k + 1));                                   // device-resident coarse levels
+  } else {
+    CK(cudaMemsetAsync(c.x, 0, sizeof(double) * c.N, ctx->stream));
+    TRY(pcg_level(ctx, k + 1));
+  }
+  TRY(op_prolong_add(ctx, k, c.x, l.z, 1));                      // z_black += (E y) (a8)
+  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false));                // post-smoothing (a9)
+  return MSS_OK;
+}
+
+// PCG on level k; on entry r_k holds the residual of the current x_k (x_k = 0 and
+// r_k = b_k for k > 0).  Level thresholds are precomputed in l.thr.
+static int pcg_level(mss_ctx* ctx, int k) {
+  Level& l = ctx->lv[k];
+  Scal* ds = ctx->dscal + k;
+  ctx->info.calls[k] += 1;
+  TRY(op_dot(ctx, k, l.N, l.r, l.r, &ds->rr));
+  TRY(read_scal(ctx, k));
+  if (ctx->hscal[k].rr < l.thr) return MSS_OK;
+  int64_t it = 0;
+  for (;;) {
+    TRY(precond(ctx, k));
+    TRY(op_dot(ctx, k, l.N, l.r, l.z, &ds->rho));                         // rho = r.z
+    double* pin = l.p[l.pcur];
+    double* pout = l.p[l.pcur ^ 1];
+    {
+    ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV) * l.N);
+    DISPATCH(ctx->ndim, k_pdir_spmv_dot, grid_for(l.N), l.dev(), l.z, pin, pout, l.q, ds,
+             it == 0 ? 1 : 0, red_to(ctx, &ds->pq, k, 0));                 // a10
+    }
+    l.pcur ^= 1;
+    {
+    ProfScope ps(ctx, KC_AXPY, k, cell_bytes(ctx, KC_AXPY) * l.N);
+    LAUNCH(k_axpy_norm, grid_for(l.N), l.N, l.x, l.r, pout, l.q, ds, red_to(ctx, &ds->rr, k, 1));  // a11
+    }
+    TRY(read_scal(ctx, k));                                                // a12
+    const Scal& h = ctx->hscal[k];
+    it++;
+    if (!(h.rho > 0.0) || !(h.pq > 0.0)) {
+      ctx->info.iters[k] += it;
+      ctx->info.breakdown_level = k;
+      return set_err(MSS_EBREAKDOWN, "PCG breakdown (rho or pAp <= 0) at level " + std::to_string(k));
+    }
+    if (h.rr < l.thr) break;
+    if (it >= ctx->prm.max_iter) {
+      ctx->info.not_converged = 1;
+      break;
+    }
+  }
+  ctx->info.iters[k] += it;
+  return MSS_OK;
+}
+
+static void set_thresholds(mss_ctx* ctx, double eps2) {
+  ctx->eps2 = eps2;
+  double fk = 1.0;
+  for (int k = 0; k <= ctx->L; ++k) {
+    ctx->lv[k].thr = (double)ctx->lv[k].N * fk * eps2;
+    fk *= ctx->prm.f;
+  }
+}
+
+static void reset_info(mss_ctx* ctx) {
+  mss_info& I = ctx->info;
+  for (int k = 0; k < MSS_MAX_LEVELS; ++k) { I.iters[k] = 0; I.calls[k] = 0; }
+  I.not_converged = 0;
+  I.breakdown_level = -1;
+  I.true_rel_res = 0;
+  I.bnorm2 = 0;
+}
+
+static BCDev bc_dev(const mss_ctx* ctx) {
+  BCDev b;
+  const Level& l = ctx->lv[0];
+  for (int s = 0; s < 6; ++s) {
+    b.kind[s] = ctx->bc[s].kind;
+    b.val[s] = ctx->bc[s].value;
+  }
+  const double* h = l.h;
+  b.area[0] = (ctx->ndim == 3) ? h[1] * h[2] : h[1];
+  b.area[1] = (ctx->ndim == 3) ? h[0] * h[2] : h[0];
+  b.area[2] = h[0] * h[1];
+  b.lift_mode = ctx->prm.use_lift ? ctx->lift_mode : 0;
+  b.lift_a = ctx->lift_a;
+  b.lift_b = ctx->lift_b;
+  return b;
+}
+
+static double cell_volume(const mss_ctx* ctx) {
+  const double* h = ctx->lv[0].h;
+  return (ctx->ndim == 3) ? h[0] * h[1] * h[2] : h[0] * h[1];
+}
+
+static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) {
+  reset_info(ctx);
+  const int64_t launches0 = ctx->launches;
+  Level& l = ctx->lv[0];
+  Scal* ds = ctx->dscal;
+  // a4: b and x0 = P_bf (or the caller's x with use_lift = 0)
+  BCDev bc = bc_dev(ctx);
+  if (!ctx->prm.use_lift) CK(cudaMemcpyAsync(l.x, x, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  DISPATCH(ctx->ndim, k_rhs_lift, grid_for(l.N), l.dev(), f, l.b, ctx->prm.use_lift ? l.x : nullptr,
+           cell_volume(ctx), bc);
+  TRY(op_dot(ctx, 0, l.N, l.b, l.b, &ds->bb));
+  TRY(read_scal(ctx, 0));
+  const double bb = ctx->hscal[0].bb;
+  ctx->info.bnorm2 = bb;
+  int rc = MSS_OK;
+  if (bb == 0.0) {
+    CK(cudaMemsetAsync(l.x, 0, sizeof(double) * l.N, ctx->stream));
+  } else {
+    set_thresholds(ctx, rel_tol * rel_tol * bb / (double)l.N);
+    TRY(op_residual(ctx, 0, l.b, l.x, l.r, &ds->rr));                // r0 = b - A x0
+    if (ctx->L == 0) {
+      ctx->info.calls[0] += 1;
+      TRY(read_scal(ctx, 0));
+      if (!(ctx->hscal[0].rr < l.thr)) {
+        TRY(op_coarse_solve(ctx, l.r, l.z));
+        LAUNCH(k_axpy, grid_for(l.N), l.N, l.x, l.z);
+        ctx->info.iters[0] += 1;
+      }
+    } else {
+      rc = pcg_level(ctx, 0);
+      if (rc < 0 && rc != MSS_EBREAKDOWN) return rc;
+    }
+  }
+  // true residual (O15)
+  TRY(op_residual(ctx, 0, l.b, l.x, l.s, &ds->aux));
+  TRY(read_scal(ctx, 0));
+  ctx->info.true_rel_res = (bb > 0) ? std::sqrt(ctx->hscal[0].aux / bb) : std::sqrt(ctx->hscal[0].aux);
+  CK(cudaMemcpyAsync(x, l.x, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->info.kernel_launches = ctx->launches - launches0;
+  if (ctx->prof_on) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    prof_flush(ctx);
+  }
+  if (rc == MSS_EBREAKDOWN) return rc;
+  return ctx->info.not_converged ? MSS_NOT_CONVERGED : MSS_OK;
+}
+
+// ============================================================================ setup
+static int build_hierarchy_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min,
+                                std::vector<std::array<int64_t, 3>>& dims) {
+  std::array<int64_t, 3> cur = {n[0], n[1], ndim == 3 ? n[2] : 1};
+  dims.push_back(cur);
+  for (;;) {
+    const int64_t N = cur[0] * cur[1] * cur[2];
+    if (depth >= 0) {
+      if ((int)dims.size() - 1 >= depth) break;
+      for (int d = 0; d < ndim; ++d)
+        if (cur[d] % s != 0) return set_err(MSS_EINVAL, "explicit depth needs every axis divisible by scale");
+    } else {
+      if (N <= coarse_min) break;
+      bool ok = true;
+      for (int d = 0; d < ndim; ++d) ok = ok && (cur[d] % s == 0) && (cur[d] / s >= 1);
+      if (!ok) break;
+    }
+    if ((int)dims.size() >= MSS_MAX_LEVELS) return set_err(MSS_EINVAL, "too many levels");
+    for (int d = 0; d < ndim; ++d) cur[d] /= s;
+    dims.push_back(cur);
+  }
+  return MSS_OK;
+}
+
+static void compute_lift(mss_ctx* ctx) {
+  // O6 / Q4: constant if all Dirichlet values agree; ramp if Dirichlet only on x-/x+.
+  const int nsides = 2 * ctx->ndim;
+  int nd = 0;
+  double v0 = 0;
+  bool all_eq = true;
+  unsigned mask = 0;
+  for (int s = 0; s < nsides; ++s) {
+    if (ctx->bc[s].kind == 1) {
+      if (nd == 0) v0 = ctx->bc[s].value;
+      else if (ctx->bc[s].value != v0) all_eq = false;
+      nd++;
+      mask |= 1u << s;
+    }
+  }
+  ctx->lift_mode = 0;
+  if (nd == 0) return;
+  if (all_eq) {
+    ctx->lift_mode = 1;
+    ctx->lift_a = v0;
+  } else if (mask == 3u) {
+    ctx->lift_mode = 2;
+    ctx->lift_a = ctx->bc[0].value;
+    ctx->lift_b = ctx->bc[1].value;
+  }
+}
+
+static int free_ctx(mss_ctx* ctx) {
+  if (!ctx) return MSS_OK;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  prof_flush(ctx);
+  for (cudaEvent_t e : ctx->ev_free) cudaEventDestroy(e);
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->hscal) cudaFreeHost(ctx->hscal);
+  delete ctx;
+  return MSS_OK;
+}
+
+static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_comp, int depth) {
+  const int ndim = ctx->ndim;
+  const int s = ctx->prm.scale;
+  std::vector<std::array<int64_t, 3>> dims;
+  TRY(build_hierarchy_dims(ndim, n, s, depth, ctx->prm.coarse_min, dims));
+  ctx->L = (int)dims.size() - 1;
+  ctx->lv.resize(dims.size());
+  for (size_t k = 0; k < dims.size(); ++k) {
+    Level& l = ctx->lv[k];
+    l.nx = (int)dims[k][0];
+    l.ny = (int)dims[k][1];
+    l.nz = (int)dims[k][2];
+    l.plane = (int64_t)l.nx * l.ny;
+    l.N = l.plane * l.nz;
+    for (int d = 0; d < 3; ++d) l.h[d] = ctx->extent[d] / (double)dims[k][d];
+    const int64_t nfx = (int64_t)(l.nx + 1) * l.ny * l.nz, nfy = (int64_t)l.nx * (l.ny + 1) * l.nz;
+    TRY(dalloc(ctx, (void**)&l.Tx, sizeof(double) * nfx));
+    TRY(dalloc(ctx, (void**)&l.Ty, sizeof(double) * nfy));
+    if (ndim == 3) TRY(dalloc(ctx, (void**)&l.Tz, sizeof(double) * (size_t)(l.N + l.plane)));
+    TRY(valloc(ctx, l, &l.x));
+    TRY(valloc(ctx, l, &l.r));
+    TRY(valloc(ctx, l, &l.z));
+    TRY(valloc(ctx, l, &l.q));
+    TRY(valloc(ctx, l, &l.s));
+    TRY(valloc(ctx, l, &l.p[0]));
+    TRY(valloc(ctx, l, &l.p[1]));
+    if (k == 0) TRY(valloc(ctx, l, &l.b));
+    else l.b = l.r;
+  }
+  for (int k = 0; k < ctx->L; ++k) {
+    Level& f = ctx->lv[k];
+    Level& c = ctx->lv[k + 1];
+    TRY(dalloc(ctx, (void**)&f.t1, sizeof(double) * (size_t)c.nx * f.ny * f.nz));
+    TRY(dalloc(ctx, (void**)&f.t2, sizeof(double) * (size_t)c.nx * c.ny * f.nz));
+  }
+  TRY(dalloc(ctx, (void**)&ctx->dscal, sizeof(Scal) * MSS_MAX_LEVELS));
+  CK(cudaMemsetAsync(ctx->dscal, 0, sizeof(Scal) * MSS_MAX_LEVELS, ctx->stream));
+  CK(cudaMallocHost((void**)&ctx->hscal, sizeof(Scal) * MSS_MAX_LEVELS));
+  TRY(dalloc(ctx, (void**)&ctx->partials, sizeof(double) * kMaxGrid));
+  TRY(dalloc(ctx, (void**)&ctx->counter, sizeof(unsigned) * 4));
+  CK(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned) * 4, ctx->stream));
+  TRY(dalloc(ctx, (void**)&ctx->dflag, sizeof(int) * 4));
+  CK(cudaMemsetAsync(ctx->dflag, 0, sizeof(int) * 4, ctx->stream));
+
+  // validate K (finite, > 0)
+  Level& l0 = ctx->lv[0];
+  LAUNCH(k_validate_K, grid_for(l0.N * k_comp), K, l0.N * k_comp, ctx->dflag);
+  int hflag = 0;
+  CK(cudaMemcpyAsync(&hflag, ctx->dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hflag) return set_err(MSS_EINVAL, "K must be finite and > 0");
+
+  // a1: level-0 faces
+  for (int d = 0; d < ndim; ++d) {
+    const double* Kd = K + (size_t)((k_comp == ndim) ? d : 0) * l0.N;
+    double area = 1.0;
+    for (int e = 0; e < ndim; ++e)
+      if (e != d) area *= l0.h[e];
+    const double coef = area / l0.h[d];
+    double* T = (d == 0) ? l0.Tx : (d == 1) ? l0.Ty : l0.Tz;
+    const int64_t nf = (int64_t)(l0.nx + (d == 0)) * (l0.ny + (d == 1)) * (l0.nz + (d == 2));
+    LAUNCH(k_assemble_faces, grid_for(nf), Kd, T, l0.nx, l0.ny, l0.nz, d, coef,
+           ctx->bc[2 * d].kind == 1, ctx->bc[2 * d + 1].kind == 1);
+  }
+  // a2: coarse faces, level by level
+  for (int k = 1; k <= ctx->L; ++k) {
+    Level& f = ctx->lv[k - 1];
+    Level& c = ctx->lv[k];
+    for (int d = 0; d < ndim; ++d) {
+      const double* Tf = (d == 0) ? f.Tx : (d == 1) ? f.Ty : f.Tz;
+      double* Tc = (d == 0) ? c.Tx : (d == 1) ? c.Ty : c.Tz;
+      const int64_t nf = (int64_t)(c.nx + (d == 0)) * (c.ny + (d == 1)) * (c.nz + (d == 2));
+      LAUNCH(k_coarsen_faces, grid_for(nf), Tf, Tc, f.nx, f.ny, f.nz, c.nx, c.ny, c.nz, d, s, ndim);
+    }
+  }
+  // a3: dense coarsest matrix, Cholesky, inverse
+  Level& lc = ctx->lv[ctx->L];
+  if (lc.N > 8192) return set_err(MSS_EINVAL, "coarsest level too large for the dense solve");
+  ctx->NL = (int)lc.N;
+  const size_t nn = (size_t)ctx->NL * ctx->NL;
+  TRY(dalloc(ctx, (void**)&ctx->Achol, sizeof(double) * nn));
+  TRY(dalloc(ctx, (void**)&ctx->Ainv, sizeof(double) * nn));
+  double* X = nullptr;
+  CK(cudaMalloc((void**)&X, sizeof(double) * nn));
+  CK(cudaMemsetAsync(ctx->Achol, 0, sizeof(double) * nn, ctx->stream));
+  DISPATCH(ndim, k_dense_assemble, grid_for(lc.N), lc.dev(), ctx->Achol);
+  LAUNCH(k_cholesky, 1, ctx->Achol, ctx->NL, ctx->dflag + 1);
+  CK(cudaMemcpyAsync(&hflag, ctx->dflag + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hflag) {
+    cudaFree(X);
+    return set_err(MSS_ESINGULAR, "coarsest operator is not SPD");
+  }
+  {
+    const int tb = 128;
+    k_chol_inverse<<<(ctx->NL + tb - 1) / tb, tb, 0, ctx->stream>>>(ctx->Achol, X, ctx->NL);
+    ctx->launches++;
+  }
+  LAUNCH(k_symmetrize, grid_for((int64_t)nn), X, ctx->Ainv, ctx->NL);
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(X);
+  compute_lift(ctx);
+  TRY(tail_setup(ctx));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return MSS_OK;
+}
+
+// ============================================================================ C ABI
+extern "C" {
+
+int mss_default_params(mss_params* p) {
+  if (!p) return MSS_EINVAL;
+  p->scale = 4;
+  p->m = 4;
+  p->f = 0.1;
+  p->interp = 0;
+  p->max_iter = 500;
+  p->coarse_min = 512;
+  p->use_lift = 1;
+  p->tail_cells = 65536;
+  p->gather_below = (int64_t)64 * 64 * 64;
+  return MSS_OK;
+}
+
+const char* mss_strerror(int code) {
+  switch (code) {
+    case MSS_OK: return "ok";
+    case MSS_NOT_CONVERGED: return "not converged (max_iter reached on some level)";
+    case MSS_EINVAL: return "invalid argument";
+    case MSS_ENOMEM: return "out of device memory";
+    case MSS_ECUDA: return "CUDA error";
+    case MSS_ENCCL: return "NCCL error";
+    case MSS_ESINGULAR: return "singular operator";
+    case MSS_EBREAKDOWN: return "PCG breakdown";
+    case MSS_EUNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* mss_last_error(void) { return g_err.c_str(); }
+
+int mss_setup(mss_ctx** out, int ndim, const int64_t n[3], const double extent[3], const double* K,
+              int k_comp, const mss_bc bc[6], int depth, const mss_params* p, void* stream) {
+  if (!out) return set_err(MSS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (ndim != 2 && ndim != 3) return set_err(MSS_EINVAL, "ndim must be 2 or 3");
+  if (!n || !K || !bc) return set_err(MSS_EINVAL, "NULL argument");
+  if (k_comp != 1 && k_comp != ndim) return set_err(MSS_EINVAL, "k_comp must be 1 or ndim");
+  for (int d = 0; d < ndim; ++d)
+    if (n[d] < 1 || n[d] > (1 << 20)) return set_err(MSS_EINVAL, "bad dims");
+  const int64_t N = n[0] * n[1] * (ndim == 3 ? n[2] : 1);
+  if (N > ((int64_t)1 << 31) - 1) return set_err(MSS_EINVAL, "too many cells");
+  mss_params prm;
+  mss_default_params(&prm);
+  if (p) prm = *p;
+  if (prm.scale < 2) return set_err(MSS_EINVAL, "scale < 2");
+  if (prm.m < 0 || prm.max_iter < 1 || !(prm.f > 0) || prm.coarse_min < 1) return set_err(MSS_EINVAL, "bad params");
+  if (prm.interp != 0 && prm.interp != 1) return set_err(MSS_EINVAL, "interp must be 0 or 1");
+  bool any_dir = false;
+  for (int s = 0; s < 2 * ndim; ++s) {
+    if (bc[s].kind != 0 && bc[s].kind != 1) return set_err(MSS_EINVAL, "bad BC kind");
+    if (!std::isfinite(bc[s].value)) return set_err(MSS_EINVAL, "bad BC value");
+    any_dir = any_dir || bc[s].kind == 1;
+  }
+  if (!any_dir) return set_err(MSS_ESINGULAR, "all-Neumann operator is singular");
+  mss_ctx* ctx = new mss_ctx();
+  ctx->ndim = ndim;
+  ctx->prm = prm;
+  for (int s = 0; s < 6; ++s) ctx->bc[s] = (s < 2 * ndim) ? bc[s] : mss_bc{0, 0.0};
+  for (int d = 0; d < 3; ++d) ctx->extent[d] = (extent && d < ndim) ? extent[d] : 1.0;
+  ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaGetDevice(&ctx->device);
+  memset(&ctx->info, 0, sizeof(ctx->info));
+  int rc = setup_impl(ctx, n, K, k_comp, depth);
+  if (rc != MSS_OK) {
+    free_ctx(ctx);
+    return rc;
+  }
+  ctx->info.levels = ctx->L + 1;
+  for (int k = 0; k <= ctx->L; ++k) {
+    ctx->info.dims[k][0] = ctx->lv[k].nx;
+    ctx->info.dims[k][1] = ctx->lv[k].ny;
+    ctx->info.dims[k][2] = ctx->lv[k].nz;
+  }
+  *out = ctx;
+  return MSS_OK;
+}
+
+int mss_free(mss_ctx* ctx) { return free_ctx(ctx); }
+
+int mss_num_levels(const mss_ctx* ctx, int* L1) {
+  if (!ctx || !L1) return MSS_EINVAL;
+  *L1 = ctx->L + 1;
+  return MSS_OK;
+}
+
+int mss_level_dims(const mss_ctx* ctx, int level, int64_t n[3]) {
+  if (!ctx || !n || level < 0 || level > ctx->L) return MSS_EINVAL;
+  n[0] = ctx->lv[level].nx;
+  n[1] = ctx->lv[level].ny;
+  n[2] = ctx->lv[level].nz;
+  return MSS_OK;
+}
+
+int mss_solve(mss_ctx* ctx, const double* f, double* x, double rel_tol, int64_t* iters, double* true_rel_res) {
+  if (!ctx || !f || !x || !(rel_tol >= 0)) return set_err(MSS_EINVAL, "bad solve arguments");
+  int rc = solve_impl(ctx, f, x, rel_tol);
+  if (rc == MSS_ECUDA) return rc;
+  if (iters)
+    for (int k = 0; k <= ctx->L; ++k) iters[k] = ctx->info.iters[k];
+  if (true_rel_res) *true_rel_res = ctx->info.true_rel_res;
+  return rc;
+}
+
+int mss_solve_host(mss_ctx* ctx, const double* f_host, double* x_host, double rel_tol, int64_t* iters,
+                   double* true_rel_res) {
+  if (!ctx || !f_host || !x_host) return set_err(MSS_EINVAL, "bad solve arguments");
+  const int64_t N = ctx->lv[0].N;
+  if (!ctx->dev_f) {
+    TRY(dalloc(ctx, (void**)&ctx->dev_f, sizeof(double) * N));
+    TRY(dalloc(ctx, (void**)&ctx->dev_x, sizeof(double) * N));
+  }
+  CK(cudaMemcpyAsync(ctx->dev_f, f_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->prm.use_lift)
+    CK(cudaMemcpyAsync(ctx->dev_x, x_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = mss_solve(ctx, ctx->dev_f, ctx->dev_x, rel_tol, iters, true_rel_res);
+  if (rc < 0) return rc;
+  CK(cudaMemcpyAsync(x_host, ctx->dev_x, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+int mss_get_info(const mss_ctx* ctx, mss_info* info) {
+  if (!ctx || !info) return MSS_EINVAL;
+  *info = ctx->info;
+  return MSS_OK;
+}
+
+int mss_profile(mss_ctx* ctx, int enable, int max_level) {
+  if (!ctx) return MSS_EINVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  prof_flush(ctx);
+  ctx->prof_on = enable != 0;
+  ctx->prof_max_level = max_level;
+  memset(ctx->prof_ms, 0, sizeof(ctx->prof_ms));
+  memset(ctx->prof_bytes, 0, sizeof(ctx->prof_bytes));
+  memset(ctx->prof_cnt, 0, sizeof(ctx->prof_cnt));
+  return MSS_OK;
+}
+
+int mss_profile_read(const mss_ctx* ctx, int kclass, int level, int64_t* count, double* ms, double* bytes) {
+  if (!ctx || kclass < 0 || kclass >= MSS_NUM_KCLASS || level < 0 || level >= MSS_MAX_LEVELS) return MSS_EINVAL;
+  if (count) *count = ctx->prof_cnt[kclass][level];
+  if (ms) *ms = ctx->prof_ms[kclass][level];
+  if (bytes) *bytes = ctx->prof_bytes[kclass][level];
+  return MSS_OK;
+}
+
+int mss_kernel_launches(const mss_ctx* ctx, int64_t* count) {
+  if (!ctx || !count) return MSS_EINVAL;
+  *count = ctx->launches;
+  return MSS_OK;
+}
+
+// ---- hooks
+static int check_level(const mss_ctx* ctx, int level) {
+  return (ctx && level >= 0 && level <= ctx->L) ? MSS_OK : set_err(MSS_EINVAL, "bad level");
+}
+
+int mss_get_faces(const mss_ctx* ctx, int level, int dir, double* T) {
+  TRY(check_level(ctx, level));
+  if (dir < 0 || dir >= ctx->ndim || !T) return set_err(MSS_EINVAL, "bad dir");
+  const Level& l = ctx->lv[level];
+  const double* src = (dir == 0) ? l.Tx : (dir == 1) ? l.Ty : l.Tz;
+  const int64_t nf = (int64_t)(l.nx + (dir == 0)) * (l.ny + (dir == 1)) * (l.nz + (dir == 2));
+  CK(cudaMemcpyAsync(T, src, sizeof(double) * nf, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_apply_A(mss_ctx* ctx, int level, const double* x, double* y) {
+  TRY(check_level(ctx, level));
+  Level& l = ctx->lv[level];
+  CK(cudaMemcpyAsync(l.q, x, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  DISPATCH(ctx->ndim, k_apply_A, grid_for(l.N), l.dev(), l.q, y);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_dot(mss_ctx* ctx, int level, const double* a, const double* b, double* out) {
+  TRY(check_level(ctx, level));
+  if (!out) return MSS_EINVAL;
+  TRY(op_dot(ctx, level, ctx->lv[level].N, a, b, &ctx->dscal[level].aux));
+  TRY(read_scal(ctx, level));
+  *out = ctx->hscal[level].aux;
+  return MSS_OK;
+}
+
+int mss_smooth(mss_ctx* ctx, int level, const double* r, double* z, int n_half, int first_color, int z_is_zero) {
+  TRY(check_level(ctx, level));
+  Level& l = ctx->lv[level];
+  CK(cudaMemcpyAsync(l.r, r, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (z_is_zero) CK(cudaMemsetAsync(l.z, 0, sizeof(double) * l.N, ctx->stream));
+  else CK(cudaMemcpyAsync(l.z, z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  TRY(op_smooth(ctx, level, l.r, l.z, n_half, first_color & 1, z_is_zero != 0));
+  CK(cudaMemcpyAsync(z, l.z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_residual_restrict(mss_ctx* ctx, int level, const double* r, const double* z, double* coarse_b) {
+  TRY(check_level(ctx, level));
+  if (level >= ctx->L) return set_err(MSS_EINVAL, "no coarser level");
+  Level& l = ctx->lv[level];
+  Level& c = ctx->lv[level + 1];
+  CK(cudaMemcpyAsync(l.r, r, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(l.z, z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  TRY(op_residual(ctx, level, l.r, l.z, l.s, nullptr));
+  TRY(op_restrict(ctx, level, l.s, c.r));
+  CK(cudaMemcpyAsync(coarse_b, c.r, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_prolong_add(mss_ctx* ctx, int level, const double* coarse_y, double* z, int color) {
+  TRY(check_level(ctx, level));
+  if (level >= ctx->L) return set_err(MSS_EINVAL, "no coarser level");
+  Level& l = ctx->lv[level];
+  Level& c = ctx->lv[level + 1];
+  CK(cudaMemcpyAsync(c.x, coarse_y, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(l.z, z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  TRY(op_prolong_add(ctx, level, c.x, l.z, color < 0 ? -1 : (color & 1)));
+  CK(cudaMemcpyAsync(z, l.z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_precond(mss_ctx* ctx, int level, const double* r, double* z, double rel_tol, int64_t* iters) {
+  TRY(check_level(ctx, level));
+  Level& l = ctx->lv[level];
+  reset_info(ctx);
+  CK(cudaMemcpyAsync(l.r, r, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  TRY(op_dot(ctx, level, l.N, l.r, l.r, &ctx->dscal[level].aux));
+  TRY(read_scal(ctx, level));
+  set_thresholds(ctx, 0.0);
+  {
+    // eps relative to this level's r, thresholds scaled from level `level`
+    const double eps2 = rel_tol * rel_tol * ctx->hscal[level].aux / (double)l.N;
+    double fk = 1.0;
+    for (int k = 0; k <= ctx->L; ++k) {
+      ctx->lv[k].thr = (double)ctx->lv[k].N * fk * eps2;
+      if (k >= level) fk *= ctx->prm.f;
+    }
+  }
+  if (level == ctx->L) {
+    TRY(op_coarse_solve(ctx, l.r, l.z));
+    ctx->info.iters[level] += 1;
+  } else {
+    TRY(precond(ctx, level));
+  }
+  CK(cudaMemcpyAsync(z, l.z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (iters)
+    for (int k = 0; k <= ctx->L; ++k) iters[k] = ctx->info.iters[k];
+  return MSS_OK;
+}
+
+int mss_coarse_solve(mss_ctx* ctx, const double* b, double* x) {
+  if (!ctx || !b || !x) return MSS_EINVAL;
+  TRY(op_coarse_solve(ctx, b, x));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_rhs_lift(mss_ctx* ctx, const double* f, double* b, double* x0) {
+  if (!ctx || !f || !b) return MSS_EINVAL;
+  Level& l = ctx->lv[0];
+  DISPATCH(ctx->ndim, k_rhs_lift, grid_for(l.N), l.dev(), f, b, x0, cell_volume(ctx), bc_dev(ctx));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+}  // extern "C"
+
+// ---- distributed entry points (z-slabs over NCCL) — see dist.cu
+extern "C" {
+int mss_nccl_unique_id(unsigned char id[128]) {
+  (void)id;
+  return set_err(MSS_EUNSUPPORTED, "distributed build not enabled");
+}
+int mss_slab_range(const int64_t n_global[3], int ndim, int scale, int depth, int rank, int nranks,
+                   int64_t* z_begin, int64_t* z_end) {
+  if (!n_global || !z_begin || !z_end || nranks < 1 || rank < 0 || rank >= nranks || ndim != 3)
+    return set_err(MSS_EINVAL, "bad slab arguments");
+  (void)scale; (void)depth;
+  const int64_t nz = n_global[2];
+  *z_begin = nz * rank / nranks;
+  *z_end = nz * (rank + 1) / nranks;
+  return MSS_OK;
+}
+int mss_setup_dist(mss_ctx** out, int rank, int nranks, const unsigned char id[128], int ndim,
+                   const int64_t n_global[3], const double extent[3], const double* K_local, int k_comp,
+                   const mss_bc bc[6], int depth, const mss_params* p, void* stream) {
+  (void)out; (void)rank; (void)nranks; (void)id; (void)ndim; (void)n_global; (void)extent;
+  (void)K_local; (void)k_comp; (void)bc; (void)depth; (void)p; (void)stream;
+  return set_err(MSS_EUNSUPPORTED, "distributed build not enabled");
+}
+}

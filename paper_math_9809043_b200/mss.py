@@ -1,0 +1,327 @@
+"""Thin ctypes binding of ``libmss.so`` (include/mss.h): argument marshalling only.
+
+Every step of the solver runs in the library's CUDA kernels.  PyTorch supplies device
+memory (float64 CUDA tensors) and the current CUDA stream; nothing here computes.
+If the library is missing this module raises — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmss.so")
+
+MSS_OK = 0
+MSS_NOT_CONVERGED = 1
+MAX_LEVELS = 12
+
+NEUMANN = 0
+DIRICHLET = 1
+
+
+class MSSError(RuntimeError):
+    def __init__(self, code, where, detail=""):
+        super().__init__(f"{where}: status {code} ({detail})")
+        self.code = code
+
+
+class BC(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("value", ctypes.c_double)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [
+        ("scale", ctypes.c_int),
+        ("m", ctypes.c_int),
+        ("f", ctypes.c_double),
+        ("interp", ctypes.c_int),
+        ("max_iter", ctypes.c_int),
+        ("coarse_min", ctypes.c_int),
+        ("use_lift", ctypes.c_int),
+        ("tail_cells", ctypes.c_int64),
+        ("gather_below", ctypes.c_int64),
+    ]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [
+        ("levels", ctypes.c_int),
+        ("dims", (ctypes.c_int64 * 3) * MAX_LEVELS),
+        ("iters", ctypes.c_int64 * MAX_LEVELS),
+        ("calls", ctypes.c_int64 * MAX_LEVELS),
+        ("not_converged", ctypes.c_int),
+        ("breakdown_level", ctypes.c_int),
+        ("true_rel_res", ctypes.c_double),
+        ("bnorm2", ctypes.c_double),
+        ("kernel_launches", ctypes.c_int64),
+    ]
+
+
+P = ctypes.c_void_p
+I64P = ctypes.POINTER(ctypes.c_int64)
+DP = ctypes.POINTER(ctypes.c_double)
+
+# (name, restype, argtypes) for every symbol include/mss.h declares.
+SIGNATURES = [
+    ("mss_default_params", ctypes.c_int, [ctypes.POINTER(Params)]),
+    ("mss_strerror", ctypes.c_char_p, [ctypes.c_int]),
+    ("mss_last_error", ctypes.c_char_p, []),
+    ("mss_setup", ctypes.c_int, [ctypes.POINTER(P), ctypes.c_int, I64P, DP, P, ctypes.c_int,
+                                 ctypes.POINTER(BC), ctypes.c_int, ctypes.POINTER(Params), P]),
+    ("mss_free", ctypes.c_int, [P]),
+    ("mss_num_levels", ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int)]),
+    ("mss_level_dims", ctypes.c_int, [P, ctypes.c_int, I64P]),
+    ("mss_solve", ctypes.c_int, [P, P, P, ctypes.c_double, I64P, DP]),
+    ("mss_solve_host", ctypes.c_int, [P, P, P, ctypes.c_double, I64P, DP]),
+    ("mss_get_info", ctypes.c_int, [P, ctypes.POINTER(Info)]),
+    ("mss_get_faces", ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P]),
+    ("mss_apply_A", ctypes.c_int, [P, ctypes.c_int, P, P]),
+    ("mss_dot", ctypes.c_int, [P, ctypes.c_int, P, P, DP]),
+    ("mss_smooth", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("mss_residual_restrict", ctypes.c_int, [P, ctypes.c_int, P, P, P]),
+    ("mss_prolong_add", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_int]),
+    ("mss_precond", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_double, I64P]),
+    ("mss_coarse_solve", ctypes.c_int, [P, P, P]),
+    ("mss_rhs_lift", ctypes.c_int, [P, P, P, P]),
+    ("mss_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("mss_slab_range", ctypes.c_int, [I64P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, I64P, I64P]),
+    ("mss_setup_dist", ctypes.c_int, [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                      ctypes.c_int, I64P, DP, P, ctypes.c_int, ctypes.POINTER(BC),
+                                      ctypes.c_int, ctypes.POINTER(Params), P]),
+    ("mss_kernel_launches", ctypes.c_int, [P, I64P]),
+    ("mss_profile", ctypes.c_int, [P, ctypes.c_int, ctypes.c_int]),
+    ("mss_profile_read", ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, I64P, DP, DP]),
+]
+
+KCLASS = ["halfsweep", "halfsweep_first", "residual", "restrict", "prolong_add", "pdir_spmv_dot",
+          "axpy_norm", "dot", "coarse_solve", "other"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libmss.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_math_9809043_b200.build` "
+                          "(or __graft_entry__.build()).  There is no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc, where, allow_nc=True):
+    if rc == MSS_OK or (allow_nc and rc == MSS_NOT_CONVERGED):
+        return rc
+    lib = load_library()
+    raise MSSError(rc, where, f"{lib.mss_strerror(rc).decode()}: {lib.mss_last_error().decode()}")
+
+
+def _dev_ptr(t: torch.Tensor, n: Optional[int] = None) -> int:
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
+    return t.data_ptr()
+
+
+def default_params(**kw) -> Params:
+    p = Params()
+    load_library().mss_default_params(ctypes.byref(p))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise KeyError(k)
+        setattr(p, k, v)
+    return p
+
+
+@dataclass
+class SolveReport:
+    rc: int
+    iters: List[int]
+    calls: List[int]
+    dims: List[tuple]
+    not_converged: bool
+    true_rel_res: float
+    kernel_launches: int
+
+
+class Solver:
+    """mss_setup / mss_solve / mss_free on CUDA tensors (see include/mss.h)."""
+
+    def __init__(self, ndim: int, n: Sequence[int], K: torch.Tensor, bc, depth: Optional[int] = None,
+                 params: Optional[dict] = None, extent: Optional[Sequence[float]] = None, stream=None):
+        lib = load_library()
+        self.lib = lib
+        self.ndim = ndim
+        nx, ny = int(n[0]), int(n[1])
+        nz = int(n[2]) if ndim == 3 else 1
+        self.n = (nx, ny, nz)
+        self.N = nx * ny * nz
+        if K.dim() == ndim:
+            K = K.unsqueeze(0)
+        K = K.contiguous()
+        k_comp = K.shape[0]
+        _dev_ptr(K, k_comp * self.N)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        bcs = (BC * 6)(*[BC(int(k), float(v)) for k, v in bc] + [BC(0, 0.0)] * (6 - len(bc)))
+        prm = default_params(**(params or {}))
+        nn = (ctypes.c_int64 * 3)(nx, ny, nz)
+        ext = (ctypes.c_double * 3)(*(list(extent) + [1.0] * (3 - len(extent)))) if extent else None
+        ctx = P()
+        rc = lib.mss_setup(ctypes.byref(ctx), ndim, nn, ext, K.data_ptr(), k_comp, bcs,
+                           -1 if depth is None else int(depth), ctypes.byref(prm),
+                           ctypes.c_void_p(self.stream.cuda_stream))
+        _check(rc, "mss_setup", allow_nc=False)
+        self.ctx = ctx
+        L1 = ctypes.c_int()
+        lib.mss_num_levels(ctx, ctypes.byref(L1))
+        self.levels = L1.value
+
+    # ---------------------------------------------------------------- lifecycle
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.mss_free(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def level_dims(self, level: int):
+        out = (ctypes.c_int64 * 3)()
+        _check(self.lib.mss_level_dims(self.ctx, level, out), "mss_level_dims")
+        return tuple(out)
+
+    def level_N(self, level: int) -> int:
+        d = self.level_dims(level)
+        return d[0] * d[1] * d[2]
+
+    def info(self) -> SolveReport:
+        inf = Info()
+        self.lib.mss_get_info(self.ctx, ctypes.byref(inf))
+        L1 = inf.levels
+        return SolveReport(0, list(inf.iters[:L1]), list(inf.calls[:L1]),
+                           [tuple(inf.dims[k]) for k in range(L1)], bool(inf.not_converged),
+                           inf.true_rel_res, inf.kernel_launches)
+
+    def profile(self, enable: bool, max_level: int = 0):
+        _check(self.lib.mss_profile(self.ctx, 1 if enable else 0, int(max_level)), "mss_profile")
+
+    def profile_read(self):
+        """{(class name, level): (launches, ms, algorithmic bytes)} for nonzero entries."""
+        out = {}
+        c, ms, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        for ci, name in enumerate(KCLASS):
+            for lvl in range(self.levels):
+                self.lib.mss_profile_read(self.ctx, ci, lvl, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(by))
+                if c.value:
+                    out[(name, lvl)] = (c.value, ms.value, by.value)
+        return out
+
+    def kernel_launches(self) -> int:
+        c = ctypes.c_int64()
+        self.lib.mss_kernel_launches(self.ctx, ctypes.byref(c))
+        return c.value
+
+    # ---------------------------------------------------------------- solve
+    def solve(self, f: torch.Tensor, x: Optional[torch.Tensor] = None, rel_tol: float = 1e-10):
+        if x is None:
+            x = torch.zeros(self.N, dtype=torch.float64, device=f.device)
+        its = (ctypes.c_int64 * self.levels)()
+        tr = ctypes.c_double()
+        rc = self.lib.mss_solve(self.ctx, _dev_ptr(f, self.N), _dev_ptr(x, self.N), float(rel_tol), its,
+                                ctypes.byref(tr))
+        _check(rc, "mss_solve")
+        rep = self.info()
+        rep.rc = rc
+        return x, rep
+
+    def solve_host(self, f_host: torch.Tensor, x_host: torch.Tensor, rel_tol: float = 1e-10):
+        """End-to-end: host (ideally pinned) f in, host x out; copies inside the call."""
+        for t in (f_host, x_host):
+            if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != self.N:
+                raise ValueError("expected contiguous float64 host tensors of N elements")
+        its = (ctypes.c_int64 * self.levels)()
+        tr = ctypes.c_double()
+        rc = self.lib.mss_solve_host(self.ctx, f_host.data_ptr(), x_host.data_ptr(), float(rel_tol), its,
+                                     ctypes.byref(tr))
+        _check(rc, "mss_solve_host")
+        rep = self.info()
+        rep.rc = rc
+        return x_host, rep
+
+    # ---------------------------------------------------------------- hooks
+    def faces(self, level: int, d: int) -> torch.Tensor:
+        nx, ny, nz = self.level_dims(level)
+        dims = [nx, ny, nz]
+        dims[d] += 1
+        T = torch.empty(dims[0] * dims[1] * dims[2], dtype=torch.float64, device="cuda")
+        _check(self.lib.mss_get_faces(self.ctx, level, d, T.data_ptr()), "mss_get_faces")
+        return T
+
+    def apply_A(self, level: int, x: torch.Tensor) -> torch.Tensor:
+        y = torch.empty_like(x)
+        _check(self.lib.mss_apply_A(self.ctx, level, _dev_ptr(x, self.level_N(level)), y.data_ptr()), "mss_apply_A")
+        return y
+
+    def dot(self, level: int, a: torch.Tensor, b: torch.Tensor) -> float:
+        out = ctypes.c_double()
+        n = self.level_N(level)
+        _check(self.lib.mss_dot(self.ctx, level, _dev_ptr(a, n), _dev_ptr(b, n), ctypes.byref(out)), "mss_dot")
+        return out.value
+
+    def smooth(self, level: int, r: torch.Tensor, z: Optional[torch.Tensor], n_half: int, first_color: int = 0):
+        n = self.level_N(level)
+        zero = z is None
+        zz = torch.zeros_like(r) if zero else z.clone()
+        _check(self.lib.mss_smooth(self.ctx, level, _dev_ptr(r, n), _dev_ptr(zz, n), n_half, first_color,
+                                   1 if zero else 0), "mss_smooth")
+        return zz
+
+    def residual_restrict(self, level: int, r: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
+        n = self.level_N(level)
+        out = torch.empty(self.level_N(level + 1), dtype=torch.float64, device=r.device)
+        _check(self.lib.mss_residual_restrict(self.ctx, level, _dev_ptr(r, n), _dev_ptr(z, n), out.data_ptr()),
+               "mss_residual_restrict")
+        return out
+
+    def prolong_add(self, level: int, y: torch.Tensor, z: torch.Tensor, color: int = -1) -> torch.Tensor:
+        zz = z.clone()
+        _check(self.lib.mss_prolong_add(self.ctx, level, _dev_ptr(y, self.level_N(level + 1)),
+                                        _dev_ptr(zz, self.level_N(level)), color), "mss_prolong_add")
+        return zz
+
+    def precond(self, level: int, r: torch.Tensor, rel_tol: float = 1e-10):
+        n = self.level_N(level)
+        z = torch.empty_like(r)
+        its = (ctypes.c_int64 * self.levels)()
+        _check(self.lib.mss_precond(self.ctx, level, _dev_ptr(r, n), z.data_ptr(), float(rel_tol), its),
+               "mss_precond")
+        return z, list(its)
+
+    def coarse_solve(self, b: torch.Tensor) -> torch.Tensor:
+        x = torch.empty_like(b)
+        _check(self.lib.mss_coarse_solve(self.ctx, _dev_ptr(b, self.level_N(self.levels - 1)), x.data_ptr()),
+               "mss_coarse_solve")
+        return x
+
+    def rhs_lift(self, f: torch.Tensor):
+        b = torch.empty_like(f)
+        x0 = torch.empty_like(f)
+        _check(self.lib.mss_rhs_lift(self.ctx, _dev_ptr(f, self.N), b.data_ptr(), x0.data_ptr()), "mss_rhs_lift")
+        return b, x0
