@@ -113,6 +113,13 @@ struct mss_ctx {
   double prof_ms[MSS_NUM_KCLASS][MSS_MAX_LEVELS] = {};
   double prof_bytes[MSS_NUM_KCLASS][MSS_MAX_LEVELS] = {};
   int64_t prof_cnt[MSS_NUM_KCLASS][MSS_MAX_LEVELS] = {};
+  // device-resident coarse levels (tail.cuh)
+  int tail_cs = 0;                         // cluster size, 0 = tail unavailable
+  void* tail_d = nullptr;                  // device TailArgs
+  std::vector<char> tail_h;                // host image of TailArgs
+  long long* tail_cnt = nullptr;           // [2 * MSS_MAX_LEVELS] iters, calls
+  int* tail_flags = nullptr;               // [0] not converged, [1] breakdown level + 1
+  bool tail_dirty = true;
   // distributed (rank/nranks == 0/1 single GPU)
   int rank = 0, nranks = 1;
 };

@@ -337,19 +337,143 @@ __global__ void k_rhs_lift(LevelDev L, const double* __restrict__ f, double* __r
   }
 }
 
-// ------------------------------------------------------------------ operator (K08 part) & residual
+// ------------------------------------------------------------------ per-item bodies
+// Each body processes one work item; the grid kernels below and the cluster-resident
+// tail kernel (tail.cuh) share them, so both paths do identical per-cell arithmetic.
+
+// (A x)_c = diag_c x_c - sum_f T_f x_nbr (O4).  Returns b_c - (A x)_c and stores it.
+template <int NDIM>
+__device__ __forceinline__ double residual_item(const LevelDev& L, int64_t c, const double* __restrict__ b,
+                                                const double* __restrict__ x, double* __restrict__ r) {
+  const Cell e = cell_of(L, c);
+  double t[6];
+  load_faces<NDIM>(L, e, t);
+  const double ax = diag_of<NDIM>(t) * x[c] - nbr_sum<NDIM>(L, e, t, [&](int64_t q) { return x[q]; });
+  const double rv = (b ? b[c] : 0.0) - ax;
+  r[c] = rv;
+  return rv;
+}
+
+// a5/a9 half-sweep item t of colour `colour`: row = t / hx, i = 2 (t % hx) + parity.
+// z_c = (r_c + sum_f T_f z_nbr) / diag_c  (FIRST: z = 0 on entry, z_c = r_c / diag_c).
+template <int NDIM, bool FIRST>
+__device__ __forceinline__ void sweep_item(const LevelDev& L, uint32_t hx, uint32_t t, const double* __restrict__ r,
+                                           double* __restrict__ z, int colour) {
+  const uint32_t row = t / hx;
+  const uint32_t m = t - row * hx;
+  const uint32_t k = row / (uint32_t)L.ny;
+  const uint32_t j = row - k * (uint32_t)L.ny;
+  const int i = 2 * (int)m + (int)((j + k + (uint32_t)L.z0 + (uint32_t)colour) & 1u);
+  if (i >= L.nx) return;
+  Cell e;
+  e.i = i; e.j = (int)j; e.k = (int)k;
+  e.c = i + (int64_t)L.nx * row;
+  double tf[6];
+  load_faces<NDIM>(L, e, tf);
+  double acc = r[e.c];
+  if (!FIRST) acc += nbr_sum<NDIM>(L, e, tf, [&](int64_t q) { return z[q]; });
+  z[e.c] = acc / diag_of<NDIM>(tf);
+}
+
+// 1-D weights of fine cell i onto coarse cells: (I0, w0) + (I1, w1)  (P:412-428).
+__device__ __forceinline__ void interp_w(int i, int nc, int s, int kind, int& I0, double& w0, int& I1, double& w1) {
+  if (kind == 1 || nc == 1) {   // piecewise constant (P:414)
+    I0 = min(i / s, nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
+    return;
+  }
+  const double x = i + 0.5;                   // fine centre in fine-cell units
+  const double X0 = 0.5 * s, Xl = s * (nc - 0.5);
+  if (x <= X0) { I0 = 0; w0 = 1.0; I1 = 0; w1 = 0.0; return; }          // zero slope (P:416-418)
+  if (x >= Xl) { I0 = nc - 1; w0 = 1.0; I1 = nc - 1; w1 = 0.0; return; }
+  const int I = (int)floor((x - X0) / s);
+  const double tt = (x - s * (I + 0.5)) / s;
+  I0 = I; w0 = 1.0 - tt; I1 = I + 1; w1 = tt;
+}
+
+// One output of the restriction R = E^T along `axis`: (n0,n1,n2) -> n_axis = nc.
+__device__ __forceinline__ void restrict_item(const double* __restrict__ in, double* __restrict__ out, int n0, int n1,
+                                              int n2, int axis, int nc, int s, int kind, int64_t t) {
+  const int o0 = (axis == 0) ? nc : n0, o1 = (axis == 1) ? nc : n1;
+  const int nf = (axis == 0) ? n0 : (axis == 1) ? n1 : n2;
+  const int64_t stride_ax = (axis == 0) ? 1 : (axis == 1) ? (int64_t)n0 : (int64_t)n0 * n1;
+  int q[3];
+  q[0] = (int)(t % o0);
+  const int64_t rr = t / o0;
+  q[1] = (int)(rr % o1);
+  q[2] = (int)(rr / o1);
+  const int I = q[axis];
+  q[axis] = 0;
+  const int64_t base = q[0] + (int64_t)n0 * (q[1] + (int64_t)n1 * q[2]);
+  double acc = 0.0;
+  const int ilo = max(0, s * (I - 1)), ihi = min(nf, s * (I + 2));
+  for (int i = ilo; i < ihi; ++i) {
+    int I0, I1; double w0, w1;
+    interp_w(i, nc, s, kind, I0, w0, I1, w1);
+    double w = 0.0;
+    if (I0 == I) w += w0;
+    if (I1 == I && I1 != I0) w += w1;
+    if (w != 0.0) acc += w * in[base + i * stride_ax];
+  }
+  out[t] = acc;
+}
+
+// z_c += (E y)_c for fine cell c if it has colour `colour` (-1 = all).
+template <int NDIM>
+__device__ __forceinline__ void prolong_item(const LevelDev& L, int ncx, int ncy, int ncz, int s, int kind,
+                                             const double* __restrict__ y, double* __restrict__ z, int colour,
+                                             int64_t c) {
+  const Cell e = cell_of(L, c);
+  if (colour >= 0 && (((e.i + e.j + e.k + L.z0) & 1) != colour)) return;
+  int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
+  double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
+  interp_w(e.i, ncx, s, kind, X0, wx0, X1, wx1);
+  interp_w(e.j, ncy, s, kind, Y0, wy0, Y1, wy1);
+  if (NDIM == 3) interp_w(e.k, ncz, s, kind, Z0, wz0, Z1, wz1);
+  const int64_t cp = (int64_t)ncx * ncy;
+  auto Y = [&](int a, int bb, int cc) { return y[a + (int64_t)ncx * bb + cp * cc]; };
+  double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
+               wy1 * (wx0 * Y(X0, Y1, Z0) + wx1 * Y(X1, Y1, Z0));
+  if (NDIM == 3) {
+    acc *= wz0;
+    acc += wz1 * (wy0 * (wx0 * Y(X0, Y0, Z1) + wx1 * Y(X1, Y0, Z1)) +
+                  wy1 * (wx0 * Y(X0, Y1, Z1) + wx1 * Y(X1, Y1, Z1)));
+  }
+  z[c] += acc;
+}
+
+// a10: p_out = z + beta p_in (p = z when first); q = A p_out; returns p_out . q term.
+template <int NDIM>
+__device__ __forceinline__ double spmv_item(const LevelDev& L, const double* __restrict__ z,
+                                            const double* __restrict__ pin, double* __restrict__ pout,
+                                            double* __restrict__ q, double beta, int first, int64_t c) {
+  const Cell e = cell_of(L, c);
+  double t[6];
+  load_faces<NDIM>(L, e, t);
+  auto P = [&](int64_t idx) { return first ? z[idx] : z[idx] + beta * pin[idx]; };
+  const double pc = P(c);
+  const double qc = diag_of<NDIM>(t) * pc - nbr_sum<NDIM>(L, e, t, P);
+  pout[c] = pc;
+  q[c] = qc;
+  return pc * qc;
+}
+
+// a11: x += alpha p; r -= alpha q; returns r^2.
+__device__ __forceinline__ double axpy_item(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                                            const double* __restrict__ q, double alpha, int64_t c) {
+  x[c] += alpha * p[c];
+  const double rv = r[c] - alpha * q[c];
+  r[c] = rv;
+  return rv * rv;
+}
+
+// ------------------------------------------------------------------ grid kernels
 // r = b - A x, with ||r||^2 reduced when ro.out != nullptr.
 template <int NDIM>
 __global__ void k_residual(LevelDev L, const double* __restrict__ b, const double* __restrict__ x,
                            double* __restrict__ r, RedOut ro) {
   double acc = 0.0;
   for (int64_t c = gtid(); c < L.N; c += gstride()) {
-    const Cell e = cell_of(L, c);
-    double t[6];
-    load_faces<NDIM>(L, e, t);
-    const double ax = diag_of<NDIM>(t) * x[c] - nbr_sum<NDIM>(L, e, t, [&](int64_t q) { return x[q]; });
-    const double rv = b[c] - ax;
-    r[c] = rv;
+    const double rv = residual_item<NDIM>(L, c, b, x, r);
     acc += rv * rv;
   }
   if (ro.out) grid_sum_finish(acc, ro);
@@ -365,126 +489,34 @@ __global__ void k_apply_A(LevelDev L, const double* __restrict__ x, double* __re
   }
 }
 
-// ------------------------------------------------------------------ a5/a9: red-black half-sweep (K05)
-// Cells of colour `colour` ((i + j + k + z0) % 2): z_c = (r_c + sum_f T_f z_nbr) / diag_c.
-// FIRST: z = 0 on entry, so z_c = r_c / diag_c (only T and r are read).
-// Threads walk the colour's cells: thread t -> row = t / hx, i = 2 (t % hx) + parity(row).
 template <int NDIM, bool FIRST>
 __global__ void k_halfsweep(LevelDev L, const double* __restrict__ r, double* __restrict__ z, int colour) {
   const uint32_t hx = (uint32_t)(L.nx + 1) >> 1;
   const int64_t total = (int64_t)hx * L.ny * L.nz;
-  for (int64_t t = gtid(); t < total; t += gstride()) {
-    const uint32_t ut = (uint32_t)t;
-    const uint32_t row = ut / hx;
-    const uint32_t m = ut - row * hx;
-    const uint32_t k = row / (uint32_t)L.ny;
-    const uint32_t j = row - k * (uint32_t)L.ny;
-    const int i = 2 * (int)m + (int)((j + k + (uint32_t)L.z0 + (uint32_t)colour) & 1u);
-    if (i >= L.nx) continue;
-    Cell e;
-    e.i = i; e.j = (int)j; e.k = (int)k;
-    e.c = i + (int64_t)L.nx * row;
-    double tf[6];
-    load_faces<NDIM>(L, e, tf);
-    double acc = r[e.c];
-    if (!FIRST) acc += nbr_sum<NDIM>(L, e, tf, [&](int64_t q) { return z[q]; });
-    z[e.c] = acc / diag_of<NDIM>(tf);
-  }
+  for (int64_t t = gtid(); t < total; t += gstride()) sweep_item<NDIM, FIRST>(L, hx, (uint32_t)t, r, z, colour);
 }
 
-// ------------------------------------------------------------------ a6/a8: transfer
-// 1-D weights of fine cell i onto coarse cells: (I0, w0) + (I1, w1).
-__device__ __forceinline__ void interp_w(int i, int nc, int s, int kind, int& I0, double& w0, int& I1, double& w1) {
-  if (kind == 1 || nc == 1) {   // piecewise constant (P:414)
-    I0 = min(i / s, nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
-    return;
-  }
-  const double x = i + 0.5;                   // fine centre in fine-cell units
-  const double X0 = 0.5 * s, Xl = s * (nc - 0.5);
-  if (x <= X0) { I0 = 0; w0 = 1.0; I1 = 0; w1 = 0.0; return; }          // zero slope (P:416-418)
-  if (x >= Xl) { I0 = nc - 1; w0 = 1.0; I1 = nc - 1; w1 = 0.0; return; }
-  const int I = (int)floor((x - X0) / s);
-  const double tt = (x - s * (I + 0.5)) / s;
-  I0 = I; w0 = 1.0 - tt; I1 = I + 1; w1 = tt;
-}
-
-// out = R_axis in along one axis: (n0,n1,n2) -> same with n_axis -> nc.  Gather form.
 __global__ void k_restrict_axis(const double* __restrict__ in, double* __restrict__ out,
                                 int n0, int n1, int n2, int axis, int nc, int s, int kind) {
   const int o0 = (axis == 0) ? nc : n0, o1 = (axis == 1) ? nc : n1, o2 = (axis == 2) ? nc : n2;
   const int64_t total = (int64_t)o0 * o1 * o2;
-  const int nf = (axis == 0) ? n0 : (axis == 1) ? n1 : n2;
-  const int64_t stride_ax = (axis == 0) ? 1 : (axis == 1) ? (int64_t)n0 : (int64_t)n0 * n1;
-  for (int64_t t = gtid(); t < total; t += gstride()) {
-    int q[3];
-    q[0] = (int)(t % o0);
-    const int64_t rr = t / o0;
-    q[1] = (int)(rr % o1);
-    q[2] = (int)(rr / o1);
-    const int I = q[axis];
-    q[axis] = 0;
-    const int64_t base = q[0] + (int64_t)n0 * (q[1] + (int64_t)n1 * q[2]);
-    double acc = 0.0;
-    const int ilo = max(0, s * (I - 1)), ihi = min(nf, s * (I + 2));
-    for (int i = ilo; i < ihi; ++i) {
-      int I0, I1; double w0, w1;
-      interp_w(i, nc, s, kind, I0, w0, I1, w1);
-      double w = 0.0;
-      if (I0 == I) w += w0;
-      if (I1 == I && I1 != I0) w += w1;
-      if (w != 0.0) acc += w * in[base + i * stride_ax];
-    }
-    out[t] = acc;
-  }
+  for (int64_t t = gtid(); t < total; t += gstride()) restrict_item(in, out, n0, n1, n2, axis, nc, s, kind, t);
 }
 
-// z_c += (E y)_c on cells of colour `colour` (-1 = all).  y is the coarse level's
-// compact vector.
 template <int NDIM>
 __global__ void k_prolong_add(LevelDev L, int ncx, int ncy, int ncz, int s, int kind,
                               const double* __restrict__ y, double* __restrict__ z, int colour) {
-  for (int64_t c = gtid(); c < L.N; c += gstride()) {
-    const Cell e = cell_of(L, c);
-    if (colour >= 0 && (((e.i + e.j + e.k + L.z0) & 1) != colour)) continue;
-    int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
-    double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
-    interp_w(e.i, ncx, s, kind, X0, wx0, X1, wx1);
-    interp_w(e.j, ncy, s, kind, Y0, wy0, Y1, wy1);
-    if (NDIM == 3) interp_w(e.k, ncz, s, kind, Z0, wz0, Z1, wz1);
-    const int64_t cp = (int64_t)ncx * ncy;
-    auto Y = [&](int a, int bb, int cc) { return y[a + (int64_t)ncx * bb + cp * cc]; };
-    double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
-                 wy1 * (wx0 * Y(X0, Y1, Z0) + wx1 * Y(X1, Y1, Z0));
-    if (NDIM == 3) {
-      acc *= wz0;
-      acc += wz1 * (wy0 * (wx0 * Y(X0, Y0, Z1) + wx1 * Y(X1, Y0, Z1)) +
-                    wy1 * (wx0 * Y(X0, Y1, Z1) + wx1 * Y(X1, Y1, Z1)));
-    }
-    z[c] += acc;
-  }
+  for (int64_t c = gtid(); c < L.N; c += gstride()) prolong_item<NDIM>(L, ncx, ncy, ncz, s, kind, y, z, colour, c);
 }
 
-// ------------------------------------------------------------------ a10: direction + SpMV + dot (K08)
-// p_out = z + beta p_in (beta = rho / rho_prev; p = z on the first iteration);
-// q = A p_out; reduces p_out . q into scal->pq.  The neighbours' p_out are formed on
-// the fly from z and p_in, so the update and the SpMV are one pass.
+// a10: direction + SpMV + p.q in one pass (neighbours' p formed on the fly).
 template <int NDIM>
 __global__ void k_pdir_spmv_dot(LevelDev L, const double* __restrict__ z, const double* __restrict__ pin,
                                 double* __restrict__ pout, double* __restrict__ q, const Scal* sc,
                                 int first, RedOut ro) {
   const double beta = first ? 0.0 : sc->rho / sc->rho_prev;
   double acc = 0.0;
-  for (int64_t c = gtid(); c < L.N; c += gstride()) {
-    const Cell e = cell_of(L, c);
-    double t[6];
-    load_faces<NDIM>(L, e, t);
-    auto P = [&](int64_t idx) { return first ? z[idx] : z[idx] + beta * pin[idx]; };
-    const double pc = P(c);
-    const double qc = diag_of<NDIM>(t) * pc - nbr_sum<NDIM>(L, e, t, P);
-    pout[c] = pc;
-    q[c] = qc;
-    acc += pc * qc;
-  }
+  for (int64_t c = gtid(); c < L.N; c += gstride()) acc += spmv_item<NDIM>(L, z, pin, pout, q, beta, first, c);
   grid_sum_finish(acc, ro);
 }
 
@@ -494,12 +526,7 @@ __global__ void k_axpy_norm(int64_t n, double* __restrict__ x, double* __restric
                             const Scal* sc, RedOut ro) {
   const double alpha = sc->rho / sc->pq;
   double acc = 0.0;
-  for (int64_t c = gtid(); c < n; c += gstride()) {
-    x[c] += alpha * p[c];
-    const double rv = r[c] - alpha * q[c];
-    r[c] = rv;
-    acc += rv * rv;
-  }
+  for (int64_t c = gtid(); c < n; c += gstride()) acc += axpy_item(x, r, p, q, alpha, c);
   grid_sum_finish(acc, ro);
 }
 

@@ -18,9 +18,11 @@
 
 #include "internal.cuh"
 #include "kernels.cuh"
-#include "tail.cuh"
 
 using namespace mss;
+
+static int set_err(int code, const std::string& msg);
+#include "tail.cuh"
 
 static thread_local std::string g_err;
 
@@ -314,6 +316,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
 
 static void set_thresholds(mss_ctx* ctx, double eps2) {
   ctx->eps2 = eps2;
+  tail_mark_dirty(ctx);
   double fk = 1.0;
   for (int k = 0; k <= ctx->L; ++k) {
     ctx->lv[k].thr = (double)ctx->lv[k].N * fk * eps2;
@@ -384,6 +387,11 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
       rc = pcg_level(ctx, 0);
       if (rc < 0 && rc != MSS_EBREAKDOWN) return rc;
     }
+  }
+  {
+    const int trc = tail_collect(ctx);
+    if (trc == MSS_ECUDA) return trc;
+    if (trc == MSS_EBREAKDOWN && rc == MSS_OK) rc = MSS_EBREAKDOWN;
   }
   // true residual (O15)
   TRY(op_residual(ctx, 0, l.b, l.x, l.s, &ds->aux));
@@ -815,6 +823,7 @@ int mss_precond(mss_ctx* ctx, int level, const double* r, double* z, double rel_
       ctx->lv[k].thr = (double)ctx->lv[k].N * fk * eps2;
       if (k >= level) fk *= ctx->prm.f;
     }
+    tail_mark_dirty(ctx);
   }
   if (level == ctx->L) {
     TRY(op_coarse_solve(ctx, l.r, l.z));
@@ -824,6 +833,7 @@ int mss_precond(mss_ctx* ctx, int level, const double* r, double* z, double rel_
   }
   CK(cudaMemcpyAsync(z, l.z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  TRY(tail_collect(ctx));
   if (iters)
     for (int k = 0; k <= ctx->L; ++k) iters[k] = ctx->info.iters[k];
   return MSS_OK;

@@ -1,7 +1,373 @@
-// tail.cuh — device-resident coarse levels (placeholder until the cluster kernel lands).
+// tail.cuh — device-resident coarse levels (K13): one thread-block-cluster launch runs
+// the whole recursive PCG of levels k0..L (Eq. 2.10 recursion, with the
+// dynamic per-level stop of P:448-456) without returning to the host.
+//
+// Why: below ~64K cells a PCG iteration is ~25 dependent passes of a few microseconds
+// of work each; as separate launches with a host-side convergence test they are pure
+// launch/sync latency (SURVEY §7 hard part 2).  Here the passes are separated by
+// cluster barriers (barrier.cluster, ~0.2 us) and the CG scalars are reduced through
+// distributed shared memory, so control never leaves the GPU.
+//
+// Layout: the level vectors stay where the grid path keeps them (ghosted, in HBM and
+// hot in the 126 MB L2); the per-cell arithmetic is the same *_item bodies the grid
+// kernels use, so both paths compute identical values.
 #pragma once
-#include "internal.cuh"
+#include <cooperative_groups.h>
 
-static inline bool tail_supported(const mss_ctx*, int) { return false; }
-static inline int tail_pcg(mss_ctx*, int) { return MSS_EUNSUPPORTED; }
-static inline int tail_setup(mss_ctx*) { return MSS_OK; }
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mss {
+
+constexpr int kTailThreads = 512;
+
+struct TLevel {
+  LevelDev g;
+  double *x, *r, *z, *q, *s, *t1, *t2, *p0, *p1;
+  double thr;
+  int ncx, ncy, ncz;   // dims of level k+1 (if any)
+};
+
+struct TailArgs {
+  int k0, L, ndim, m, scale, interp, max_iter, NL;
+  const double* Ainv;
+  long long* iters;    // [MSS_MAX_LEVELS]
+  long long* calls;    // [MSS_MAX_LEVELS]
+  int* flags;          // [0] not converged, [1] breakdown level + 1
+  TLevel lv[MSS_MAX_LEVELS];
+};
+
+template <int NDIM>
+struct Tail {
+  const TailArgs* __restrict__ A;
+  cg::cluster_group cl;
+  uint32_t tid, nth;
+  int phase;
+  double* red_w;      // [32] per-CTA warp partials
+  double* slot;       // [2]  per-CTA block partial (double-buffered)
+  double* bcast;      // [1]
+
+  __device__ Tail(const TailArgs* a, double* sh) : A(a), cl(cg::this_cluster()), phase(0) {
+    tid = cl.block_rank() * blockDim.x + threadIdx.x;
+    nth = cl.num_blocks() * blockDim.x;
+    red_w = sh;
+    slot = sh + 32;
+    bcast = sh + 34;
+  }
+
+  __device__ __forceinline__ void sync() { cl.sync(); }
+
+  // Cluster-wide sum: warp shuffles, CTA partial in smem, cluster barrier, then every
+  // CTA sums all CTA partials through DSMEM in rank order -> identical bits everywhere.
+  __device__ double sum(double v) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red_w[w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      const int nw = blockDim.x >> 5;
+      for (int i = 0; i < nw; ++i) s += red_w[i];
+      slot[phase] = s;
+    }
+    sync();
+    if (w == 0) {
+      const int cs = (int)cl.num_blocks();
+      double pv = 0.0;
+      if (lane < cs) pv = *cl.map_shared_rank(&slot[phase], lane);
+      pv = warp_sum(pv);
+      if (lane == 0) *bcast = pv;
+    }
+    __syncthreads();
+    const double tot = *bcast;
+    phase ^= 1;
+    return tot;
+  }
+
+  __device__ void sweep(int k, int colour, bool first) {
+    const TLevel& l = A->lv[k];
+    const uint32_t hx = (uint32_t)(l.g.nx + 1) >> 1;
+    const uint32_t total = hx * (uint32_t)l.g.ny * (uint32_t)l.g.nz;
+    if (first) {
+      for (uint32_t t = tid; t < total; t += nth) sweep_item<NDIM, true>(l.g, hx, t, l.r, l.z, colour);
+    } else {
+      for (uint32_t t = tid; t < total; t += nth) sweep_item<NDIM, false>(l.g, hx, t, l.r, l.z, colour);
+    }
+    sync();
+  }
+
+  __device__ void smooth(int k, bool from_zero) {
+    const int nh = 2 * A->m + 1;
+    for (int h = 0; h < nh; ++h) sweep(k, h & 1, from_zero && h == 0);
+  }
+
+  __device__ void residual(int k) {
+    const TLevel& l = A->lv[k];
+    for (int64_t c = tid; c < l.g.N; c += nth) residual_item<NDIM>(l.g, c, l.r, l.z, l.s);
+    sync();
+  }
+
+  __device__ void restrict_to(int k) {
+    const TLevel& f = A->lv[k];
+    const TLevel& c = A->lv[k + 1];
+    const int S = A->scale, kind = A->interp;
+    if (NDIM == 3) {
+      const int64_t n1 = (int64_t)c.g.nx * f.g.ny * f.g.nz;
+      for (int64_t t = tid; t < n1; t += nth) restrict_item(f.s, f.t1, f.g.nx, f.g.ny, f.g.nz, 0, c.g.nx, S, kind, t);
+      sync();
+      const int64_t n2 = (int64_t)c.g.nx * c.g.ny * f.g.nz;
+      for (int64_t t = tid; t < n2; t += nth) restrict_item(f.t1, f.t2, c.g.nx, f.g.ny, f.g.nz, 1, c.g.ny, S, kind, t);
+      sync();
+      for (int64_t t = tid; t < c.g.N; t += nth) restrict_item(f.t2, c.r, c.g.nx, c.g.ny, f.g.nz, 2, c.g.nz, S, kind, t);
+      sync();
+    } else {
+      const int64_t n1 = (int64_t)c.g.nx * f.g.ny;
+      for (int64_t t = tid; t < n1; t += nth) restrict_item(f.s, f.t1, f.g.nx, f.g.ny, 1, 0, c.g.nx, S, kind, t);
+      sync();
+      for (int64_t t = tid; t < c.g.N; t += nth) restrict_item(f.t1, c.r, c.g.nx, f.g.ny, 1, 1, c.g.ny, S, kind, t);
+      sync();
+    }
+  }
+
+  __device__ void prolong(int k) {
+    const TLevel& f = A->lv[k];
+    const TLevel& c = A->lv[k + 1];
+    for (int64_t t = tid; t < f.g.N; t += nth)
+      prolong_item<NDIM>(f.g, c.g.nx, c.g.ny, c.g.nz, A->scale, A->interp, c.x, f.z, 1, t);
+    sync();
+  }
+
+  // x_L = A_L^{-1} r_L, one warp per row.
+  __device__ void coarse() {
+    const TLevel& c = A->lv[A->L];
+    const int n = A->NL;
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = tid >> 5, nw = nth >> 5;
+    for (uint32_t row = gw; row < (uint32_t)n; row += nw) {
+      double acc = 0.0;
+      const double* a = A->Ainv + (int64_t)row * n;
+      for (int k = lane; k < n; k += 32) acc += a[k] * c.r[k];
+      acc = warp_sum(acc);
+      if (lane == 0) c.x[row] = acc;
+    }
+    sync();
+  }
+
+  __device__ void count(long long* arr, int k, long long v) {
+    if (tid == 0) arr[k] += v;
+  }
+
+  template <int D>
+  __device__ bool precond(int k) {
+    smooth(k, true);
+    residual(k);
+    restrict_to(k);
+    if (k + 1 == A->L) {
+      coarse();
+      count(A->iters, k + 1, 1);
+      count(A->calls, k + 1, 1);
+    } else {
+      if (!pcg<D - 1>(k + 1)) return false;
+    }
+    prolong(k);
+    smooth(k, false);
+    return true;
+  }
+
+  // PCG on level k from x = 0, r = b (r already holds b).  Returns false on breakdown.
+  template <int D>
+  __device__ bool pcg(int k) {
+    if (D <= 0) {
+      if (tid == 0) A->flags[1] = k + 1;
+      return false;
+    }
+    const TLevel& l = A->lv[k];
+    count(A->calls, k, 1);
+    double acc = 0.0;
+    for (int64_t c = tid; c < l.g.N; c += nth) {
+      l.x[c] = 0.0;
+      const double rv = l.r[c];
+      acc += rv * rv;
+    }
+    double rr = sum(acc);
+    if (rr < l.thr) return true;
+    long long it = 0;
+    double rho_prev = 1.0;
+    int cur = 0;
+    for (;;) {
+      if (!precond<D>(k)) return false;
+      acc = 0.0;
+      for (int64_t c = tid; c < l.g.N; c += nth) acc += l.r[c] * l.z[c];
+      const double rho = sum(acc);
+      double* pin = cur ? l.p1 : l.p0;
+      double* pout = cur ? l.p0 : l.p1;
+      const double beta = (it == 0) ? 0.0 : rho / rho_prev;
+      acc = 0.0;
+      for (int64_t c = tid; c < l.g.N; c += nth)
+        acc += spmv_item<NDIM>(l.g, l.z, pin, pout, l.q, beta, it == 0 ? 1 : 0, c);
+      const double pq = sum(acc);
+      cur ^= 1;
+      if (!(rho > 0.0) || !(pq > 0.0)) {
+        count(A->iters, k, it + 1);
+        if (tid == 0) A->flags[1] = k + 1;
+        return false;
+      }
+      const double alpha = rho / pq;
+      acc = 0.0;
+      for (int64_t c = tid; c < l.g.N; c += nth) acc += axpy_item(l.x, l.r, pout, l.q, alpha, c);
+      rr = sum(acc);
+      it++;
+      rho_prev = rho;
+      if (rr < l.thr) break;
+      if (it >= A->max_iter) {
+        if (tid == 0) A->flags[0] = 1;
+        break;
+      }
+    }
+    count(A->iters, k, it);
+    return true;
+  }
+};
+
+template <>
+template <>
+__device__ bool Tail<2>::precond<0>(int) { return false; }
+template <>
+template <>
+__device__ bool Tail<3>::precond<0>(int) { return false; }
+
+template <int NDIM>
+__global__ void __launch_bounds__(kTailThreads, 1) k_tail(const TailArgs* __restrict__ A, int k0) {
+  __shared__ double sh[40];
+  Tail<NDIM> T(A, sh);
+  T.template pcg<6>(k0);
+}
+
+}  // namespace mss
+
+// ============================================================================ host side
+static int tail_setup(mss_ctx* ctx) {
+  ctx->tail_cs = 0;
+  if (ctx->prm.tail_cells <= 0 || ctx->nranks > 1) return MSS_OK;
+  auto kern = (ctx->ndim == 3) ? (void*)mss::k_tail<3> : (void*)mss::k_tail<2>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int cs : {16, 8, 4}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(mss::kTailThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
+    if (e == cudaSuccess && nclusters >= 1) {
+      ctx->tail_cs = cs;
+      break;
+    }
+    cudaGetLastError();
+  }
+  if (!ctx->tail_cs) return MSS_OK;
+  void* p = nullptr;
+  if (cudaMalloc(&p, sizeof(mss::TailArgs)) != cudaSuccess) return MSS_ENOMEM;
+  ctx->allocs.push_back(p);
+  ctx->tail_d = p;
+  if (cudaMalloc(&p, sizeof(long long) * 2 * MSS_MAX_LEVELS) != cudaSuccess) return MSS_ENOMEM;
+  ctx->allocs.push_back(p);
+  ctx->tail_cnt = (long long*)p;
+  if (cudaMalloc(&p, sizeof(int) * 2) != cudaSuccess) return MSS_ENOMEM;
+  ctx->allocs.push_back(p);
+  ctx->tail_flags = (int*)p;
+  cudaMemsetAsync(ctx->tail_cnt, 0, sizeof(long long) * 2 * MSS_MAX_LEVELS, ctx->stream);
+  cudaMemsetAsync(ctx->tail_flags, 0, sizeof(int) * 2, ctx->stream);
+  ctx->tail_h.assign(sizeof(mss::TailArgs), 0);
+  ctx->tail_dirty = true;
+  return MSS_OK;
+}
+
+static bool tail_supported(mss_ctx* ctx, int k) {
+  return ctx->tail_cs > 0 && k >= 1 && k < ctx->L && ctx->lv[k].N <= ctx->prm.tail_cells;
+}
+
+static void tail_mark_dirty(mss_ctx* ctx) { ctx->tail_dirty = true; }
+
+static int tail_pcg(mss_ctx* ctx, int k) {
+  if (ctx->tail_dirty) {
+    mss::TailArgs& a = *reinterpret_cast<mss::TailArgs*>(ctx->tail_h.data());
+    a.k0 = 0;
+    a.L = ctx->L;
+    a.ndim = ctx->ndim;
+    a.m = ctx->prm.m;
+    a.scale = ctx->prm.scale;
+    a.interp = ctx->prm.interp;
+    a.max_iter = ctx->prm.max_iter;
+    a.NL = ctx->NL;
+    a.Ainv = ctx->Ainv;
+    a.iters = ctx->tail_cnt;
+    a.calls = ctx->tail_cnt + MSS_MAX_LEVELS;
+    a.flags = ctx->tail_flags;
+    for (int q = 0; q <= ctx->L; ++q) {
+      const mss::Level& l = ctx->lv[q];
+      mss::TLevel& t = a.lv[q];
+      t.g = l.dev();
+      t.x = l.x; t.r = l.r; t.z = l.z; t.q = l.q; t.s = l.s; t.t1 = l.t1; t.t2 = l.t2;
+      t.p0 = l.p[0]; t.p1 = l.p[1];
+      t.thr = l.thr;
+      if (q < ctx->L) {
+        t.ncx = ctx->lv[q + 1].nx; t.ncy = ctx->lv[q + 1].ny; t.ncz = ctx->lv[q + 1].nz;
+      } else {
+        t.ncx = t.ncy = t.ncz = 0;
+      }
+    }
+    if (cudaMemcpyAsync(ctx->tail_d, &a, sizeof(mss::TailArgs), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+      return MSS_ECUDA;
+    // the host image must stay unchanged until the copy has run
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return MSS_ECUDA;
+    ctx->tail_dirty = false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->tail_cs);
+  cfg.blockDim = dim3(mss::kTailThreads);
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ctx->tail_cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const mss::TailArgs* dp = reinterpret_cast<const mss::TailArgs*>(ctx->tail_d);
+  cudaError_t e = (ctx->ndim == 3) ? cudaLaunchKernelEx(&cfg, mss::k_tail<3>, dp, k)
+                                   : cudaLaunchKernelEx(&cfg, mss::k_tail<2>, dp, k);
+  ctx->launches++;
+  return e == cudaSuccess ? MSS_OK : MSS_ECUDA;
+}
+
+// Add the device-side counters of the tail into ctx->info and reset them.
+static int tail_collect(mss_ctx* ctx) {
+  if (!ctx->tail_cs) return MSS_OK;
+  long long c[2 * MSS_MAX_LEVELS];
+  int fl[2];
+  if (cudaMemcpyAsync(c, ctx->tail_cnt, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess) return MSS_ECUDA;
+  if (cudaMemcpyAsync(fl, ctx->tail_flags, sizeof(fl), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+    return MSS_ECUDA;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return MSS_ECUDA;
+  for (int k = 0; k < MSS_MAX_LEVELS; ++k) {
+    ctx->info.iters[k] += c[k];
+    ctx->info.calls[k] += c[MSS_MAX_LEVELS + k];
+  }
+  if (fl[0]) ctx->info.not_converged = 1;
+  int rc = MSS_OK;
+  if (fl[1]) {
+    ctx->info.breakdown_level = fl[1] - 1;
+    rc = MSS_EBREAKDOWN;
+  }
+  cudaMemsetAsync(ctx->tail_cnt, 0, sizeof(long long) * 2 * MSS_MAX_LEVELS, ctx->stream);
+  cudaMemsetAsync(ctx->tail_flags, 0, sizeof(int) * 2, ctx->stream);
+  return rc;
+}
