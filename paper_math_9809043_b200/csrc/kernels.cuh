@@ -354,25 +354,40 @@ __device__ __forceinline__ double residual_item(const LevelDev& L, int64_t c, co
   return rv;
 }
 
-// a5/a9 half-sweep item t of colour `colour`: row = t / hx, i = 2 (t % hx) + parity.
-// z_c = (r_c + sum_f T_f z_nbr) / diag_c  (FIRST: z = 0 on entry, z_c = r_c / diag_c).
-template <int NDIM, bool FIRST>
-__device__ __forceinline__ void sweep_item(const LevelDev& L, uint32_t hx, uint32_t t, const double* __restrict__ r,
-                                           double* __restrict__ z, int colour) {
+// a5/a9 half-sweep, item t = cell pair (2m, 2m+1) of row t / hx; the pair's cell of
+// colour `colour` ((i+j+k+z0) % 2) is updated:
+//   z_c = (r_c + sum_f T_f z_nbr) / diag_c     (FIRST: z = 0 on entry -> r_c / diag_c).
+// DOT: also returns r.z over both cells of the pair (the partner's z is final for this
+// sweep), so rho = r.z of the last post-smoothing sweep costs no extra pass.
+template <int NDIM, bool FIRST, bool DOT>
+__device__ __forceinline__ double sweep_item(const LevelDev& L, uint32_t hx, uint32_t t, const double* __restrict__ r,
+                                             double* __restrict__ z, int colour) {
   const uint32_t row = t / hx;
   const uint32_t m = t - row * hx;
   const uint32_t k = row / (uint32_t)L.ny;
   const uint32_t j = row - k * (uint32_t)L.ny;
-  const int i = 2 * (int)m + (int)((j + k + (uint32_t)L.z0 + (uint32_t)colour) & 1u);
-  if (i >= L.nx) return;
-  Cell e;
-  e.i = i; e.j = (int)j; e.k = (int)k;
-  e.c = i + (int64_t)L.nx * row;
-  double tf[6];
-  load_faces<NDIM>(L, e, tf);
-  double acc = r[e.c];
-  if (!FIRST) acc += nbr_sum<NDIM>(L, e, tf, [&](int64_t q) { return z[q]; });
-  z[e.c] = acc / diag_of<NDIM>(tf);
+  const int par = (int)((j + k + (uint32_t)L.z0 + (uint32_t)colour) & 1u);
+  const int i = 2 * (int)m + par;
+  const int64_t rowoff = (int64_t)L.nx * row;
+  double dot = 0.0;
+  if (i < L.nx) {
+    Cell e;
+    e.i = i; e.j = (int)j; e.k = (int)k;
+    e.c = i + rowoff;
+    double tf[6];
+    load_faces<NDIM>(L, e, tf);
+    const double rc = r[e.c];
+    double acc = rc;
+    if (!FIRST) acc += nbr_sum<NDIM>(L, e, tf, [&](int64_t q) { return z[q]; });
+    const double zc = acc / diag_of<NDIM>(tf);
+    z[e.c] = zc;
+    if (DOT) dot += rc * zc;
+  }
+  if (DOT) {
+    const int ip = 2 * (int)m + (1 - par);
+    if (ip < L.nx) dot += r[ip + rowoff] * z[ip + rowoff];
+  }
+  return dot;
 }
 
 // 1-D weights of fine cell i onto coarse cells: (I0, w0) + (I1, w1).
@@ -415,6 +430,67 @@ __device__ __forceinline__ void restrict_item(const double* __restrict__ in, dou
     if (w != 0.0) acc += w * in[base + i * stride_ax];
   }
   out[t] = acc;
+}
+
+// a6 fused: t1[I, j, k] = sum_i w_x(i -> I) (r - A z)_(i,j,k) — the residual is formed
+// on the fly and never stored.  black_only: after the closing red sweep the red
+// residual is zero (to rounding), so only black cells are evaluated.
+template <int NDIM>
+__device__ __forceinline__ void resid_restrict_x_item(const LevelDev& L, const double* __restrict__ r,
+                                                      const double* __restrict__ z, double* __restrict__ t1,
+                                                      int ncx, int s, int kind, int black_only, uint32_t t) {
+  const uint32_t row = t / (uint32_t)ncx;
+  const int I = (int)(t - row * (uint32_t)ncx);
+  const uint32_t k = row / (uint32_t)L.ny;
+  const uint32_t j = row - k * (uint32_t)L.ny;
+  const int64_t rowoff = (int64_t)L.nx * row;
+  const int ilo = max(0, s * (I - 1)), ihi = min(L.nx, s * (I + 2));
+  double acc = 0.0;
+  for (int i = ilo; i < ihi; ++i) {
+    if (black_only && (((uint32_t)i + j + k + (uint32_t)L.z0) & 1u) == 0u) continue;
+    int I0, I1; double w0, w1;
+    interp_w(i, ncx, s, kind, I0, w0, I1, w1);
+    double w = 0.0;
+    if (I0 == I) w += w0;
+    if (I1 == I && I1 != I0) w += w1;
+    if (w == 0.0) continue;
+    Cell e;
+    e.i = i; e.j = (int)j; e.k = (int)k; e.c = i + rowoff;
+    double tf[6];
+    load_faces<NDIM>(L, e, tf);
+    const double res = r[e.c] - (diag_of<NDIM>(tf) * z[e.c] - nbr_sum<NDIM>(L, e, tf, [&](int64_t q) { return z[q]; }));
+    acc += w * res;
+  }
+  t1[t] = acc;
+}
+
+// a8 on the black cells only (the next red sweep overwrites every red value, SURVEY
+// §0.3): item t = black cell of pair (2m, 2m+1) in row t / hx.
+template <int NDIM>
+__device__ __forceinline__ void prolong_black_item(const LevelDev& L, uint32_t hx, int ncx, int ncy, int ncz, int s,
+                                                   int kind, const double* __restrict__ y, double* __restrict__ z,
+                                                   uint32_t t) {
+  const uint32_t row = t / hx;
+  const uint32_t m = t - row * hx;
+  const uint32_t k = row / (uint32_t)L.ny;
+  const uint32_t j = row - k * (uint32_t)L.ny;
+  const int i = 2 * (int)m + (int)((j + k + (uint32_t)L.z0 + 1u) & 1u);
+  if (i >= L.nx) return;
+  int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
+  double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
+  interp_w(i, ncx, s, kind, X0, wx0, X1, wx1);
+  interp_w((int)j, ncy, s, kind, Y0, wy0, Y1, wy1);
+  if (NDIM == 3) interp_w((int)k, ncz, s, kind, Z0, wz0, Z1, wz1);
+  const int64_t cp = (int64_t)ncx * ncy;
+  auto Y = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * cc); };
+  double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
+               wy1 * (wx0 * Y(X0, Y1, Z0) + wx1 * Y(X1, Y1, Z0));
+  if (NDIM == 3) {
+    acc *= wz0;
+    acc += wz1 * (wy0 * (wx0 * Y(X0, Y0, Z1) + wx1 * Y(X1, Y0, Z1)) +
+                  wy1 * (wx0 * Y(X0, Y1, Z1) + wx1 * Y(X1, Y1, Z1)));
+  }
+  z[i + (int64_t)L.nx * row] += acc;
 }
 
 // z_c += (E y)_c for fine cell c if it has colour `colour` (-1 = all).
@@ -489,11 +565,31 @@ __global__ void k_apply_A(LevelDev L, const double* __restrict__ x, double* __re
   }
 }
 
-template <int NDIM, bool FIRST>
-__global__ void k_halfsweep(LevelDev L, const double* __restrict__ r, double* __restrict__ z, int colour) {
+template <int NDIM, bool FIRST, bool DOT>
+__global__ void __launch_bounds__(256, DOT ? 6 : 8) k_halfsweep(LevelDev L, const double* __restrict__ r, double* __restrict__ z,
+                                                      int colour, RedOut ro) {
   const uint32_t hx = (uint32_t)(L.nx + 1) >> 1;
   const int64_t total = (int64_t)hx * L.ny * L.nz;
-  for (int64_t t = gtid(); t < total; t += gstride()) sweep_item<NDIM, FIRST>(L, hx, (uint32_t)t, r, z, colour);
+  double acc = 0.0;
+  for (int64_t t = gtid(); t < total; t += gstride()) acc += sweep_item<NDIM, FIRST, DOT>(L, hx, (uint32_t)t, r, z, colour);
+  if (DOT) grid_sum_finish(acc, ro);
+}
+
+template <int NDIM>
+__global__ void k_resid_restrict_x(LevelDev L, const double* __restrict__ r, const double* __restrict__ z,
+                                   double* __restrict__ t1, int ncx, int s, int kind, int black_only) {
+  const int64_t total = (int64_t)ncx * L.ny * L.nz;
+  for (int64_t t = gtid(); t < total; t += gstride())
+    resid_restrict_x_item<NDIM>(L, r, z, t1, ncx, s, kind, black_only, (uint32_t)t);
+}
+
+template <int NDIM>
+__global__ void k_prolong_black(LevelDev L, int ncx, int ncy, int ncz, int s, int kind,
+                                const double* __restrict__ y, double* __restrict__ z) {
+  const uint32_t hx = (uint32_t)(L.nx + 1) >> 1;
+  const int64_t total = (int64_t)hx * L.ny * L.nz;
+  for (int64_t t = gtid(); t < total; t += gstride())
+    prolong_black_item<NDIM>(L, hx, ncx, ncy, ncz, s, kind, y, z, (uint32_t)t);
 }
 
 __global__ void k_restrict_axis(const double* __restrict__ in, double* __restrict__ out,
@@ -511,7 +607,7 @@ __global__ void k_prolong_add(LevelDev L, int ncx, int ncy, int ncz, int s, int 
 
 // a10: direction + SpMV + p.q in one pass (neighbours' p formed on the fly).
 template <int NDIM>
-__global__ void k_pdir_spmv_dot(LevelDev L, const double* __restrict__ z, const double* __restrict__ pin,
+__global__ void __launch_bounds__(256, 5) k_pdir_spmv_dot(LevelDev L, const double* __restrict__ z, const double* __restrict__ pin,
                                 double* __restrict__ pout, double* __restrict__ q, const Scal* sc,
                                 int first, RedOut ro) {
   const double beta = first ? 0.0 : sc->rho / sc->rho_prev;

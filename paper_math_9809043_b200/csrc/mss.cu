@@ -95,7 +95,7 @@ static RedOut red_to(mss_ctx* ctx, double* out, int level, int mode) {
   } while (0)
 
 // ============================================================================ live kernel timing
-enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_OTHER };
+enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_TAIL };
 
 static cudaEvent_t ev_get(mss_ctx* ctx) {
   if (!ctx->ev_free.empty()) {
@@ -151,7 +151,7 @@ struct ProfScope {
 static double cell_bytes(const mss_ctx* ctx, int cls) {
   const double T = ctx->ndim;
   switch (cls) {
-    case KC_SWEEP: return 8.0 * (T + 3);    // T + r + z(nbr lines) + z write
+    case KC_SWEEP: return 8.0 * (T + 3);    // T + r + z(nbr lines) + z write (r.z fused: same lines)
     case KC_SWEEP0: return 8.0 * (T + 2);   // T + r + z write
     case KC_RESID: return 8.0 * (T + 3);    // T + r + z + s write
     case KC_PROLONG: return 8.0 * 2;        // z read + write (coarse y from L2)
@@ -177,57 +177,93 @@ static int op_residual(mss_ctx* ctx, int k, const double* b, const double* x, do
   return MSS_OK;
 }
 
-static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int colour, bool first) {
+static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int colour, bool first,
+                        double* dot_out = nullptr) {
   Level& l = ctx->lv[k];
   const int64_t work = (int64_t)((l.nx + 1) / 2) * l.ny * l.nz;
   const int g = grid_for(work);
-  ProfScope ps(ctx, first ? KC_SWEEP0 : KC_SWEEP, k, cell_bytes(ctx, first ? KC_SWEEP0 : KC_SWEEP) * l.N);
+  const int cls = first ? KC_SWEEP0 : KC_SWEEP;
+  ProfScope ps(ctx, cls, k, cell_bytes(ctx, cls) * l.N);
+  RedOut ro = red_to(ctx, dot_out, k, 0);
+  const LevelDev d = l.dev();
+#define HS(ND, F, D) LAUNCH((k_halfsweep<ND, F, D>), g, d, r, z, colour, ro)
   if (ctx->ndim == 3) {
-    if (first) LAUNCH((k_halfsweep<3, true>), g, l.dev(), r, z, colour);
-    else LAUNCH((k_halfsweep<3, false>), g, l.dev(), r, z, colour);
+    if (first) HS(3, true, false);
+    else if (dot_out) HS(3, false, true);
+    else HS(3, false, false);
   } else {
-    if (first) LAUNCH((k_halfsweep<2, true>), g, l.dev(), r, z, colour);
-    else LAUNCH((k_halfsweep<2, false>), g, l.dev(), r, z, colour);
+    if (first) HS(2, true, false);
+    else if (dot_out) HS(2, false, true);
+    else HS(2, false, false);
   }
+#undef HS
   return MSS_OK;
 }
 
-// n_half alternating half-sweeps starting with `first_colour`.
-static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero) {
+// n_half alternating half-sweeps starting with `first_colour`; the last one also
+// reduces r.z into *dot_last when given.
+static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero,
+                     double* dot_last = nullptr) {
   for (int h = 0; h < n_half; ++h) {
     const int col = (first_colour + h) & 1;
-    TRY(op_halfsweep(ctx, k, r, z, col, z_zero && h == 0));
+    const bool first = z_zero && h == 0;
+    TRY(op_halfsweep(ctx, k, r, z, col, first, (h == n_half - 1 && !first) ? dot_last : nullptr));
   }
   return MSS_OK;
 }
 
-// coarse r_{k+1} = R s_k where s_k is the level-k vector `s` (ghost-free use).
-static int op_restrict(mss_ctx* ctx, int k, const double* s, double* coarse) {
+// y/z passes of R = E^T from the x-restricted t1 (level k) to the coarse vector.
+static int op_restrict_yz(mss_ctx* ctx, int k, double* coarse) {
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   const int S = ctx->prm.scale, kind = ctx->prm.interp;
-  const double rb = (ctx->ndim == 3)
-      ? 8.0 * ((double)f.N + 2.0 * c.nx * f.ny * f.nz + 2.0 * c.nx * c.ny * f.nz + c.N)
-      : 8.0 * ((double)f.N + 2.0 * c.nx * f.ny + c.N);
+  const double rb = (ctx->ndim == 3) ? 8.0 * (2.0 * c.nx * f.ny * f.nz + 2.0 * c.nx * c.ny * f.nz + c.N)
+                                     : 8.0 * ((double)c.nx * f.ny + c.N);
   ProfScope ps(ctx, KC_RESTRICT, k, rb);
   if (ctx->ndim == 3) {
-    // x: (nx,ny,nz) -> (ncx,ny,nz) ; y: -> (ncx,ncy,nz) ; z: -> (ncx,ncy,ncz)
-    LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * f.ny * f.nz), s, f.t1, f.nx, f.ny, f.nz, 0, c.nx, S, kind);
     LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * c.ny * f.nz), f.t1, f.t2, c.nx, f.ny, f.nz, 1, c.ny, S, kind);
     LAUNCH(k_restrict_axis, grid_for(c.N), f.t2, coarse, c.nx, c.ny, f.nz, 2, c.nz, S, kind);
   } else {
-    LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * f.ny), s, f.t1, f.nx, f.ny, 1, 0, c.nx, S, kind);
     LAUNCH(k_restrict_axis, grid_for(c.N), f.t1, coarse, c.nx, f.ny, 1, 1, c.ny, S, kind);
   }
   return MSS_OK;
 }
 
+// coarse = R (r - A z): residual fused with the x-pass of the restriction (a6).
+static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double* z, double* coarse, int black_only) {
+  Level& f = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  {
+    const double by = 8.0 * (ctx->ndim + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
+    ProfScope ps(ctx, KC_RESID, k, by);
+    DISPATCH(ctx->ndim, k_resid_restrict_x, grid_for((int64_t)c.nx * f.ny * f.nz), f.dev(), r, z, f.t1, c.nx,
+             ctx->prm.scale, ctx->prm.interp, black_only);
+  }
+  return op_restrict_yz(ctx, k, coarse);
+}
+
+// coarse r_{k+1} = R s_k where s_k is a materialised level-k vector (hooks only).
+[[maybe_unused]] static int op_restrict(mss_ctx* ctx, int k, const double* s, double* coarse) {
+  Level& f = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * f.ny * f.nz), s, f.t1, f.nx, f.ny, f.nz, 0, c.nx,
+         ctx->prm.scale, ctx->prm.interp);
+  return op_restrict_yz(ctx, k, coarse);
+}
+
+// z += E y on cells of `colour` (1 = black, the solver's case; -1 = all, hooks).
 static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int colour) {
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
-  DISPATCH(ctx->ndim, k_prolong_add, grid_for(f.N), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
-           ctx->prm.interp, y, z, colour);
+  if (colour == 1) {
+    const int64_t work = (int64_t)((f.nx + 1) / 2) * f.ny * f.nz;
+    DISPATCH(ctx->ndim, k_prolong_black, grid_for(work), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
+             ctx->prm.interp, y, z);
+  } else {
+    DISPATCH(ctx->ndim, k_prolong_add, grid_for(f.N), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
+             ctx->prm.interp, y, z, colour);
+  }
   return MSS_OK;
 }
 
@@ -254,20 +290,20 @@ static int precond(mss_ctx* ctx, int k) {
   Level& c = ctx->lv[k + 1];
   const int nh = 2 * ctx->prm.m + 1;
   TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));                 // pre-smoothing (a5)
-  TRY(op_residual(ctx, k, l.r, l.z, l.s, nullptr));              // s = r - A z (a6)
-  TRY(op_restrict(ctx, k, l.s, c.r));                            // b_{k+1} = R s
+  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, 1));              // b_{k+1} = R (r - A z) (a6)
   if (k + 1 == ctx->L) {                                         // coarsest: exact (a7)
     TRY(op_coarse_solve(ctx, c.r, c.x));
     ctx->info.iters[k + 1] += 1;
     ctx->info.calls[k + 1] += 1;
   } else if (c.N <= ctx->prm.tail_cells && tail_supported(ctx, k + 1)) {
+    ProfScope ps(ctx, KC_TAIL, k + 1, 0.0);
     TRY(tail_pcg(ctx, k + 1));                                   // device-resident coarse levels
   } else {
     CK(cudaMemsetAsync(c.x, 0, sizeof(double) * c.N, ctx->stream));
     TRY(pcg_level(ctx, k + 1));
   }
   TRY(op_prolong_add(ctx, k, c.x, l.z, 1));                      // z_black += (E y) (a8)
-  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false));                // post-smoothing (a9)
+  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho));  // post-smoothing (a9), rho = r.z
   return MSS_OK;
 }
 
@@ -282,8 +318,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
   if (ctx->hscal[k].rr < l.thr) return MSS_OK;
   int64_t it = 0;
   for (;;) {
-    TRY(precond(ctx, k));
-    TRY(op_dot(ctx, k, l.N, l.r, l.z, &ds->rho));                         // rho = r.z
+    TRY(precond(ctx, k));                                                  // z = M r, rho = r.z
     double* pin = l.p[l.pcur];
     double* pout = l.p[l.pcur ^ 1];
     {
@@ -787,8 +822,7 @@ int mss_residual_restrict(mss_ctx* ctx, int level, const double* r, const double
   Level& c = ctx->lv[level + 1];
   CK(cudaMemcpyAsync(l.r, r, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(l.z, z, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
-  TRY(op_residual(ctx, level, l.r, l.z, l.s, nullptr));
-  TRY(op_restrict(ctx, level, l.s, c.r));
+  TRY(op_resid_restrict(ctx, level, l.r, l.z, c.r, 0));
   CK(cudaMemcpyAsync(coarse_b, c.r, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return MSS_OK;

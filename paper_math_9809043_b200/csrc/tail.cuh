@@ -86,46 +86,50 @@ struct Tail {
     return tot;
   }
 
-  __device__ void sweep(int k, int colour, bool first) {
+  // one half-sweep; with dot, also returns r.z (cluster-reduced) of the result
+  __device__ double sweep(int k, int colour, bool first, bool dot = false) {
     const TLevel& l = A->lv[k];
     const uint32_t hx = (uint32_t)(l.g.nx + 1) >> 1;
     const uint32_t total = hx * (uint32_t)l.g.ny * (uint32_t)l.g.nz;
     if (first) {
-      for (uint32_t t = tid; t < total; t += nth) sweep_item<NDIM, true>(l.g, hx, t, l.r, l.z, colour);
+      for (uint32_t t = tid; t < total; t += nth) sweep_item<NDIM, true, false>(l.g, hx, t, l.r, l.z, colour);
+    } else if (dot) {
+      double acc = 0.0;
+      for (uint32_t t = tid; t < total; t += nth) acc += sweep_item<NDIM, false, true>(l.g, hx, t, l.r, l.z, colour);
+      return sum(acc);
     } else {
-      for (uint32_t t = tid; t < total; t += nth) sweep_item<NDIM, false>(l.g, hx, t, l.r, l.z, colour);
+      for (uint32_t t = tid; t < total; t += nth) sweep_item<NDIM, false, false>(l.g, hx, t, l.r, l.z, colour);
     }
     sync();
+    return 0.0;
   }
 
-  __device__ void smooth(int k, bool from_zero) {
+  __device__ double smooth(int k, bool from_zero, bool dot_last) {
     const int nh = 2 * A->m + 1;
-    for (int h = 0; h < nh; ++h) sweep(k, h & 1, from_zero && h == 0);
+    double d = 0.0;
+    for (int h = 0; h < nh; ++h) {
+      const bool first = from_zero && h == 0;
+      d = sweep(k, h & 1, first, dot_last && h == nh - 1 && !first);
+    }
+    return d;
   }
 
-  __device__ void residual(int k) {
-    const TLevel& l = A->lv[k];
-    for (int64_t c = tid; c < l.g.N; c += nth) residual_item<NDIM>(l.g, c, l.r, l.z, l.s);
-    sync();
-  }
-
-  __device__ void restrict_to(int k) {
+  // b_{k+1} = R (r - A z): residual fused into the x-pass (black cells only), then y, z.
+  __device__ void resid_restrict(int k) {
     const TLevel& f = A->lv[k];
     const TLevel& c = A->lv[k + 1];
     const int S = A->scale, kind = A->interp;
+    const uint32_t n1 = (uint32_t)c.g.nx * f.g.ny * f.g.nz;
+    for (uint32_t t = tid; t < n1; t += nth)
+      resid_restrict_x_item<NDIM>(f.g, f.r, f.z, f.t1, c.g.nx, S, kind, 1, t);
+    sync();
     if (NDIM == 3) {
-      const int64_t n1 = (int64_t)c.g.nx * f.g.ny * f.g.nz;
-      for (int64_t t = tid; t < n1; t += nth) restrict_item(f.s, f.t1, f.g.nx, f.g.ny, f.g.nz, 0, c.g.nx, S, kind, t);
-      sync();
       const int64_t n2 = (int64_t)c.g.nx * c.g.ny * f.g.nz;
       for (int64_t t = tid; t < n2; t += nth) restrict_item(f.t1, f.t2, c.g.nx, f.g.ny, f.g.nz, 1, c.g.ny, S, kind, t);
       sync();
       for (int64_t t = tid; t < c.g.N; t += nth) restrict_item(f.t2, c.r, c.g.nx, c.g.ny, f.g.nz, 2, c.g.nz, S, kind, t);
       sync();
     } else {
-      const int64_t n1 = (int64_t)c.g.nx * f.g.ny;
-      for (int64_t t = tid; t < n1; t += nth) restrict_item(f.s, f.t1, f.g.nx, f.g.ny, 1, 0, c.g.nx, S, kind, t);
-      sync();
       for (int64_t t = tid; t < c.g.N; t += nth) restrict_item(f.t1, c.r, c.g.nx, f.g.ny, 1, 1, c.g.ny, S, kind, t);
       sync();
     }
@@ -134,8 +138,10 @@ struct Tail {
   __device__ void prolong(int k) {
     const TLevel& f = A->lv[k];
     const TLevel& c = A->lv[k + 1];
-    for (int64_t t = tid; t < f.g.N; t += nth)
-      prolong_item<NDIM>(f.g, c.g.nx, c.g.ny, c.g.nz, A->scale, A->interp, c.x, f.z, 1, t);
+    const uint32_t hx = (uint32_t)(f.g.nx + 1) >> 1;
+    const uint32_t total = hx * (uint32_t)f.g.ny * (uint32_t)f.g.nz;
+    for (uint32_t t = tid; t < total; t += nth)
+      prolong_black_item<NDIM>(f.g, hx, c.g.nx, c.g.ny, c.g.nz, A->scale, A->interp, c.x, f.z, t);
     sync();
   }
 
@@ -159,11 +165,11 @@ struct Tail {
     if (tid == 0) arr[k] += v;
   }
 
+  // z = M_k r (Eq. 2.10 sequence); returns rho = r.z from the closing sweep.
   template <int D>
-  __device__ bool precond(int k) {
-    smooth(k, true);
-    residual(k);
-    restrict_to(k);
+  __device__ bool precond(int k, double& rho) {
+    smooth(k, true, false);
+    resid_restrict(k);
     if (k + 1 == A->L) {
       coarse();
       count(A->iters, k + 1, 1);
@@ -172,7 +178,7 @@ struct Tail {
       if (!pcg<D - 1>(k + 1)) return false;
     }
     prolong(k);
-    smooth(k, false);
+    rho = smooth(k, false, true);
     return true;
   }
 
@@ -197,10 +203,8 @@ struct Tail {
     double rho_prev = 1.0;
     int cur = 0;
     for (;;) {
-      if (!precond<D>(k)) return false;
-      acc = 0.0;
-      for (int64_t c = tid; c < l.g.N; c += nth) acc += l.r[c] * l.z[c];
-      const double rho = sum(acc);
+      double rho = 0.0;
+      if (!precond<D>(k, rho)) return false;
       double* pin = cur ? l.p1 : l.p0;
       double* pout = cur ? l.p0 : l.p1;
       const double beta = (it == 0) ? 0.0 : rho / rho_prev;
@@ -233,10 +237,10 @@ struct Tail {
 
 template <>
 template <>
-__device__ bool Tail<2>::precond<0>(int) { return false; }
+__device__ bool Tail<2>::precond<0>(int, double&) { return false; }
 template <>
 template <>
-__device__ bool Tail<3>::precond<0>(int) { return false; }
+__device__ bool Tail<3>::precond<0>(int, double&) { return false; }
 
 template <int NDIM>
 __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const TailArgs* __restrict__ A, int k0) {

@@ -100,7 +100,7 @@ SIGNATURES = [
 ]
 
 KCLASS = ["halfsweep", "halfsweep_first", "residual", "restrict", "prolong_add", "pdir_spmv_dot",
-          "axpy_norm", "dot", "coarse_solve", "other"]
+          "axpy_norm", "dot", "coarse_solve", "tail"]
 
 _lib = None
 

@@ -250,17 +250,18 @@ def test_solve_host_matches_device(torch_mod):
     assert torch.equal(xh, xd.cpu()) and rep2.iters == rep.iters
 
 
-@pytest.mark.parametrize("name", ["C2", "C4_32", "3d_ragged"])
+@pytest.mark.parametrize("name", ["C2", "C5_128", "C3_256"])
 def test_tail_kernel_matches_host_driven_levels(torch_mod, name):
     """The cluster-resident coarse levels (tail) and the host-driven grid kernels
     compute the same solve: identical counts, solutions within 1e-12."""
     torch = torch_mod
-    w = {"C2": lambda: make_workload("C2"), "C4_32": lambda: make_workload("C4", n=32),
-         "3d_ragged": CASES[1][1]}[name]()
+    w = {"C2": lambda: make_workload("C2"), "C5_128": lambda: make_workload("C5", n=128),
+         "C3_256": lambda: make_workload("C3", n=256)}[name]()
     from paper_math_9809043_b200.mss import Solver
     K = torch.from_numpy(w.K).cuda()
-    a = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params={"tail_cells": 0})
-    b = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params={"tail_cells": 1 << 20})
+    kw = {"use_lift": 0, "interp": 1} if name.startswith("C3") else {}
+    a = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params={"tail_cells": 0, **kw})
+    b = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params={"tail_cells": 1 << 20, **kw})
     xa, ra = a.solve(cu(torch, w.f), rel_tol=w.rel_tol)
     xb, rb = b.solve(cu(torch, w.f), rel_tol=w.rel_tol)
     assert ra.iters == rb.iters
