@@ -82,10 +82,36 @@ static RedOut red_to(mss_ctx* ctx, double* out, int level, int mode) {
   return ro;
 }
 
-#define LAUNCH(kern, grid, ...)                                       \
-  do {                                                                \
-    kern<<<(grid), kBlock, 0, ctx->stream>>>(__VA_ARGS__);            \
-    ctx->launches++;                                                  \
+// Streaming kernels run as ONE resident wave (grid = SMs x resident CTAs per SM, the
+// work strided over it): the working front then moves through the domain once, so
+// z-neighbour planes are still in L2 when reused.  A two-wave grid-stride launch let
+// each wave sweep the whole 512^3 domain and moved 1.5x the algorithmic bytes (ncu,
+// profiles/r01).
+static int wave_clamp(const void* kern, int grid) {
+  static std::vector<std::pair<const void*, int>> cache;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = kSMs;
+  }
+  int occ = 0;
+  for (auto& e : cache)
+    if (e.first == kern) occ = e.second;
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
+    cache.push_back({kern, occ});
+  }
+  const int w = occ * nsm;
+  return grid < w ? grid : (w < kMaxGrid ? w : kMaxGrid);
+}
+
+#define LAUNCH(kern, grid, ...)                                                          \
+  do {                                                                                   \
+    const int _g = wave_clamp((const void*)(kern), (grid));                              \
+    kern<<<_g, kBlock, 0, ctx->stream>>>(__VA_ARGS__);                                   \
+    ctx->launches++;                                                                     \
   } while (0)
 
 #define DISPATCH(ndim, kern, grid, ...)                               \
