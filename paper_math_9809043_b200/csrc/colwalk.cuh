@@ -1,0 +1,150 @@
+// colwalk.cuh — 2.5-D "column-walk" fine-grid kernels (3-D, n_x even).
+//
+// Each thread owns one red/black cell pair (2m, 2m+1) of one row j and walks z through a
+// chunk of planes.  Pairs move as 128-bit (double2) loads; the pair of plane k+1 loaded
+// for the upper z-neighbour is carried to the next step as the current pair, the
+// current pair becomes the lower neighbour, and the upper z-faces become the next lower
+// faces — so every array streams through HBM once per launch (the grid-stride item
+// kernels moved ~1.5x the algorithmic bytes: profiles/r01).
+//
+// Per-cell arithmetic is the same as the item bodies in kernels.cuh:
+//   half-sweep  z_c = (r_c + sum_f T_f z_nbr) / sum_f T_f      (O12)
+//   direction   p = z + beta p_in, q = A p, p.q               (a10)
+#pragma once
+#include "kernels.cuh"
+
+namespace mss {
+
+constexpr int kColX = 32;   // pairs per block in x (64 cells)
+constexpr int kColY = 8;    // rows per block
+
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double sel(const double2& v, int par) { return par ? v.y : v.x; }
+
+// Half-sweep of colour `colour` over planes [blockIdx.z * kchunk, +kchunk).
+template <bool FIRST, bool DOT>
+__global__ void __launch_bounds__(kColX * kColY) k_sweep_col(LevelDev L, const double* __restrict__ r,
+                                                              double* __restrict__ z, int colour, int kchunk,
+                                                              RedOut ro) {
+  const int m = blockIdx.x * kColX + threadIdx.x;
+  const int j = blockIdx.y * kColY + threadIdx.y;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(L.nz, k0 + kchunk);
+  const int nx = L.nx, ny = L.ny;
+  const int64_t plane = L.plane;
+  double acc = 0.0;
+  if (2 * m < nx && j < ny && k0 < k1) {
+    const int i0 = 2 * m;
+    const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
+    int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
+    double2 zdn = make_double2(0.0, 0.0), zc = make_double2(0.0, 0.0);
+    if (!FIRST) {
+      zdn = ld2(z + c - plane);            // plane k0-1 (ghost plane when k0 == 0)
+      zc = ld2(z + c);
+    }
+    double2 tzl = ldg2(L.Tz + c);
+    for (int k = k0; k < k1; ++k) {
+      const int par = (i0 + j + k + L.z0 + colour) & 1;   // updated cell: i0 + par
+      const int64_t row = j + (int64_t)ny * k;
+      const int64_t fx = c + row;
+      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
+      const int64_t fy = c + (int64_t)nx * k;
+      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
+      const double2 tzu = ldg2(L.Tz + c + plane);
+      const double2 rr = ld2(r + c);
+      const double txl = par ? tx1 : tx0, txh = par ? tx2 : tx1;
+      const double t2 = sel(tyl, par), t3 = sel(tyu, par), t4 = sel(tzl, par), t5 = sel(tzu, par);
+      const double rp = sel(rr, par);
+      double zup_x = 0.0, zup_y = 0.0;
+      double acc_c = rp;
+      if (!FIRST) {
+        const double2 zup = ld2(z + c + plane);
+        zup_x = zup.x;
+        zup_y = zup.y;
+        double xl, xh;
+        if (par) {
+          xl = zc.x;
+          xh = hasR ? z[c + 2] : 0.0;
+        } else {
+          xl = hasL ? z[c - 1] : 0.0;
+          xh = zc.y;
+        }
+        const double ys = hasS ? sel(ld2(z + c - nx), par) : 0.0;
+        const double yn = hasN ? sel(ld2(z + c + nx), par) : 0.0;
+        acc_c += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * (par ? zup_y : zup_x);
+      }
+      const double zn = acc_c / (txl + txh + t2 + t3 + t4 + t5);
+      z[c + par] = zn;
+      if (DOT) acc += rp * zn + sel(rr, 1 - par) * sel(zc, 1 - par);
+      if (!FIRST) {
+        zdn = zc;
+        zc = make_double2(zup_x, zup_y);
+      }
+      tzl = tzu;
+      c += plane;
+    }
+  }
+  if (DOT) grid_sum_finish_2d(acc, ro);
+}
+
+// a10 column-walk: p_out = z + beta p_in (p = z when first); q = A p_out; p.q reduced.
+// Neighbour p values are formed on the fly from z and p_in (never from p_out), so the
+// pass has no intra-launch dependency.
+__global__ void __launch_bounds__(kColX * kColY) k_spmv_col(LevelDev L, const double* __restrict__ z,
+                                                             const double* __restrict__ pin, double* __restrict__ pout,
+                                                             double* __restrict__ q, const Scal* sc, int first,
+                                                             int kchunk, RedOut ro) {
+  const int m = blockIdx.x * kColX + threadIdx.x;
+  const int j = blockIdx.y * kColY + threadIdx.y;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(L.nz, k0 + kchunk);
+  const int nx = L.nx, ny = L.ny;
+  const int64_t plane = L.plane;
+  const double beta = first ? 0.0 : sc->rho / sc->rho_prev;
+  double acc = 0.0;
+  if (2 * m < nx && j < ny && k0 < k1) {
+    const int i0 = 2 * m;
+    const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
+    int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
+    auto P2 = [&](int64_t idx) {
+      const double2 zz = ld2(z + idx);
+      if (first) return zz;
+      const double2 pp = ld2(pin + idx);
+      return make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
+    };
+    auto P1 = [&](int64_t idx) { return first ? z[idx] : z[idx] + beta * pin[idx]; };
+    double2 pdn = P2(c - plane);
+    double2 pc = P2(c);
+    double2 tzl = ldg2(L.Tz + c);
+    for (int k = k0; k < k1; ++k) {
+      const int64_t row = j + (int64_t)ny * k;
+      const int64_t fx = c + row;
+      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
+      const int64_t fy = c + (int64_t)nx * k;
+      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
+      const double2 tzu = ldg2(L.Tz + c + plane);
+      const double2 pup = P2(c + plane);
+      const double2 ps = hasS ? P2(c - nx) : make_double2(0.0, 0.0);
+      const double2 pn = hasN ? P2(c + nx) : make_double2(0.0, 0.0);
+      const double pl = hasL ? P1(c - 1) : 0.0;
+      const double pr = hasR ? P1(c + 2) : 0.0;
+      // cell i0 (x), cell i0+1 (y): q = diag p - sum T p_nbr
+      const double d0 = tx0 + tx1 + tyl.x + tyu.x + tzl.x + tzu.x;
+      const double d1 = tx1 + tx2 + tyl.y + tyu.y + tzl.y + tzu.y;
+      const double s0 = tx0 * pl + tx1 * pc.y + tyl.x * ps.x + tyu.x * pn.x + tzl.x * pdn.x + tzu.x * pup.x;
+      const double s1 = tx1 * pc.x + tx2 * pr + tyl.y * ps.y + tyu.y * pn.y + tzl.y * pdn.y + tzu.y * pup.y;
+      const double q0 = d0 * pc.x - s0, q1 = d1 * pc.y - s1;
+      *reinterpret_cast<double2*>(pout + c) = pc;
+      *reinterpret_cast<double2*>(q + c) = make_double2(q0, q1);
+      acc += pc.x * q0 + pc.y * q1;
+      pdn = pc;
+      pc = pup;
+      tzl = tzu;
+      c += plane;
+    }
+  }
+  grid_sum_finish_2d(acc, ro);
+}
+
+}  // namespace mss

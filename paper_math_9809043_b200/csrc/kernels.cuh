@@ -21,17 +21,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int lin_nthreads() { return blockDim.x * blockDim.y * blockDim.z; }
+__device__ __forceinline__ int lin_bid() { return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); }
+__device__ __forceinline__ int lin_nblocks() { return gridDim.x * gridDim.y * gridDim.z; }
+
 // Block sum, fixed order (warp shuffles, then warp 0 over the warp partials); the
-// result is valid in thread 0.
+// result is valid in thread 0.  Works for 1-, 2- and 3-D blocks.
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double sh[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = lin_tid();
+  const int lane = t & 31, w = t >> 5;
   v = warp_sum(v);
   __syncthreads();
   if (lane == 0) sh[w] = v;
   __syncthreads();
-  const int nw = (blockDim.x + 31) >> 5;
-  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  const int nw = (lin_nthreads() + 31) >> 5;
+  v = (t < nw) ? sh[t] : 0.0;
   if (w == 0) v = warp_sum(v);
   return v;
 }
@@ -50,26 +56,28 @@ struct RedOut {
 // arrive sums the partials in block order (deterministic for a fixed grid).
 __device__ __forceinline__ void grid_sum_finish(double v, const RedOut& ro) {
   __shared__ int s_last;
+  const int t = lin_tid(), nb = lin_nblocks();
   double bsum = block_sum(v);
-  if (threadIdx.x == 0) {
-    ro.partials[blockIdx.x] = bsum;
+  if (t == 0) {
+    ro.partials[lin_bid()] = bsum;
     __threadfence();
-    unsigned t = atomicAdd(ro.counter, 1u);
-    s_last = (t == gridDim.x - 1);
+    unsigned old = atomicAdd(ro.counter, 1u);
+    s_last = (old == (unsigned)nb - 1);
   }
   __syncthreads();
   if (s_last) {
     __threadfence();
     double acc = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) acc += __ldcg(&ro.partials[i]);
+    for (int i = t; i < nb; i += lin_nthreads()) acc += __ldcg(&ro.partials[i]);
     acc = block_sum(acc);
-    if (threadIdx.x == 0) {
+    if (t == 0) {
       *ro.out = acc;
       if (ro.mode == 1) ro.scal->rho_prev = ro.scal->rho;
       *ro.counter = 0;
     }
   }
 }
+__device__ __forceinline__ void grid_sum_finish_2d(double v, const RedOut& ro) { grid_sum_finish(v, ro); }
 
 // ------------------------------------------------------------------ cell geometry
 struct Cell {

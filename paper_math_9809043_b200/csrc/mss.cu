@@ -12,12 +12,14 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "internal.cuh"
 #include "kernels.cuh"
+#include "colwalk.cuh"
 
 using namespace mss;
 
@@ -105,6 +107,46 @@ static int wave_clamp(const void* kern, int grid) {
   }
   const int w = occ * nsm;
   return grid < w ? grid : (w < kMaxGrid ? w : kMaxGrid);
+}
+
+static int occupancy_of(const void* kern, int threads) {
+  static std::vector<std::pair<const void*, int>> cache;
+  for (auto& e : cache)
+    if (e.first == kern) return e.second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  cache.push_back({kern, occ});
+  return occ;
+}
+
+// Column-walk kernels (colwalk.cuh) for 3-D levels with even n_x: grid = (pairs/32,
+// rows/8, z-chunks) with the chunk count chosen so the grid is one resident wave.
+static bool col_ok(const mss_ctx* ctx, const Level& l) {
+  static int disabled = -1;
+  if (disabled < 0) disabled = getenv("MSS_NO_COLWALK") ? 1 : 0;
+  return !disabled && ctx->ndim == 3 && (l.nx % 2) == 0 && l.N >= 32768;
+}
+
+static bool col_grid(const void* kern, const Level& l, dim3* grid, int* kchunk) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = kSMs;
+  }
+  const int bx = (l.nx / 2 + kColX - 1) / kColX, by = (l.ny + kColY - 1) / kColY;
+  const int layer = bx * by;
+  if (layer > kMaxGrid) return false;
+  const int resident = occupancy_of(kern, kColX * kColY) * nsm;
+  int nch = resident / layer;
+  if (nch < 1) nch = 1;
+  if (nch > l.nz) nch = l.nz;
+  if (nch * layer > kMaxGrid) nch = kMaxGrid / layer;
+  *kchunk = (l.nz + nch - 1) / nch;
+  nch = (l.nz + *kchunk - 1) / *kchunk;
+  *grid = dim3(bx, by, nch);
+  return true;
 }
 
 #define LAUNCH(kern, grid, ...)                                                          \
@@ -212,6 +254,20 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   ProfScope ps(ctx, cls, k, cell_bytes(ctx, cls) * l.N);
   RedOut ro = red_to(ctx, dot_out, k, 0);
   const LevelDev d = l.dev();
+  if (col_ok(ctx, l)) {
+    const void* kern = first ? (const void*)k_sweep_col<true, false>
+                             : (dot_out ? (const void*)k_sweep_col<false, true> : (const void*)k_sweep_col<false, false>);
+    dim3 grid;
+    int kch = 0;
+    if (col_grid(kern, l, &grid, &kch)) {
+      const dim3 blk(kColX, kColY);
+      if (first) k_sweep_col<true, false><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);
+      else if (dot_out) k_sweep_col<false, true><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);
+      else k_sweep_col<false, false><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);
+      ctx->launches++;
+      return MSS_OK;
+    }
+  }
 #define HS(ND, F, D) LAUNCH((k_halfsweep<ND, F, D>), g, d, r, z, colour, ro)
   if (ctx->ndim == 3) {
     if (first) HS(3, true, false);
@@ -349,6 +405,13 @@ static int pcg_level(mss_ctx* ctx, int k) {
     double* pout = l.p[l.pcur ^ 1];
     {
     ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV) * l.N);
+    dim3 cgrid;
+    int kch = 0;
+    if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col, l, &cgrid, &kch)) {
+      k_spmv_col<<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
+                                                                 kch, red_to(ctx, &ds->pq, k, 0));
+      ctx->launches++;
+    } else
     DISPATCH(ctx->ndim, k_pdir_spmv_dot, grid_for(l.N), l.dev(), l.z, pin, pout, l.q, ds,
              it == 0 ? 1 : 0, red_to(ctx, &ds->pq, k, 0));                 // a10
     }
