@@ -17,14 +17,15 @@ namespace mss {
 
 constexpr int kColX = 32;   // pairs per block in x (64 cells)
 constexpr int kColY = 8;    // rows per block
+constexpr int kColChunk = 32;  // planes walked per thread (default chunk)
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double sel(const double2& v, int par) { return par ? v.y : v.x; }
 
 // Half-sweep of colour `colour` over planes [blockIdx.z * kchunk, +kchunk).
-template <bool FIRST, bool DOT>
-__global__ void __launch_bounds__(kColX * kColY) k_sweep_col(LevelDev L, const double* __restrict__ r,
+template <bool FIRST, bool DOT, int MINB>
+__global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, const double* __restrict__ r,
                                                               double* __restrict__ z, int colour, int kchunk,
                                                               RedOut ro) {
   const int m = blockIdx.x * kColX + threadIdx.x;
@@ -91,7 +92,8 @@ __global__ void __launch_bounds__(kColX * kColY) k_sweep_col(LevelDev L, const d
 // a10 column-walk: p_out = z + beta p_in (p = z when first); q = A p_out; p.q reduced.
 // Neighbour p values are formed on the fly from z and p_in (never from p_out), so the
 // pass has no intra-launch dependency.
-__global__ void __launch_bounds__(kColX * kColY) k_spmv_col(LevelDev L, const double* __restrict__ z,
+template <int MINB>
+__global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, const double* __restrict__ z,
                                                              const double* __restrict__ pin, double* __restrict__ pout,
                                                              double* __restrict__ q, const Scal* sc, int first,
                                                              int kchunk, RedOut ro) {
@@ -145,6 +147,131 @@ __global__ void __launch_bounds__(kColX * kColY) k_spmv_col(LevelDev L, const do
     }
   }
   grid_sum_finish_2d(acc, ro);
+}
+
+// a6 column-walk, residual + x-restriction fused: one CTA per row j walks a chunk of
+// planes; thread m owns pair (2m, 2m+1) and evaluates the residual of its BLACK cell
+// (the red residual is zero after the closing red sweep); the x-weighted
+// contributions meet in shared memory and thread I sums the pairs of coarse cell I in
+// a fixed order (deterministic).  t1 has dims (ncx, ny, nz).
+template <int MINB>
+__global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, const double* __restrict__ r,
+                                                                  const double* __restrict__ z,
+                                                                  double* __restrict__ t1, int ncx, int s, int kind,
+                                                                  int kchunk) {
+  extern __shared__ double shc[];             // [2 * hx] contributions
+  int* shi = reinterpret_cast<int*>(shc + 2 * blockDim.x);   // [2 * hx] coarse indices (per parity: 4 * hx)
+  const int nx = L.nx, ny = L.ny;
+  const int hx = nx >> 1;
+  const int m = threadIdx.x;
+  const int j = blockIdx.x;
+  const int k0 = blockIdx.y * kchunk;
+  const int k1 = min(L.nz, k0 + kchunk);
+  const int64_t plane = L.plane;
+  const bool act = m < hx;
+  const int i0 = 2 * m;
+  // x-weights of both cells of the pair (the black one alternates with k)
+  int Ia0 = 0, Ia1 = 0, Ib0 = 0, Ib1 = 0;
+  double wa0 = 0, wa1 = 0, wb0 = 0, wb1 = 0;
+  if (act) {
+    interp_w(i0, ncx, s, kind, Ia0, wa0, Ia1, wa1);
+    interp_w(i0 + 1, ncx, s, kind, Ib0, wb0, Ib1, wb1);
+    if (Ia1 == Ia0) wa1 = 0.0;
+    if (Ib1 == Ib0) wb1 = 0.0;
+  }
+  const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
+  int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
+  double2 zdn = make_double2(0, 0), zc = make_double2(0, 0), tzl = make_double2(0, 0);
+  if (act && k0 < k1) {
+    zdn = ld2(z + c - plane);
+    zc = ld2(z + c);
+    tzl = ldg2(L.Tz + c);
+  }
+  for (int k = k0; k < k1; ++k) {
+    const int par = (i0 + j + k + L.z0 + 1) & 1;   // black cell of the pair: i0 + par
+    double2 zup = make_double2(0, 0), tzu = make_double2(0, 0);
+    if (act) {
+      const int64_t row = j + (int64_t)ny * k;
+      const int64_t fx = c + row;
+      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
+      const int64_t fy = c + (int64_t)nx * k;
+      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
+      tzu = ldg2(L.Tz + c + plane);
+      const double2 rr = ld2(r + c);
+      zup = ld2(z + c + plane);
+      const double txl = par ? tx1 : tx0, txh = par ? tx2 : tx1;
+      const double t2 = sel(tyl, par), t3 = sel(tyu, par), t4 = sel(tzl, par), t5 = sel(tzu, par);
+      double xl, xh;
+      if (par) {
+        xl = zc.x;
+        xh = hasR ? z[c + 2] : 0.0;
+      } else {
+        xl = hasL ? z[c - 1] : 0.0;
+        xh = zc.y;
+      }
+      const double ys = hasS ? sel(ld2(z + c - nx), par) : 0.0;
+      const double yn = hasN ? sel(ld2(z + c + nx), par) : 0.0;
+      const double nb = txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * sel(zup, par);
+      const double res = sel(rr, par) - ((txl + txh + t2 + t3 + t4 + t5) * sel(zc, par) - nb);
+      shc[2 * m] = (par ? wb0 : wa0) * res;
+      shc[2 * m + 1] = (par ? wb1 : wa1) * res;
+      shi[2 * m] = par ? Ib0 : Ia0;
+      shi[2 * m + 1] = par ? Ib1 : Ia1;
+    }
+    __syncthreads();
+    const int64_t obase = (int64_t)ncx * (j + (int64_t)ny * k);
+    for (int I = threadIdx.x; I < ncx; I += blockDim.x) {
+      const int mlo = max(0, (s * (I - 1)) >> 1), mhi = min(hx, (s * (I + 2) + 1) >> 1);
+      double acc = 0.0;
+      for (int q = mlo; q < mhi; ++q) {
+        if (shi[2 * q] == I) acc += shc[2 * q];
+        if (shi[2 * q + 1] == I) acc += shc[2 * q + 1];
+      }
+      t1[obase + I] = acc;
+    }
+    __syncthreads();
+    zdn = zc;
+    zc = zup;
+    tzl = tzu;
+    c += plane;
+  }
+}
+
+// a8 column-walk: z_black += (E y)_black, thread per pair walking z.
+template <int MINB>
+__global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L, int ncx, int ncy, int ncz, int s,
+                                                                      int kind, const double* __restrict__ y,
+                                                                      double* __restrict__ z, int kchunk) {
+  const int m = blockIdx.x * kColX + threadIdx.x;
+  const int j = blockIdx.y * kColY + threadIdx.y;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(L.nz, k0 + kchunk);
+  const int nx = L.nx, ny = L.ny;
+  if (2 * m >= nx || j >= ny || k0 >= k1) return;
+  const int i0 = 2 * m;
+  int Xa0, Xa1, Xb0, Xb1, Y0, Y1;
+  double wxa0, wxa1, wxb0, wxb1, wy0, wy1;
+  interp_w(i0, ncx, s, kind, Xa0, wxa0, Xa1, wxa1);
+  interp_w(i0 + 1, ncx, s, kind, Xb0, wxb0, Xb1, wxb1);
+  interp_w(j, ncy, s, kind, Y0, wy0, Y1, wy1);
+  const int64_t cp = (int64_t)ncx * ncy;
+  int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
+  for (int k = k0; k < k1; ++k) {
+    const int par = (i0 + j + k + L.z0 + 1) & 1;
+    const int X0 = par ? Xb0 : Xa0, X1 = par ? Xb1 : Xa1;
+    const double wx0 = par ? wxb0 : wxa0, wx1 = par ? wxb1 : wxa1;
+    int Z0, Z1;
+    double wz0, wz1;
+    interp_w(k, ncz, s, kind, Z0, wz0, Z1, wz1);
+    auto Yv = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * cc); };
+    double acc = wy0 * (wx0 * Yv(X0, Y0, Z0) + wx1 * Yv(X1, Y0, Z0)) +
+                 wy1 * (wx0 * Yv(X0, Y1, Z0) + wx1 * Yv(X1, Y1, Z0));
+    acc *= wz0;
+    acc += wz1 * (wy0 * (wx0 * Yv(X0, Y0, Z1) + wx1 * Yv(X1, Y0, Z1)) +
+                  wy1 * (wx0 * Yv(X0, Y1, Z1) + wx1 * Yv(X1, Y1, Z1)));
+    z[c + par] += acc;
+    c += L.plane;
+  }
 }
 
 }  // namespace mss

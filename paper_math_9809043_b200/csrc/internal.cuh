@@ -22,6 +22,7 @@ namespace mss {
 constexpr int kBlock = 256;           // threads per CTA for the streaming kernels
 constexpr int kSMs = 148;             // B200
 constexpr int kMaxGrid = kSMs * 16;   // grid-stride cap: 16 CTAs of 256 per SM in flight
+constexpr int kMaxPartials = 65536;   // reduction partials (any grid up to this many CTAs)
 
 // Per-level CG scalars, resident on the device (one 64-byte record per level).
 struct Scal {

@@ -9,6 +9,7 @@
 // excursion is decided dynamically.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -137,12 +138,19 @@ static bool col_grid(const void* kern, const Level& l, dim3* grid, int* kchunk) 
   }
   const int bx = (l.nx / 2 + kColX - 1) / kColX, by = (l.ny + kColY - 1) / kColY;
   const int layer = bx * by;
-  if (layer > kMaxGrid) return false;
+  if (layer > kMaxPartials) return false;
   const int resident = occupancy_of(kern, kColX * kColY) * nsm;
-  int nch = resident / layer;
+  // Short walks (~32 planes per thread) with many more CTAs than one wave measured best
+  // on B200 (half-sweep 6.5 TB/s at 32-plane chunks vs 4.7 TB/s at 1 chunk, profiles/r01);
+  // at least one full wave either way.
+  int nch = (l.nz + kColChunk - 1) / kColChunk;
+  if (nch * layer < resident) nch = (resident + layer - 1) / layer;
+  static int force = -1;
+  if (force < 0) force = getenv("MSS_COL_NCH") ? atoi(getenv("MSS_COL_NCH")) : 0;
+  if (force > 0) nch = force;
   if (nch < 1) nch = 1;
   if (nch > l.nz) nch = l.nz;
-  if (nch * layer > kMaxGrid) nch = kMaxGrid / layer;
+  if (nch * layer > kMaxPartials) nch = kMaxPartials / layer;
   *kchunk = (l.nz + nch - 1) / nch;
   nch = (l.nz + *kchunk - 1) / *kchunk;
   *grid = dim3(bx, by, nch);
@@ -255,18 +263,26 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   RedOut ro = red_to(ctx, dot_out, k, 0);
   const LevelDev d = l.dev();
   if (col_ok(ctx, l)) {
-    const void* kern = first ? (const void*)k_sweep_col<true, false>
-                             : (dot_out ? (const void*)k_sweep_col<false, true> : (const void*)k_sweep_col<false, false>);
-    dim3 grid;
-    int kch = 0;
-    if (col_grid(kern, l, &grid, &kch)) {
-      const dim3 blk(kColX, kColY);
-      if (first) k_sweep_col<true, false><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);
-      else if (dot_out) k_sweep_col<false, true><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);
-      else k_sweep_col<false, false><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);
-      ctx->launches++;
-      return MSS_OK;
+    static int minb = -1;
+    if (minb < 0) minb = getenv("MSS_COL_MINB") ? atoi(getenv("MSS_COL_MINB")) : 4;  // 64 regs: measured best
+#define SWEEPCOL(MB)                                                                                        \
+    {                                                                                                       \
+      const void* kern = first ? (const void*)k_sweep_col<true, false, MB>                                 \
+                               : (dot_out ? (const void*)k_sweep_col<false, true, MB>                       \
+                                          : (const void*)k_sweep_col<false, false, MB>);                    \
+      dim3 grid;                                                                                            \
+      int kch = 0;                                                                                          \
+      if (col_grid(kern, l, &grid, &kch)) {                                                                 \
+        const dim3 blk(kColX, kColY);                                                                       \
+        if (first) k_sweep_col<true, false, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);   \
+        else if (dot_out) k_sweep_col<false, true, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro); \
+        else k_sweep_col<false, false, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);       \
+        ctx->launches++;                                                                                    \
+        return MSS_OK;                                                                                      \
+      }                                                                                                     \
     }
+    if (minb <= 3) SWEEPCOL(3) else if (minb == 4) SWEEPCOL(4) else SWEEPCOL(5)
+#undef SWEEPCOL
   }
 #define HS(ND, F, D) LAUNCH((k_halfsweep<ND, F, D>), g, d, r, z, colour, ro)
   if (ctx->ndim == 3) {
@@ -318,6 +334,18 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
   {
     const double by = 8.0 * (ctx->ndim + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
     ProfScope ps(ctx, KC_RESID, k, by);
+    const int hx = f.nx / 2;
+    if (black_only && col_ok(ctx, f) && hx >= 32 && hx <= 512) {
+      const int bt = (hx + 31) / 32 * 32;
+      int nch = (f.nz + kColChunk - 1) / kColChunk;
+      if ((int64_t)nch * f.ny < 2 * kSMs * 4) nch = std::min<int>(f.nz, (2 * kSMs * 4 + f.ny - 1) / f.ny);
+      const int kch = (f.nz + nch - 1) / nch;
+      nch = (f.nz + kch - 1) / kch;
+      const size_t shm = (size_t)bt * 2 * (sizeof(double) + sizeof(int));
+      k_resid_restrict_col<2><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(f.dev(), r, z, f.t1, c.nx, ctx->prm.scale,
+                                                                          ctx->prm.interp, kch);
+      ctx->launches++;
+    } else
     DISPATCH(ctx->ndim, k_resid_restrict_x, grid_for((int64_t)c.nx * f.ny * f.nz), f.dev(), r, z, f.t1, c.nx,
              ctx->prm.scale, ctx->prm.interp, black_only);
   }
@@ -338,7 +366,13 @@ static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int c
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
-  if (colour == 1) {
+  dim3 cgrid;
+  int kch = 0;
+  if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && col_grid((const void*)k_prolong_col<4>, f, &cgrid, &kch)) {
+    k_prolong_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
+                                                                     ctx->prm.interp, y, z, kch);
+    ctx->launches++;
+  } else if (colour == 1) {
     const int64_t work = (int64_t)((f.nx + 1) / 2) * f.ny * f.nz;
     DISPATCH(ctx->ndim, k_prolong_black, grid_for(work), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
              ctx->prm.interp, y, z);
@@ -407,8 +441,8 @@ static int pcg_level(mss_ctx* ctx, int k) {
     ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV) * l.N);
     dim3 cgrid;
     int kch = 0;
-    if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col, l, &cgrid, &kch)) {
-      k_spmv_col<<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
+    if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
+      k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
                                                                  kch, red_to(ctx, &ds->pq, k, 0));
       ctx->launches++;
     } else
@@ -631,7 +665,7 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   TRY(dalloc(ctx, (void**)&ctx->dscal, sizeof(Scal) * MSS_MAX_LEVELS));
   CK(cudaMemsetAsync(ctx->dscal, 0, sizeof(Scal) * MSS_MAX_LEVELS, ctx->stream));
   CK(cudaMallocHost((void**)&ctx->hscal, sizeof(Scal) * MSS_MAX_LEVELS));
-  TRY(dalloc(ctx, (void**)&ctx->partials, sizeof(double) * kMaxGrid));
+  TRY(dalloc(ctx, (void**)&ctx->partials, sizeof(double) * kMaxPartials));
   TRY(dalloc(ctx, (void**)&ctx->counter, sizeof(unsigned) * 4));
   CK(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned) * 4, ctx->stream));
   TRY(dalloc(ctx, (void**)&ctx->dflag, sizeof(int) * 4));
