@@ -121,6 +121,13 @@ struct mss_ctx {
   long long* tail_cnt = nullptr;           // [2 * MSS_MAX_LEVELS] iters, calls
   int* tail_flags = nullptr;               // [0] not converged, [1] breakdown level + 1
   bool tail_dirty = true;
+  // shared-memory-resident tail (tailsm.cuh)
+  int tsm_L0 = -1;                         // top level it serves, -1 = unavailable
+  int tsm_cs = 0;
+  size_t tsm_shm = 0;
+  void* tsm_d = nullptr;
+  std::vector<char> tsm_h;
+  bool tsm_dirty = true;
   // distributed (rank/nranks == 0/1 single GPU)
   int rank = 0, nranks = 1;
 };

@@ -16,6 +16,7 @@
 
 #include "internal.cuh"
 #include "kernels.cuh"
+#include "tailsm.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -291,6 +292,7 @@ static int tail_setup(mss_ctx* ctx) {
   cudaMemsetAsync(ctx->tail_flags, 0, sizeof(int) * 2, ctx->stream);
   ctx->tail_h.assign(sizeof(mss::TailArgs), 0);
   ctx->tail_dirty = true;
+  tailsm_setup(ctx);
   return MSS_OK;
 }
 
@@ -298,9 +300,13 @@ static bool tail_supported(mss_ctx* ctx, int k) {
   return ctx->tail_cs > 0 && k >= 1 && k < ctx->L && ctx->lv[k].N <= ctx->prm.tail_cells;
 }
 
-static void tail_mark_dirty(mss_ctx* ctx) { ctx->tail_dirty = true; }
+static void tail_mark_dirty(mss_ctx* ctx) {
+  ctx->tail_dirty = true;
+  ctx->tsm_dirty = true;
+}
 
 static int tail_pcg(mss_ctx* ctx, int k) {
+  if (k == ctx->tsm_L0) return tailsm_launch(ctx, k);
   if (ctx->tail_dirty) {
     mss::TailArgs& a = *reinterpret_cast<mss::TailArgs*>(ctx->tail_h.data());
     a.k0 = 0;

@@ -1,0 +1,632 @@
+// tailsm.cuh — shared-memory-resident device tail (K13 v2).
+//
+// The recursive PCG of levels L0..L (Eq. 2.10 recursion; per-level stop
+// P:448-456) runs inside ONE launch of a 16-CTA thread-block cluster, with every level
+// vector and face array of those levels held in the CTAs' shared memory: CTA r owns the
+// outer slices [r*ppc, (r+1)*ppc) (z-planes in 3-D, y-rows in 2-D) of every level, and a
+// neighbour in another CTA is read through distributed shared memory (DSMEM).  Faces
+// are staged from HBM once per launch.  Passes are separated by cluster barriers and
+// CG scalars are reduced through DSMEM in rank order, so every CTA takes identical
+// decisions.  Used when level L0 fits (~2.7K cells per CTA); tail.cuh (L2-resident)
+// covers larger tails.
+//
+// Per-cell arithmetic follows the item bodies of kernels.cuh (same formulas, same
+// operand order): half-sweep P:353-357, residual O4, transfer P:412-428, CG P:440-441.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mss {
+
+constexpr int kTsThreads = 512;
+constexpr int kTsMaxLv = 8;
+
+struct TsLevel {
+  int nx, ny, nz;      // dims of the level
+  int P;               // cells per outer slice: nx*ny (3-D) | nx (2-D)
+  int no;              // outer extent: nz (3-D) | ny (2-D)
+  int ppc;             // outer slices per CTA
+  int cap;             // ppc * P
+  // shared-memory offsets (doubles)
+  int o_tx, o_ty, o_tz, o_dg, o_x, o_r, o_z, o_p0, o_p1, o_q, o_t1, o_t2;
+  int t1_slice, t2_slice;   // elements per outer slice of t1 / t2
+  int ncx, ncy, ncz;   // dims of the next level
+  double thr;
+  const double *Tx, *Ty, *Tz;   // HBM faces (staged at launch)
+};
+
+struct TsArgs {
+  int L0, L, ndim, m, s, interp, max_iter, NL;
+  const double* Ainv;
+  const double* r_in;   // HBM r of level L0 (the restricted residual)
+  double* x_out;        // HBM x of level L0 (read by the prolongation above)
+  long long* iters;     // [MSS_MAX_LEVELS]
+  long long* calls;
+  int* flags;
+  int o_rfull;          // replicated full r_L (NL doubles)
+  int o_red;            // reduction scratch (40 doubles)
+  int smem_doubles;
+  TsLevel lv[kTsMaxLv]; // index = level - L0
+};
+
+template <int NDIM>
+struct TailSm {
+  const TsArgs* __restrict__ A;
+  cg::cluster_group cl;
+  double* sm;
+  int rank, cs;
+  int phase;
+
+  __device__ TailSm(const TsArgs* a, double* s) : A(a), cl(cg::this_cluster()), sm(s), phase(0) {
+    rank = (int)cl.block_rank();
+    cs = (int)cl.num_blocks();
+  }
+  __device__ __forceinline__ void sync() { cl.sync(); }
+  __device__ __forceinline__ const TsLevel& lvl(int q) const { return A->lv[q - A->L0]; }
+
+  // outer-slice range owned by this CTA
+  __device__ __forceinline__ int olo(const TsLevel& l) const { return min(l.no, rank * l.ppc); }
+  __device__ __forceinline__ int ohi(const TsLevel& l) const { return min(l.no, (rank + 1) * l.ppc); }
+
+  // address of element `in` (index inside an outer slice of `slice` elements) of outer
+  // slice `o` of the distributed array at offset `off`
+  __device__ __forceinline__ double* at(int off, int slice, int ppc, int o, int in) {
+    const int own = o / ppc;
+    double* p = sm + off + (o - own * ppc) * slice + in;
+    return own == rank ? p : cl.map_shared_rank(p, own);
+  }
+  // cell (i, j, k) of a level array
+  __device__ __forceinline__ double* cell(const TsLevel& l, int off, int i, int j, int k) {
+    if (NDIM == 3) return at(off, l.P, l.ppc, k, i + l.nx * j);
+    return at(off, l.P, l.ppc, j, i);
+  }
+
+  // cluster-wide sum, identical bits in every CTA
+  __device__ double sum(double v) {
+    double* red_w = sm + A->o_red;
+    double* slot = red_w + 32;
+    double* bc = red_w + 34;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red_w[w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red_w[i];
+      slot[phase] = s;
+    }
+    sync();
+    if (w == 0) {
+      double pv = (lane < cs) ? *cl.map_shared_rank(&slot[phase], lane) : 0.0;
+      pv = warp_sum(pv);
+      if (lane == 0) *bc = pv;
+    }
+    __syncthreads();
+    const double t = *bc;
+    phase ^= 1;
+    return t;
+  }
+
+  // ---------------------------------------------------------------- staging
+  __device__ void stage(int q) {
+    const TsLevel& l = lvl(q);
+    if (q == A->L) return;
+    const int o0 = olo(l), o1 = ohi(l);
+    const int n = (o1 - o0) * l.P;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      int i, j, k;
+      if (NDIM == 3) {
+        const int kk = t / l.P, in = t - kk * l.P;
+        j = in / l.nx; i = in - j * l.nx; k = o0 + kk;
+      } else {
+        const int jj = t / l.nx;
+        i = t - jj * l.nx; j = o0 + jj; k = 0;
+      }
+      const int64_t c = i + (int64_t)l.nx * (j + (int64_t)l.ny * k);
+      const int64_t row = j + (int64_t)l.ny * k;
+      const double t0 = l.Tx[c + row], t1 = l.Tx[c + row + 1];
+      const double t2 = l.Ty[c + (int64_t)l.nx * k], t3 = l.Ty[c + (int64_t)l.nx * k + l.nx];
+      double t4 = 0.0, t5 = 0.0;
+      if (NDIM == 3) {
+        t4 = l.Tz[c];
+        t5 = l.Tz[c + (int64_t)l.P];
+      }
+      sm[l.o_tx + t] = t0;
+      sm[l.o_ty + t] = t2;
+      sm[l.o_tz + t] = t4;
+      double d = t0 + t1 + t2 + t3;
+      if (NDIM == 3) d += t4 + t5;
+      sm[l.o_dg + t] = d;
+    }
+  }
+
+  // sum_f T_f v_nbr for local cell t = (i, j, k) of level l (array at offset `off`);
+  // operand order as nbr_sum in kernels.cuh.
+  __device__ __forceinline__ double nbr(const TsLevel& l, int off, int t, int i, int j, int k) {
+    const double* tx = sm + l.o_tx;
+    const double* ty = sm + l.o_ty;
+    const double* tz = sm + l.o_tz;
+    const double* v = sm + off;
+    const double xl = (i > 0) ? v[t - 1] : 0.0;
+    const double xh = (i < l.nx - 1) ? v[t + 1] : 0.0;
+    const double txh = (i < l.nx - 1) ? tx[t + 1] : 0.0;
+    double yl, yh, tyh;
+    if (NDIM == 3) {
+      yl = (j > 0) ? v[t - l.nx] : 0.0;
+      yh = (j < l.ny - 1) ? v[t + l.nx] : 0.0;
+      tyh = (j < l.ny - 1) ? ty[t + l.nx] : 0.0;
+    } else {
+      yl = (j > 0) ? *cell(l, off, i, j - 1, 0) : 0.0;
+      yh = (j < l.ny - 1) ? *cell(l, off, i, j + 1, 0) : 0.0;
+      tyh = (j < l.ny - 1) ? *cell(l, l.o_ty, i, j + 1, 0) : 0.0;
+    }
+    double s = tx[t] * xl + txh * xh + ty[t] * yl + tyh * yh;
+    if (NDIM == 3) {
+      const double zl = (k > 0) ? *cell(l, off, i, j, k - 1) : 0.0;
+      const double zh = (k < l.nz - 1) ? *cell(l, off, i, j, k + 1) : 0.0;
+      const double tzh = (k < l.nz - 1) ? *cell(l, l.o_tz, i, j, k + 1) : 0.0;
+      s += tz[t] * zl + tzh * zh;
+    }
+    return s;
+  }
+
+  __device__ __forceinline__ void decode(const TsLevel& l, int t, int o0, int& i, int& j, int& k) {
+    if (NDIM == 3) {
+      const int kk = t / l.P, in = t - kk * l.P;
+      j = in / l.nx; i = in - j * l.nx; k = o0 + kk;
+    } else {
+      const int jj = t / l.nx;
+      i = t - jj * l.nx; j = o0 + jj; k = 0;
+    }
+  }
+
+  // ---------------------------------------------------------------- passes
+  // half-sweep of colour col; dot: returns r.z over all local cells (cluster-summed)
+  __device__ double sweep(int q, int col, bool first, bool dot) {
+    const TsLevel& l = lvl(q);
+    const int o0 = olo(l), o1 = ohi(l);
+    const int hx = (l.nx + 1) >> 1;
+    const int rows = (o1 - o0) * (NDIM == 3 ? l.ny : 1);
+    const int n = hx * rows;
+    double acc = 0.0;
+    double* z = sm + l.o_z;
+    const double* r = sm + l.o_r;
+    for (int u = threadIdx.x; u < n; u += blockDim.x) {
+      const int rw = u / hx, mm = u - rw * hx;
+      int j, k;
+      if (NDIM == 3) {
+        const int kk = rw / l.ny;
+        j = rw - kk * l.ny; k = o0 + kk;
+      } else {
+        j = o0 + rw; k = 0;
+      }
+      const int par = (j + k + col) & 1;
+      const int i = 2 * mm + par;
+      const int base = rw * l.nx;
+      if (i < l.nx) {
+        const int t = base + i;
+        double a = r[t];
+        if (!first) a += nbr(l, l.o_z, t, i, j, k);
+        const double zn = a / sm[l.o_dg + t];
+        z[t] = zn;
+        if (dot) acc += r[t] * zn;
+      }
+      if (dot) {
+        const int ip = 2 * mm + 1 - par;
+        if (ip < l.nx) acc += r[base + ip] * z[base + ip];
+      }
+    }
+    if (dot) return sum(acc);
+    sync();
+    return 0.0;
+  }
+
+  __device__ double smooth(int q, bool zero, bool dot_last) {
+    const int nh = 2 * A->m + 1;
+    double d = 0.0;
+    for (int h = 0; h < nh; ++h) {
+      const bool first = zero && h == 0;
+      d = sweep(q, h & 1, first, dot_last && h == nh - 1 && !first);
+    }
+    return d;
+  }
+
+  // r_{q+1} = R (r - A z) on level q (black residual only)
+  __device__ void resid_restrict(int q) {
+    const TsLevel& f = lvl(q);
+    const TsLevel& c = lvl(q + 1);
+    const int S = A->s, kind = A->interp;
+    const int o0 = olo(f), o1 = ohi(f);
+    // pass A: t1[I, j, k] (3-D) / t1[I, j] (2-D) on local outer slices
+    {
+      const int per_slice = f.t1_slice;              // ncx * ny (3-D) | ncx (2-D)
+      const int n = (o1 - o0) * per_slice;
+      for (int u = threadIdx.x; u < n; u += blockDim.x) {
+        const int ss = u / per_slice, in = u - ss * per_slice;
+        const int I = in % f.ncx;
+        const int j = (NDIM == 3) ? in / f.ncx : o0 + ss;
+        const int k = (NDIM == 3) ? o0 + ss : 0;
+        const int ilo = max(0, S * (I - 1)), ihi = min(f.nx, S * (I + 2));
+        const int base = (NDIM == 3) ? ss * f.P + j * f.nx : ss * f.P;
+        double acc = 0.0;
+        for (int i = ilo; i < ihi; ++i) {
+          if (((i + j + k) & 1) == 0) continue;
+          int I0, I1; double w0, w1;
+          interp_w(i, f.ncx, S, kind, I0, w0, I1, w1);
+          double w = 0.0;
+          if (I0 == I) w += w0;
+          if (I1 == I && I1 != I0) w += w1;
+          if (w == 0.0) continue;
+          const int t = base + i;
+          const double res = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nbr(f, f.o_z, t, i, j, k));
+          acc += w * res;
+        }
+        sm[f.o_t1 + u] = acc;
+      }
+      sync();
+    }
+    if (NDIM == 3) {
+      // pass B: t2[I, J, k] = sum_j w(j -> J) t1[I, j, k]  (local planes)
+      const int per_slice = f.t2_slice;              // ncx * ncy
+      const int n = (o1 - o0) * per_slice;
+      for (int u = threadIdx.x; u < n; u += blockDim.x) {
+        const int ss = u / per_slice, in = u - ss * per_slice;
+        const int J = in / f.ncx, I = in - J * f.ncx;
+        const int jlo = max(0, S * (J - 1)), jhi = min(f.ny, S * (J + 2));
+        double acc = 0.0;
+        for (int j = jlo; j < jhi; ++j) {
+          int J0, J1; double w0, w1;
+          interp_w(j, f.ncy, S, kind, J0, w0, J1, w1);
+          double w = 0.0;
+          if (J0 == J) w += w0;
+          if (J1 == J && J1 != J0) w += w1;
+          if (w != 0.0) acc += w * sm[f.o_t1 + ss * f.t1_slice + j * f.ncx + I];
+        }
+        sm[f.o_t2 + u] = acc;
+      }
+      sync();
+    }
+    // pass C: coarse r on the coarse level's local slices, gathering along the outer axis
+    {
+      const int c0 = olo(c), c1 = ohi(c);
+      const int n = (c1 - c0) * c.P;
+      const int src_off = (NDIM == 3) ? f.o_t2 : f.o_t1;
+      const int src_slice = (NDIM == 3) ? f.t2_slice : f.t1_slice;
+      const int nco = (NDIM == 3) ? f.ncz : f.ncy;
+      for (int u = threadIdx.x; u < n; u += blockDim.x) {
+        const int ss = u / c.P, in = u - ss * c.P;
+        const int K = c0 + ss;
+        const int klo = max(0, S * (K - 1)), khi = min(f.no, S * (K + 2));
+        double acc = 0.0;
+        for (int k = klo; k < khi; ++k) {
+          int K0, K1; double w0, w1;
+          interp_w(k, nco, S, kind, K0, w0, K1, w1);
+          double w = 0.0;
+          if (K0 == K) w += w0;
+          if (K1 == K && K1 != K0) w += w1;
+          if (w != 0.0) acc += w * *at(src_off, src_slice, f.ppc, k, in);
+        }
+        sm[c.o_r + u] = acc;
+      }
+      sync();
+    }
+  }
+
+  // z_black += (E x_{q+1})_black on level q
+  __device__ void prolong(int q) {
+    const TsLevel& f = lvl(q);
+    const TsLevel& c = lvl(q + 1);
+    const int S = A->s, kind = A->interp;
+    const int o0 = olo(f), o1 = ohi(f);
+    const int hx = (f.nx + 1) >> 1;
+    const int rows = (o1 - o0) * (NDIM == 3 ? f.ny : 1);
+    const int n = hx * rows;
+    for (int u = threadIdx.x; u < n; u += blockDim.x) {
+      const int rw = u / hx, mm = u - rw * hx;
+      int j, k;
+      if (NDIM == 3) {
+        const int kk = rw / f.ny;
+        j = rw - kk * f.ny; k = o0 + kk;
+      } else {
+        j = o0 + rw; k = 0;
+      }
+      const int i = 2 * mm + ((j + k + 1) & 1);
+      if (i >= f.nx) continue;
+      int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
+      double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
+      interp_w(i, f.ncx, S, kind, X0, wx0, X1, wx1);
+      interp_w(j, f.ncy, S, kind, Y0, wy0, Y1, wy1);
+      if (NDIM == 3) interp_w(k, f.ncz, S, kind, Z0, wz0, Z1, wz1);
+      auto Yv = [&](int a, int bb, int cc) { return *cell(c, c.o_x, a, bb, cc); };
+      double acc = wy0 * (wx0 * Yv(X0, Y0, Z0) + wx1 * Yv(X1, Y0, Z0)) +
+                   wy1 * (wx0 * Yv(X0, Y1, Z0) + wx1 * Yv(X1, Y1, Z0));
+      if (NDIM == 3) {
+        acc *= wz0;
+        acc += wz1 * (wy0 * (wx0 * Yv(X0, Y0, Z1) + wx1 * Yv(X1, Y0, Z1)) +
+                      wy1 * (wx0 * Yv(X0, Y1, Z1) + wx1 * Yv(X1, Y1, Z1)));
+      }
+      sm[f.o_z + rw * f.nx + i] += acc;
+    }
+    sync();
+  }
+
+  // x_L = A_L^{-1} r_L: gather r_L everywhere, each CTA computes the rows it owns
+  __device__ void coarse() {
+    const TsLevel& c = lvl(A->L);
+    const int n = A->NL;
+    double* rf = sm + A->o_rfull;
+    for (int g = threadIdx.x; g < n; g += blockDim.x) {
+      const int o = g / c.P, in = g - o * c.P;
+      rf[g] = *at(c.o_r, c.P, c.ppc, o, in);
+    }
+    __syncthreads();
+    const int o0 = olo(c), o1 = ohi(c);
+    const int nl = (o1 - o0) * c.P;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = w; t < nl; t += nw) {
+      const int row = o0 * c.P + t;
+      const double* a = A->Ainv + (int64_t)row * n;
+      double acc = 0.0;
+      for (int q = lane; q < n; q += 32) acc += __ldg(a + q) * rf[q];
+      acc = warp_sum(acc);
+      if (lane == 0) sm[c.o_x + t] = acc;
+    }
+    sync();
+  }
+
+  __device__ void count(long long* arr, int k, long long v) {
+    if (rank == 0 && threadIdx.x == 0) arr[k] += v;
+  }
+
+  template <int D>
+  __device__ bool precond(int q, double& rho) {
+    smooth(q, true, false);
+    resid_restrict(q);
+    if (q + 1 == A->L) {
+      coarse();
+      count(A->iters, q + 1, 1);
+      count(A->calls, q + 1, 1);
+    } else {
+      if (!pcg<D - 1>(q + 1)) return false;
+    }
+    prolong(q);
+    rho = smooth(q, false, true);
+    return true;
+  }
+
+  template <int D>
+  __device__ bool pcg(int q) {
+    if (D <= 0) {
+      if (rank == 0 && threadIdx.x == 0) A->flags[1] = q + 1;
+      return false;
+    }
+    const TsLevel& l = lvl(q);
+    const int n = (ohi(l) - olo(l)) * l.P;
+    double* x = sm + l.o_x;
+    double* r = sm + l.o_r;
+    double* z = sm + l.o_z;
+    double* qv = sm + l.o_q;
+    count(A->calls, q, 1);
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      x[t] = 0.0;
+      acc += r[t] * r[t];
+    }
+    double rr = sum(acc);
+    if (rr < l.thr) return true;
+    long long it = 0;
+    double rho_prev = 1.0;
+    int cur = 0;
+    const int o0 = olo(l);
+    for (;;) {
+      double rho = 0.0;
+      if (!precond<D>(q, rho)) return false;
+      const int off_in = cur ? l.o_p1 : l.o_p0;
+      const int off_out = cur ? l.o_p0 : l.o_p1;
+      const double beta = (it == 0) ? 0.0 : rho / rho_prev;
+      // p_out = z + beta p_in, then q = A p_out (p_out of remote neighbours needs a barrier)
+      acc = 0.0;
+      double* po = sm + off_out;
+      const double* pi = sm + off_in;
+      for (int t = threadIdx.x; t < n; t += blockDim.x) po[t] = (it == 0) ? z[t] : z[t] + beta * pi[t];
+      sync();
+      for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        int i, j, k;
+        decode(l, t, o0, i, j, k);
+        const double pc = po[t];
+        const double qc = sm[l.o_dg + t] * pc - nbr(l, off_out, t, i, j, k);
+        qv[t] = qc;
+        acc += pc * qc;
+      }
+      const double pq = sum(acc);
+      cur ^= 1;
+      if (!(rho > 0.0) || !(pq > 0.0)) {
+        count(A->iters, q, it + 1);
+        if (rank == 0 && threadIdx.x == 0) A->flags[1] = q + 1;
+        return false;
+      }
+      const double alpha = rho / pq;
+      acc = 0.0;
+      for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        x[t] += alpha * po[t];
+        const double rv = r[t] - alpha * qv[t];
+        r[t] = rv;
+        acc += rv * rv;
+      }
+      rr = sum(acc);
+      it++;
+      rho_prev = rho;
+      if (rr < l.thr) break;
+      if (it >= A->max_iter) {
+        if (rank == 0 && threadIdx.x == 0) A->flags[0] = 1;
+        break;
+      }
+    }
+    count(A->iters, q, it);
+    return true;
+  }
+};
+
+template <>
+template <>
+__device__ bool TailSm<2>::precond<0>(int, double&) { return false; }
+template <>
+template <>
+__device__ bool TailSm<3>::precond<0>(int, double&) { return false; }
+
+template <int NDIM>
+__global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restrict__ A) {
+  extern __shared__ double sm_dyn[];
+  TailSm<NDIM> T(A, sm_dyn);
+  // stage faces of every PCG level, and the input residual of the top level
+  for (int q = A->L0; q < A->L; ++q) T.stage(q);
+  {
+    const TsLevel& l = T.lvl(A->L0);
+    const int o0 = T.olo(l), o1 = T.ohi(l);
+    const int n = (o1 - o0) * l.P;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) sm_dyn[l.o_r + t] = A->r_in[(int64_t)o0 * l.P + t];
+  }
+  T.sync();
+  const bool ok = T.template pcg<7>(A->L0);
+  (void)ok;
+  {
+    const TsLevel& l = T.lvl(A->L0);
+    const int o0 = T.olo(l), o1 = T.ohi(l);
+    const int n = (o1 - o0) * l.P;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) A->x_out[(int64_t)o0 * l.P + t] = sm_dyn[l.o_x + t];
+  }
+  T.sync();   // keep every CTA's shared memory alive until remote readers are done
+}
+
+}  // namespace mss
+
+// ============================================================================ host side
+// Lay out levels L0..L in shared memory; returns false if they do not fit.
+static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
+  using namespace mss;
+  if (ctx->L - L0 + 1 > kTsMaxLv) return false;
+  const int nd = ctx->ndim;
+  int off = 0;
+  a.L0 = L0;
+  a.L = ctx->L;
+  a.ndim = nd;
+  a.m = ctx->prm.m;
+  a.s = ctx->prm.scale;
+  a.interp = ctx->prm.interp;
+  a.max_iter = ctx->prm.max_iter;
+  a.NL = ctx->NL;
+  a.Ainv = ctx->Ainv;
+  for (int q = L0; q <= ctx->L; ++q) {
+    const Level& L = ctx->lv[q];
+    TsLevel& t = a.lv[q - L0];
+    t.nx = L.nx; t.ny = L.ny; t.nz = L.nz;
+    t.P = (nd == 3) ? L.nx * L.ny : L.nx;
+    t.no = (nd == 3) ? L.nz : L.ny;
+    t.ppc = (t.no + cs - 1) / cs;
+    t.cap = t.ppc * t.P;
+    t.Tx = L.Tx; t.Ty = L.Ty; t.Tz = L.Tz;
+    t.thr = L.thr;
+    if (q < ctx->L) {
+      const Level& C = ctx->lv[q + 1];
+      t.ncx = C.nx; t.ncy = C.ny; t.ncz = C.nz;
+      int* o[10] = {&t.o_tx, &t.o_ty, &t.o_tz, &t.o_dg, &t.o_x, &t.o_r, &t.o_z, &t.o_p0, &t.o_p1, &t.o_q};
+      for (int u = 0; u < 10; ++u) { *o[u] = off; off += t.cap; }
+      t.t1_slice = (nd == 3) ? C.nx * L.ny : C.nx;
+      t.t2_slice = (nd == 3) ? C.nx * C.ny : 0;
+      t.o_t1 = off; off += t.ppc * t.t1_slice;
+      t.o_t2 = off; off += t.ppc * t.t2_slice;
+    } else {
+      t.ncx = t.ncy = t.ncz = 0;
+      t.o_x = off; off += t.cap;
+      t.o_r = off; off += t.cap;
+      t.o_tx = t.o_ty = t.o_tz = t.o_dg = t.o_z = t.o_p0 = t.o_p1 = t.o_q = t.o_t1 = t.o_t2 = -1;
+      t.t1_slice = t.t2_slice = 0;
+    }
+  }
+  a.o_rfull = off; off += ctx->NL;
+  a.o_red = off; off += 40;
+  a.smem_doubles = off;
+  return (size_t)off * sizeof(double) <= 227 * 1024;
+}
+
+// Pick the tail implementation for the top tail level L0 (smem-resident if it fits).
+static void tailsm_setup(mss_ctx* ctx) {
+  ctx->tsm_L0 = -1;
+  if (ctx->prm.tail_cells <= 0 || ctx->nranks > 1 || ctx->L < 1) return;
+  if (getenv("MSS_NO_TAILSM")) return;
+  int L0 = -1;
+  for (int q = 1; q < ctx->L; ++q)
+    if (ctx->lv[q].N <= ctx->prm.tail_cells) { L0 = q; break; }
+  if (L0 < 0) return;
+  const int cs = 16;
+  mss::TsArgs a;
+  memset(&a, 0, sizeof(a));
+  if (!tailsm_layout(ctx, L0, cs, a)) return;
+  auto kern = (ctx->ndim == 3) ? (void*)mss::k_tailsm<3> : (void*)mss::k_tailsm<2>;
+  const size_t shm = (size_t)a.smem_doubles * sizeof(double);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(mss::kTsThreads);
+  cfg.dynamicSmemBytes = shm;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
+    cudaGetLastError();
+    return;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, sizeof(mss::TsArgs)) != cudaSuccess) return;
+  ctx->allocs.push_back(p);
+  ctx->tsm_d = p;
+  ctx->tsm_h.assign(sizeof(mss::TsArgs), 0);
+  memcpy(ctx->tsm_h.data(), &a, sizeof(a));
+  ctx->tsm_L0 = L0;
+  ctx->tsm_cs = cs;
+  ctx->tsm_shm = shm;
+}
+
+static int tailsm_launch(mss_ctx* ctx, int k) {
+  mss::TsArgs& a = *reinterpret_cast<mss::TsArgs*>(ctx->tsm_h.data());
+  if (ctx->tsm_dirty) {
+    for (int q = a.L0; q <= a.L; ++q) a.lv[q - a.L0].thr = ctx->lv[q].thr;
+    a.r_in = ctx->lv[k].r;
+    a.x_out = ctx->lv[k].x;
+    a.iters = ctx->tail_cnt;
+    a.calls = ctx->tail_cnt + MSS_MAX_LEVELS;
+    a.flags = ctx->tail_flags;
+    if (cudaMemcpyAsync(ctx->tsm_d, &a, sizeof(a), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) return MSS_ECUDA;
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return MSS_ECUDA;
+    ctx->tsm_dirty = false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->tsm_cs);
+  cfg.blockDim = dim3(mss::kTsThreads);
+  cfg.dynamicSmemBytes = ctx->tsm_shm;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ctx->tsm_cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const mss::TsArgs* dp = reinterpret_cast<const mss::TsArgs*>(ctx->tsm_d);
+  cudaError_t e = (ctx->ndim == 3) ? cudaLaunchKernelEx(&cfg, mss::k_tailsm<3>, dp)
+                                   : cudaLaunchKernelEx(&cfg, mss::k_tailsm<2>, dp);
+  ctx->launches++;
+  return e == cudaSuccess ? MSS_OK : MSS_ECUDA;
+}

@@ -267,3 +267,23 @@ def test_tail_kernel_matches_host_driven_levels(torch_mod, name):
     assert ra.iters == rb.iters
     assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-12
     assert rb.kernel_launches < ra.kernel_launches
+
+
+@pytest.mark.parametrize("name", ["C2", "C5_128", "C3_256", "C1"])
+def test_smem_tail_matches_l2_tail(torch_mod, name, monkeypatch):
+    """The shared-memory-resident cluster tail (tailsm.cuh) against the L2-resident one
+    (tail.cuh): identical per-level counts, solutions within 1e-12."""
+    torch = torch_mod
+    w = {"C2": lambda: make_workload("C2"), "C5_128": lambda: make_workload("C5", n=128),
+         "C3_256": lambda: make_workload("C3", n=256), "C1": lambda: make_workload("C1")}[name]()
+    from paper_math_9809043_b200.mss import Solver
+    K = torch.from_numpy(w.K).cuda()
+    kw = {"use_lift": 0, "interp": 1} if name.startswith("C3") else {}
+    monkeypatch.setenv("MSS_NO_TAILSM", "1")
+    a = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=kw)
+    monkeypatch.delenv("MSS_NO_TAILSM")
+    b = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=kw)
+    xa, ra = a.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    xb, rb = b.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    assert ra.iters == rb.iters
+    assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-12
