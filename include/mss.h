@@ -72,6 +72,8 @@ typedef struct {
   double  true_rel_res;                  /* ||b - A x|| / ||b|| after the solve */
   double  bnorm2;                        /* ||b||^2 of the full RHS (O5) */
   int64_t kernel_launches;               /* library kernels launched during the solve */
+  int     tail_level;                    /* first level run device-resident (-1 = none) */
+  int     tail_kind;                     /* 0 none, 1 L2-resident cluster, 2 smem-resident cluster */
 } mss_info;
 
 int         mss_default_params(mss_params* p);

@@ -56,6 +56,7 @@ struct Level {
   double *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *b = nullptr, *s = nullptr;
   double *p[2] = {nullptr, nullptr};
   double *t1 = nullptr, *t2 = nullptr;   // restriction temporaries (to level+1)
+  void* w[3] = {nullptr, nullptr, nullptr};  // 1-D transfer weight tables (mss::W1) per axis, to level+1
   int pcur = 0;
   double thr = 0;                          // N_k f^k eps^2 for the current solve
   LevelDev dev() const {
@@ -128,6 +129,7 @@ struct mss_ctx {
   void* tsm_d = nullptr;
   std::vector<char> tsm_h;
   bool tsm_dirty = true;
+  long long* tsm_phase = nullptr;
   // distributed (rank/nranks == 0/1 single GPU)
   int rank = 0, nranks = 1;
 };

@@ -489,6 +489,8 @@ static void reset_info(mss_ctx* ctx) {
   I.breakdown_level = -1;
   I.true_rel_res = 0;
   I.bnorm2 = 0;
+  I.tail_level = -1;
+  I.tail_kind = 0;
 }
 
 static BCDev bc_dev(const mss_ctx* ctx) {
@@ -566,6 +568,21 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
 }
 
 // ============================================================================ setup
+// Host mirror of interp_w (kernels.cuh): 1-D extension weights of fine cell i.
+static void interp_host(int i, int nc, int s, int kind, int& I0, double& w0, int& I1, double& w1) {
+  if (kind == 1 || nc == 1) {
+    I0 = std::min(i / s, nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
+    return;
+  }
+  const double x = i + 0.5;
+  const double X0 = 0.5 * s, Xl = s * (nc - 0.5);
+  if (x <= X0) { I0 = 0; w0 = 1.0; I1 = 0; w1 = 0.0; return; }
+  if (x >= Xl) { I0 = nc - 1; w0 = 1.0; I1 = nc - 1; w1 = 0.0; return; }
+  const int I = (int)std::floor((x - X0) / s);
+  const double tt = (x - s * (I + 0.5)) / s;
+  I0 = I; w0 = 1.0 - tt; I1 = I + 1; w1 = tt;
+}
+
 static int build_hierarchy_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min,
                                 std::vector<std::array<int64_t, 3>>& dims) {
   std::array<int64_t, 3> cur = {n[0], n[1], ndim == 3 ? n[2] : 1};
@@ -620,6 +637,7 @@ static int free_ctx(mss_ctx* ctx) {
   if (!ctx) return MSS_OK;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   prof_flush(ctx);
+  tailsm_report(ctx);
   for (cudaEvent_t e : ctx->ev_free) cudaEventDestroy(e);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->hscal) cudaFreeHost(ctx->hscal);
@@ -661,6 +679,23 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     Level& c = ctx->lv[k + 1];
     TRY(dalloc(ctx, (void**)&f.t1, sizeof(double) * (size_t)c.nx * f.ny * f.nz));
     TRY(dalloc(ctx, (void**)&f.t2, sizeof(double) * (size_t)c.nx * c.ny * f.nz));
+  }
+  // 1-D transfer weight tables, built on the host with the same rule as
+  // interp_w and uploaded once; the cluster tail stages them in shared memory.
+  for (int k = 0; k < ctx->L; ++k) {
+    Level& f = ctx->lv[k];
+    Level& c = ctx->lv[k + 1];
+    const int nf[3] = {f.nx, f.ny, f.nz}, ncs[3] = {c.nx, c.ny, c.nz};
+    for (int d = 0; d < ndim; ++d) {
+      std::vector<W1> tab(nf[d]);
+      for (int i = 0; i < nf[d]; ++i) {
+        W1& e = tab[i];
+        interp_host(i, ncs[d], s, ctx->prm.interp, e.I0, e.w0, e.I1, e.w1);
+        if (e.I1 == e.I0) e.w1 = 0.0;
+      }
+      TRY(dalloc(ctx, &f.w[d], sizeof(W1) * tab.size()));
+      CK(cudaMemcpy(f.w[d], tab.data(), sizeof(W1) * tab.size(), cudaMemcpyHostToDevice));
+    }
   }
   TRY(dalloc(ctx, (void**)&ctx->dscal, sizeof(Scal) * MSS_MAX_LEVELS));
   CK(cudaMemsetAsync(ctx->dscal, 0, sizeof(Scal) * MSS_MAX_LEVELS, ctx->stream));

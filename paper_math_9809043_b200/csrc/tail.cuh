@@ -306,6 +306,8 @@ static void tail_mark_dirty(mss_ctx* ctx) {
 }
 
 static int tail_pcg(mss_ctx* ctx, int k) {
+  ctx->info.tail_level = k;
+  ctx->info.tail_kind = (k == ctx->tsm_L0) ? 2 : 1;
   if (k == ctx->tsm_L0) return tailsm_launch(ctx, k);
   if (ctx->tail_dirty) {
     mss::TailArgs& a = *reinterpret_cast<mss::TailArgs*>(ctx->tail_h.data());

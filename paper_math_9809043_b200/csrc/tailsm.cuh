@@ -14,6 +14,9 @@
 // operand order): half-sweep P:353-357, residual O4, transfer P:412-428, CG P:440-441.
 #pragma once
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -24,18 +27,41 @@ namespace mss {
 constexpr int kTsThreads = 512;
 constexpr int kTsMaxLv = 8;
 
+// Unsigned division by a runtime constant as multiply-high + shift (valid for n < 2^31):
+// the tail's index decoding was instruction-bound on IMAD/IABS division sequences.
+struct FDiv {
+  uint32_t d, m, s;
+  __host__ void init(uint32_t dd) {
+    d = dd ? dd : 1;
+    s = 0;
+    while ((1ull << s) < d) s++;
+    m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - d)) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
+// one 1-D extension weight: fine index -> (I0, w0) + (I1, w1), w1 = 0 when I1 == I0
+struct W1 {
+  int I0, I1;
+  double w0, w1;
+};
+
 struct TsLevel {
   int nx, ny, nz;      // dims of the level
   int P;               // cells per outer slice: nx*ny (3-D) | nx (2-D)
   int no;              // outer extent: nz (3-D) | ny (2-D)
   int ppc;             // outer slices per CTA
   int cap;             // ppc * P
+  int hx;              // cell pairs per row
+  FDiv f_hx, f_ny, f_nx, f_ppc, f_P, f_ncx, f_t1s, f_t2s, f_cP;
   // shared-memory offsets (doubles)
   int o_tx, o_ty, o_tz, o_dg, o_x, o_r, o_z, o_p0, o_p1, o_q, o_t1, o_t2;
+  int o_wx, o_wy, o_wz;     // W1 tables (3 doubles per entry) for the transfer to level+1
   int t1_slice, t2_slice;   // elements per outer slice of t1 / t2
   int ncx, ncy, ncz;   // dims of the next level
   double thr;
   const double *Tx, *Ty, *Tz;   // HBM faces (staged at launch)
+  const W1 *gwx, *gwy, *gwz;    // HBM weight tables (staged at launch)
 };
 
 struct TsArgs {
@@ -46,6 +72,7 @@ struct TsArgs {
   long long* iters;     // [MSS_MAX_LEVELS]
   long long* calls;
   int* flags;
+  long long* phase_cyc; // optional [16] per-phase clock64 totals (CTA 0 thread 0), null = off
   int o_rfull;          // replicated full r_L (NL doubles)
   int o_red;            // reduction scratch (40 doubles)
   int smem_doubles;
@@ -54,34 +81,42 @@ struct TsArgs {
 
 template <int NDIM>
 struct TailSm {
-  const TsArgs* __restrict__ A;
+  const TsArgs* A;
   cg::cluster_group cl;
   double* sm;
+  double* sm_lo;   // generic pointer to the shared memory of CTA rank-1 (or null)
+  double* sm_hi;   // ... of CTA rank+1
   int rank, cs;
   int phase;
+  long long tmark;
 
   __device__ TailSm(const TsArgs* a, double* s) : A(a), cl(cg::this_cluster()), sm(s), phase(0) {
     rank = (int)cl.block_rank();
     cs = (int)cl.num_blocks();
+    sm_lo = rank > 0 ? cl.map_shared_rank(sm, rank - 1) : nullptr;
+    sm_hi = rank < cs - 1 ? cl.map_shared_rank(sm, rank + 1) : nullptr;
+    tmark = clock64();
+  }
+  // per-phase timing (debug): 0 sweep, 1 resid-x, 2 restrict-y, 3 restrict-z, 4 coarse,
+  // 5 prolong, 6 p-update, 7 spmv+sum, 8 axpy+sum
+  __device__ __forceinline__ void mark(int ph) {
+    if (A->phase_cyc && rank == 0 && threadIdx.x == 0) {
+      const long long t = clock64();
+      A->phase_cyc[ph] += t - tmark;
+      tmark = t;
+    }
   }
   __device__ __forceinline__ void sync() { cl.sync(); }
   __device__ __forceinline__ const TsLevel& lvl(int q) const { return A->lv[q - A->L0]; }
-
-  // outer-slice range owned by this CTA
   __device__ __forceinline__ int olo(const TsLevel& l) const { return min(l.no, rank * l.ppc); }
   __device__ __forceinline__ int ohi(const TsLevel& l) const { return min(l.no, (rank + 1) * l.ppc); }
+  __device__ __forceinline__ const W1* wt(int off) const { return reinterpret_cast<const W1*>(sm + off); }
 
-  // address of element `in` (index inside an outer slice of `slice` elements) of outer
-  // slice `o` of the distributed array at offset `off`
-  __device__ __forceinline__ double* at(int off, int slice, int ppc, int o, int in) {
-    const int own = o / ppc;
-    double* p = sm + off + (o - own * ppc) * slice + in;
+  // element `in` of outer slice `o` of a distributed array (slice = elements per slice)
+  __device__ __forceinline__ double* at(int off, int slice, const TsLevel& l, int o, int in) {
+    const int own = (int)l.f_ppc.div((uint32_t)o);
+    double* p = sm + off + (o - own * l.ppc) * slice + in;
     return own == rank ? p : cl.map_shared_rank(p, own);
-  }
-  // cell (i, j, k) of a level array
-  __device__ __forceinline__ double* cell(const TsLevel& l, int off, int i, int j, int k) {
-    if (NDIM == 3) return at(off, l.P, l.ppc, k, i + l.nx * j);
-    return at(off, l.P, l.ppc, j, i);
   }
 
   // cluster-wide sum, identical bits in every CTA
@@ -110,6 +145,20 @@ struct TailSm {
     return t;
   }
 
+  __device__ __forceinline__ void decode(const TsLevel& l, int t, int o0, int& i, int& j, int& k) {
+    if (NDIM == 3) {
+      const int kk = (int)l.f_P.div((uint32_t)t), in = t - kk * l.P;
+      j = (int)l.f_nx.div((uint32_t)in);
+      i = in - j * l.nx;
+      k = o0 + kk;
+    } else {
+      const int jj = (int)l.f_nx.div((uint32_t)t);
+      i = t - jj * l.nx;
+      j = o0 + jj;
+      k = 0;
+    }
+  }
+
   // ---------------------------------------------------------------- staging
   __device__ void stage(int q) {
     const TsLevel& l = lvl(q);
@@ -118,13 +167,7 @@ struct TailSm {
     const int n = (o1 - o0) * l.P;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       int i, j, k;
-      if (NDIM == 3) {
-        const int kk = t / l.P, in = t - kk * l.P;
-        j = in / l.nx; i = in - j * l.nx; k = o0 + kk;
-      } else {
-        const int jj = t / l.nx;
-        i = t - jj * l.nx; j = o0 + jj; k = 0;
-      }
+      decode(l, t, o0, i, j, k);
       const int64_t c = i + (int64_t)l.nx * (j + (int64_t)l.ny * k);
       const int64_t row = j + (int64_t)l.ny * k;
       const double t0 = l.Tx[c + row], t1 = l.Tx[c + row + 1];
@@ -141,14 +184,33 @@ struct TailSm {
       if (NDIM == 3) d += t4 + t5;
       sm[l.o_dg + t] = d;
     }
+    // 1-D transfer weight tables
+    W1* wx = reinterpret_cast<W1*>(sm + l.o_wx);
+    W1* wy = reinterpret_cast<W1*>(sm + l.o_wy);
+    for (int t = threadIdx.x; t < l.nx; t += blockDim.x) wx[t] = l.gwx[t];
+    for (int t = threadIdx.x; t < l.ny; t += blockDim.x) wy[t] = l.gwy[t];
+    if (NDIM == 3) {
+      W1* wz = reinterpret_cast<W1*>(sm + l.o_wz);
+      for (int t = threadIdx.x; t < l.nz; t += blockDim.x) wz[t] = l.gwz[t];
+    }
   }
 
-  // sum_f T_f v_nbr for local cell t = (i, j, k) of level l (array at offset `off`);
-  // operand order as nbr_sum in kernels.cuh.
-  __device__ __forceinline__ double nbr(const TsLevel& l, int off, int t, int i, int j, int k) {
+  // value of array `off` at the outer-neighbour slice below/above local cell t (slice o).
+  // The neighbour slice o-1 is local unless o == o0 (then the last slice of CTA rank-1);
+  // o+1 is local unless o == o1-1 (then the first slice of CTA rank+1).
+  __device__ __forceinline__ double below(const TsLevel& l, int off, int t, int o, int o0) {
+    if (o > o0) return sm[off + t - l.P];
+    return sm_lo[off + (l.ppc - 1) * l.P + t];
+  }
+  __device__ __forceinline__ double above(const TsLevel& l, int off, int t, int o, int o1, int o0) {
+    if (o < o1 - 1) return sm[off + t + l.P];
+    return sm_hi[off + t - (o - o0) * l.P];
+  }
+
+  // sum_f T_f v_nbr for local cell t = (i, j, k) (operand order as nbr_sum in kernels.cuh)
+  __device__ __forceinline__ double nbr(const TsLevel& l, int off, int t, int i, int j, int k, int o0, int o1) {
     const double* tx = sm + l.o_tx;
     const double* ty = sm + l.o_ty;
-    const double* tz = sm + l.o_tz;
     const double* v = sm + off;
     const double xl = (i > 0) ? v[t - 1] : 0.0;
     const double xh = (i < l.nx - 1) ? v[t + 1] : 0.0;
@@ -159,28 +221,18 @@ struct TailSm {
       yh = (j < l.ny - 1) ? v[t + l.nx] : 0.0;
       tyh = (j < l.ny - 1) ? ty[t + l.nx] : 0.0;
     } else {
-      yl = (j > 0) ? *cell(l, off, i, j - 1, 0) : 0.0;
-      yh = (j < l.ny - 1) ? *cell(l, off, i, j + 1, 0) : 0.0;
-      tyh = (j < l.ny - 1) ? *cell(l, l.o_ty, i, j + 1, 0) : 0.0;
+      yl = (j > 0) ? below(l, off, t, j, o0) : 0.0;
+      yh = (j < l.ny - 1) ? above(l, off, t, j, o1, o0) : 0.0;
+      tyh = (j < l.ny - 1) ? above(l, l.o_ty, t, j, o1, o0) : 0.0;
     }
     double s = tx[t] * xl + txh * xh + ty[t] * yl + tyh * yh;
     if (NDIM == 3) {
-      const double zl = (k > 0) ? *cell(l, off, i, j, k - 1) : 0.0;
-      const double zh = (k < l.nz - 1) ? *cell(l, off, i, j, k + 1) : 0.0;
-      const double tzh = (k < l.nz - 1) ? *cell(l, l.o_tz, i, j, k + 1) : 0.0;
-      s += tz[t] * zl + tzh * zh;
+      const double zl = (k > 0) ? below(l, off, t, k, o0) : 0.0;
+      const double zh = (k < l.nz - 1) ? above(l, off, t, k, o1, o0) : 0.0;
+      const double tzh = (k < l.nz - 1) ? above(l, l.o_tz, t, k, o1, o0) : 0.0;
+      s += sm[l.o_tz + t] * zl + tzh * zh;
     }
     return s;
-  }
-
-  __device__ __forceinline__ void decode(const TsLevel& l, int t, int o0, int& i, int& j, int& k) {
-    if (NDIM == 3) {
-      const int kk = t / l.P, in = t - kk * l.P;
-      j = in / l.nx; i = in - j * l.nx; k = o0 + kk;
-    } else {
-      const int jj = t / l.nx;
-      i = t - jj * l.nx; j = o0 + jj; k = 0;
-    }
   }
 
   // ---------------------------------------------------------------- passes
@@ -188,20 +240,22 @@ struct TailSm {
   __device__ double sweep(int q, int col, bool first, bool dot) {
     const TsLevel& l = lvl(q);
     const int o0 = olo(l), o1 = ohi(l);
-    const int hx = (l.nx + 1) >> 1;
+    const int hx = l.hx;
     const int rows = (o1 - o0) * (NDIM == 3 ? l.ny : 1);
     const int n = hx * rows;
     double acc = 0.0;
     double* z = sm + l.o_z;
     const double* r = sm + l.o_r;
     for (int u = threadIdx.x; u < n; u += blockDim.x) {
-      const int rw = u / hx, mm = u - rw * hx;
+      const int rw = (int)l.f_hx.div((uint32_t)u), mm = u - rw * hx;
       int j, k;
       if (NDIM == 3) {
-        const int kk = rw / l.ny;
-        j = rw - kk * l.ny; k = o0 + kk;
+        const int kk = (int)l.f_ny.div((uint32_t)rw);
+        j = rw - kk * l.ny;
+        k = o0 + kk;
       } else {
-        j = o0 + rw; k = 0;
+        j = o0 + rw;
+        k = 0;
       }
       const int par = (j + k + col) & 1;
       const int i = 2 * mm + par;
@@ -209,7 +263,7 @@ struct TailSm {
       if (i < l.nx) {
         const int t = base + i;
         double a = r[t];
-        if (!first) a += nbr(l, l.o_z, t, i, j, k);
+        if (!first) a += nbr(l, l.o_z, t, i, j, k, o0, o1);
         const double zn = a / sm[l.o_dg + t];
         z[t] = zn;
         if (dot) acc += r[t] * zn;
@@ -219,8 +273,13 @@ struct TailSm {
         if (ip < l.nx) acc += r[base + ip] * z[base + ip];
       }
     }
-    if (dot) return sum(acc);
+    if (dot) {
+      const double d = sum(acc);
+      mark(0);
+      return d;
+    }
     sync();
+    mark(0);
     return 0.0;
   }
 
@@ -238,80 +297,83 @@ struct TailSm {
   __device__ void resid_restrict(int q) {
     const TsLevel& f = lvl(q);
     const TsLevel& c = lvl(q + 1);
-    const int S = A->s, kind = A->interp;
+    const int S = A->s;
     const int o0 = olo(f), o1 = ohi(f);
-    // pass A: t1[I, j, k] (3-D) / t1[I, j] (2-D) on local outer slices
+    const W1* wx = wt(f.o_wx);
+    const W1* wy = wt(f.o_wy);
     {
-      const int per_slice = f.t1_slice;              // ncx * ny (3-D) | ncx (2-D)
+      // pass A: t1[I, j, (k)] on local outer slices
+      const int per_slice = f.t1_slice;
       const int n = (o1 - o0) * per_slice;
       for (int u = threadIdx.x; u < n; u += blockDim.x) {
-        const int ss = u / per_slice, in = u - ss * per_slice;
-        const int I = in % f.ncx;
-        const int j = (NDIM == 3) ? in / f.ncx : o0 + ss;
-        const int k = (NDIM == 3) ? o0 + ss : 0;
+        const int ss = (int)f.f_t1s.div((uint32_t)u), in = u - ss * per_slice;
+        int I, j, k;
+        if (NDIM == 3) {
+          j = (int)f.f_ncx.div((uint32_t)in);
+          I = in - j * f.ncx;
+          k = o0 + ss;
+        } else {
+          I = in;
+          j = o0 + ss;
+          k = 0;
+        }
         const int ilo = max(0, S * (I - 1)), ihi = min(f.nx, S * (I + 2));
         const int base = (NDIM == 3) ? ss * f.P + j * f.nx : ss * f.P;
         double acc = 0.0;
         for (int i = ilo; i < ihi; ++i) {
           if (((i + j + k) & 1) == 0) continue;
-          int I0, I1; double w0, w1;
-          interp_w(i, f.ncx, S, kind, I0, w0, I1, w1);
-          double w = 0.0;
-          if (I0 == I) w += w0;
-          if (I1 == I && I1 != I0) w += w1;
+          const W1 w1 = wx[i];
+          const double w = (w1.I0 == I ? w1.w0 : 0.0) + (w1.I1 == I ? w1.w1 : 0.0);
           if (w == 0.0) continue;
           const int t = base + i;
-          const double res = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nbr(f, f.o_z, t, i, j, k));
+          const double res = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nbr(f, f.o_z, t, i, j, k, o0, o1));
           acc += w * res;
         }
         sm[f.o_t1 + u] = acc;
       }
       sync();
+      mark(1);
     }
     if (NDIM == 3) {
       // pass B: t2[I, J, k] = sum_j w(j -> J) t1[I, j, k]  (local planes)
-      const int per_slice = f.t2_slice;              // ncx * ncy
+      const int per_slice = f.t2_slice;
       const int n = (o1 - o0) * per_slice;
       for (int u = threadIdx.x; u < n; u += blockDim.x) {
-        const int ss = u / per_slice, in = u - ss * per_slice;
-        const int J = in / f.ncx, I = in - J * f.ncx;
+        const int ss = (int)f.f_t2s.div((uint32_t)u), in = u - ss * per_slice;
+        const int J = (int)f.f_ncx.div((uint32_t)in), I = in - J * f.ncx;
         const int jlo = max(0, S * (J - 1)), jhi = min(f.ny, S * (J + 2));
         double acc = 0.0;
         for (int j = jlo; j < jhi; ++j) {
-          int J0, J1; double w0, w1;
-          interp_w(j, f.ncy, S, kind, J0, w0, J1, w1);
-          double w = 0.0;
-          if (J0 == J) w += w0;
-          if (J1 == J && J1 != J0) w += w1;
+          const W1 w1 = wy[j];
+          const double w = (w1.I0 == J ? w1.w0 : 0.0) + (w1.I1 == J ? w1.w1 : 0.0);
           if (w != 0.0) acc += w * sm[f.o_t1 + ss * f.t1_slice + j * f.ncx + I];
         }
         sm[f.o_t2 + u] = acc;
       }
       sync();
+      mark(2);
     }
-    // pass C: coarse r on the coarse level's local slices, gathering along the outer axis
     {
+      // pass C: coarse r on the coarse level's local slices, gathering along the outer axis
       const int c0 = olo(c), c1 = ohi(c);
       const int n = (c1 - c0) * c.P;
       const int src_off = (NDIM == 3) ? f.o_t2 : f.o_t1;
       const int src_slice = (NDIM == 3) ? f.t2_slice : f.t1_slice;
-      const int nco = (NDIM == 3) ? f.ncz : f.ncy;
+      const W1* wo = (NDIM == 3) ? wt(f.o_wz) : wy;
       for (int u = threadIdx.x; u < n; u += blockDim.x) {
-        const int ss = u / c.P, in = u - ss * c.P;
+        const int ss = (int)f.f_cP.div((uint32_t)u), in = u - ss * c.P;
         const int K = c0 + ss;
         const int klo = max(0, S * (K - 1)), khi = min(f.no, S * (K + 2));
         double acc = 0.0;
         for (int k = klo; k < khi; ++k) {
-          int K0, K1; double w0, w1;
-          interp_w(k, nco, S, kind, K0, w0, K1, w1);
-          double w = 0.0;
-          if (K0 == K) w += w0;
-          if (K1 == K && K1 != K0) w += w1;
-          if (w != 0.0) acc += w * *at(src_off, src_slice, f.ppc, k, in);
+          const W1 w1 = wo[k];
+          const double w = (w1.I0 == K ? w1.w0 : 0.0) + (w1.I1 == K ? w1.w1 : 0.0);
+          if (w != 0.0) acc += w * *at(src_off, src_slice, f, k, in);
         }
         sm[c.o_r + u] = acc;
       }
       sync();
+      mark(3);
     }
   }
 
@@ -319,38 +381,45 @@ struct TailSm {
   __device__ void prolong(int q) {
     const TsLevel& f = lvl(q);
     const TsLevel& c = lvl(q + 1);
-    const int S = A->s, kind = A->interp;
     const int o0 = olo(f), o1 = ohi(f);
-    const int hx = (f.nx + 1) >> 1;
+    const int hx = f.hx;
     const int rows = (o1 - o0) * (NDIM == 3 ? f.ny : 1);
     const int n = hx * rows;
+    const W1* wx = wt(f.o_wx);
+    const W1* wy = wt(f.o_wy);
+    const W1* wz = (NDIM == 3) ? wt(f.o_wz) : nullptr;
     for (int u = threadIdx.x; u < n; u += blockDim.x) {
-      const int rw = u / hx, mm = u - rw * hx;
+      const int rw = (int)f.f_hx.div((uint32_t)u), mm = u - rw * hx;
       int j, k;
       if (NDIM == 3) {
-        const int kk = rw / f.ny;
-        j = rw - kk * f.ny; k = o0 + kk;
+        const int kk = (int)f.f_ny.div((uint32_t)rw);
+        j = rw - kk * f.ny;
+        k = o0 + kk;
       } else {
-        j = o0 + rw; k = 0;
+        j = o0 + rw;
+        k = 0;
       }
       const int i = 2 * mm + ((j + k + 1) & 1);
       if (i >= f.nx) continue;
-      int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
-      double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
-      interp_w(i, f.ncx, S, kind, X0, wx0, X1, wx1);
-      interp_w(j, f.ncy, S, kind, Y0, wy0, Y1, wy1);
-      if (NDIM == 3) interp_w(k, f.ncz, S, kind, Z0, wz0, Z1, wz1);
-      auto Yv = [&](int a, int bb, int cc) { return *cell(c, c.o_x, a, bb, cc); };
-      double acc = wy0 * (wx0 * Yv(X0, Y0, Z0) + wx1 * Yv(X1, Y0, Z0)) +
-                   wy1 * (wx0 * Yv(X0, Y1, Z0) + wx1 * Yv(X1, Y1, Z0));
+      const W1 ax = wx[i], ay = wy[j];
+      double acc;
       if (NDIM == 3) {
-        acc *= wz0;
-        acc += wz1 * (wy0 * (wx0 * Yv(X0, Y0, Z1) + wx1 * Yv(X1, Y0, Z1)) +
-                      wy1 * (wx0 * Yv(X0, Y1, Z1) + wx1 * Yv(X1, Y1, Z1)));
+        const W1 az = wz[k];
+        auto Yv = [&](int a, int bb, int cc) { return *at(c.o_x, c.P, c, cc, a + c.nx * bb); };
+        acc = ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0, az.I0) + ax.w1 * Yv(ax.I1, ay.I0, az.I0)) +
+              ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1, az.I0) + ax.w1 * Yv(ax.I1, ay.I1, az.I0));
+        acc *= az.w0;
+        acc += az.w1 * (ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0, az.I1) + ax.w1 * Yv(ax.I1, ay.I0, az.I1)) +
+                        ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1, az.I1) + ax.w1 * Yv(ax.I1, ay.I1, az.I1)));
+      } else {
+        auto Yv = [&](int a, int bb) { return *at(c.o_x, c.P, c, bb, a); };
+        acc = ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0) + ax.w1 * Yv(ax.I1, ay.I0)) +
+              ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1) + ax.w1 * Yv(ax.I1, ay.I1));
       }
       sm[f.o_z + rw * f.nx + i] += acc;
     }
     sync();
+    mark(5);
   }
 
   // x_L = A_L^{-1} r_L: gather r_L everywhere, each CTA computes the rows it owns
@@ -359,8 +428,8 @@ struct TailSm {
     const int n = A->NL;
     double* rf = sm + A->o_rfull;
     for (int g = threadIdx.x; g < n; g += blockDim.x) {
-      const int o = g / c.P, in = g - o * c.P;
-      rf[g] = *at(c.o_r, c.P, c.ppc, o, in);
+      const int o = (int)c.f_P.div((uint32_t)g), in = g - o * c.P;
+      rf[g] = *at(c.o_r, c.P, c, o, in);
     }
     __syncthreads();
     const int o0 = olo(c), o1 = ohi(c);
@@ -370,11 +439,12 @@ struct TailSm {
       const int row = o0 * c.P + t;
       const double* a = A->Ainv + (int64_t)row * n;
       double acc = 0.0;
-      for (int q = lane; q < n; q += 32) acc += __ldg(a + q) * rf[q];
+      for (int qq = lane; qq < n; qq += 32) acc += __ldg(a + qq) * rf[qq];
       acc = warp_sum(acc);
       if (lane == 0) sm[c.o_x + t] = acc;
     }
     sync();
+    mark(4);
   }
 
   __device__ void count(long long* arr, int k, long long v) {
@@ -404,7 +474,8 @@ struct TailSm {
       return false;
     }
     const TsLevel& l = lvl(q);
-    const int n = (ohi(l) - olo(l)) * l.P;
+    const int o0 = olo(l), o1 = ohi(l);
+    const int n = (o1 - o0) * l.P;
     double* x = sm + l.o_x;
     double* r = sm + l.o_r;
     double* z = sm + l.o_z;
@@ -420,28 +491,28 @@ struct TailSm {
     long long it = 0;
     double rho_prev = 1.0;
     int cur = 0;
-    const int o0 = olo(l);
     for (;;) {
       double rho = 0.0;
       if (!precond<D>(q, rho)) return false;
       const int off_in = cur ? l.o_p1 : l.o_p0;
       const int off_out = cur ? l.o_p0 : l.o_p1;
       const double beta = (it == 0) ? 0.0 : rho / rho_prev;
-      // p_out = z + beta p_in, then q = A p_out (p_out of remote neighbours needs a barrier)
       acc = 0.0;
       double* po = sm + off_out;
       const double* pi = sm + off_in;
       for (int t = threadIdx.x; t < n; t += blockDim.x) po[t] = (it == 0) ? z[t] : z[t] + beta * pi[t];
       sync();
+      mark(6);
       for (int t = threadIdx.x; t < n; t += blockDim.x) {
         int i, j, k;
         decode(l, t, o0, i, j, k);
         const double pc = po[t];
-        const double qc = sm[l.o_dg + t] * pc - nbr(l, off_out, t, i, j, k);
+        const double qc = sm[l.o_dg + t] * pc - nbr(l, off_out, t, i, j, k, o0, o1);
         qv[t] = qc;
         acc += pc * qc;
       }
       const double pq = sum(acc);
+      mark(7);
       cur ^= 1;
       if (!(rho > 0.0) || !(pq > 0.0)) {
         count(A->iters, q, it + 1);
@@ -457,6 +528,7 @@ struct TailSm {
         acc += rv * rv;
       }
       rr = sum(acc);
+      mark(8);
       it++;
       rho_prev = rho;
       if (rr < l.thr) break;
@@ -478,10 +550,21 @@ template <>
 __device__ bool TailSm<3>::precond<0>(int, double&) { return false; }
 
 template <int NDIM>
-__global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restrict__ A) {
+__global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restrict__ Ag) {
   extern __shared__ double sm_dyn[];
+  // The level descriptors are read in every pass; cluster barriers invalidate L1, so a
+  // copy in HBM would cost an L2 round trip per field per pass.  Keep them in smem.
+  __shared__ TsArgs As;
+  {
+    const int nw = (int)(sizeof(TsArgs) / sizeof(int));
+    const int* src = reinterpret_cast<const int*>(Ag);
+    int* dst = reinterpret_cast<int*>(&As);
+    for (int t = threadIdx.x; t < nw; t += blockDim.x) dst[t] = src[t];
+    __syncthreads();
+  }
+  const TsArgs* A = &As;
   TailSm<NDIM> T(A, sm_dyn);
-  // stage faces of every PCG level, and the input residual of the top level
+  // stage faces and weight tables of every PCG level, and the top level's residual
   for (int q = A->L0; q < A->L; ++q) T.stage(q);
   {
     const TsLevel& l = T.lvl(A->L0);
@@ -529,6 +612,8 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
     t.cap = t.ppc * t.P;
     t.Tx = L.Tx; t.Ty = L.Ty; t.Tz = L.Tz;
     t.thr = L.thr;
+    t.hx = (L.nx + 1) / 2;
+    t.f_hx.init(t.hx); t.f_ny.init(L.ny); t.f_nx.init(L.nx); t.f_ppc.init(t.ppc); t.f_P.init(t.P);
     if (q < ctx->L) {
       const Level& C = ctx->lv[q + 1];
       t.ncx = C.nx; t.ncy = C.ny; t.ncz = C.nz;
@@ -538,22 +623,33 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
       t.t2_slice = (nd == 3) ? C.nx * C.ny : 0;
       t.o_t1 = off; off += t.ppc * t.t1_slice;
       t.o_t2 = off; off += t.ppc * t.t2_slice;
+      t.f_ncx.init(C.nx); t.f_t1s.init(t.t1_slice); t.f_t2s.init(t.t2_slice ? t.t2_slice : 1);
+      t.f_cP.init((nd == 3) ? C.nx * C.ny : C.nx);
+      t.o_wx = off; off += 3 * L.nx;
+      t.o_wy = off; off += 3 * L.ny;
+      t.o_wz = off; off += (nd == 3) ? 3 * L.nz : 0;
+      t.gwx = reinterpret_cast<const W1*>(L.w[0]);
+      t.gwy = reinterpret_cast<const W1*>(L.w[1]);
+      t.gwz = reinterpret_cast<const W1*>(L.w[2]);
     } else {
       t.ncx = t.ncy = t.ncz = 0;
       t.o_x = off; off += t.cap;
       t.o_r = off; off += t.cap;
       t.o_tx = t.o_ty = t.o_tz = t.o_dg = t.o_z = t.o_p0 = t.o_p1 = t.o_q = t.o_t1 = t.o_t2 = -1;
+      t.o_wx = t.o_wy = t.o_wz = -1;
+      t.gwx = t.gwy = t.gwz = nullptr;
       t.t1_slice = t.t2_slice = 0;
     }
   }
   a.o_rfull = off; off += ctx->NL;
   a.o_red = off; off += 40;
   a.smem_doubles = off;
-  return (size_t)off * sizeof(double) <= 227 * 1024;
+  return (size_t)off * sizeof(double) + sizeof(TsArgs) + 1024 <= 227 * 1024;
 }
 
 // Pick the tail implementation for the top tail level L0 (smem-resident if it fits).
 static void tailsm_setup(mss_ctx* ctx) {
+  const bool dbg = getenv("MSS_DEBUG") != nullptr;
   ctx->tsm_L0 = -1;
   if (ctx->prm.tail_cells <= 0 || ctx->nranks > 1 || ctx->L < 1) return;
   if (getenv("MSS_NO_TAILSM")) return;
@@ -564,11 +660,15 @@ static void tailsm_setup(mss_ctx* ctx) {
   const int cs = 16;
   mss::TsArgs a;
   memset(&a, 0, sizeof(a));
-  if (!tailsm_layout(ctx, L0, cs, a)) return;
+  if (!tailsm_layout(ctx, L0, cs, a)) {
+    if (dbg) fprintf(stderr, "[mss] tailsm: level %d does not fit (%d doubles)\n", L0, a.smem_doubles);
+    return;
+  }
   auto kern = (ctx->ndim == 3) ? (void*)mss::k_tailsm<3> : (void*)mss::k_tailsm<2>;
   const size_t shm = (size_t)a.smem_doubles * sizeof(double);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    if (dbg) fprintf(stderr, "[mss] tailsm: attribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
     cudaGetLastError();
     return;
   }
@@ -584,7 +684,9 @@ static void tailsm_setup(mss_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
+  cudaError_t oe = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+  if (dbg) fprintf(stderr, "[mss] tailsm: L0=%d smem=%zu B clusters=%d (%s)\n", L0, shm, ncl, cudaGetErrorString(oe));
+  if (oe != cudaSuccess || ncl < 1) {
     cudaGetLastError();
     return;
   }
@@ -597,6 +699,27 @@ static void tailsm_setup(mss_ctx* ctx) {
   ctx->tsm_L0 = L0;
   ctx->tsm_cs = cs;
   ctx->tsm_shm = shm;
+  if (getenv("MSS_TAIL_PHASES")) {
+    void* ph = nullptr;
+    if (cudaMalloc(&ph, 16 * sizeof(long long)) == cudaSuccess) {
+      ctx->allocs.push_back(ph);
+      cudaMemset(ph, 0, 16 * sizeof(long long));
+      reinterpret_cast<mss::TsArgs*>(ctx->tsm_h.data())->phase_cyc = (long long*)ph;
+      ctx->tsm_phase = (long long*)ph;
+    }
+  }
+}
+
+static void tailsm_report(mss_ctx* ctx) {
+  if (!ctx->tsm_phase) return;
+  long long h[16];
+  cudaMemcpy(h, ctx->tsm_phase, sizeof(h), cudaMemcpyDeviceToHost);
+  const char* nm[10] = {"sweep", "resid-x", "restrict-y", "restrict-z", "coarse", "prolong", "p-update",
+                        "spmv+sum", "axpy+sum", "other"};
+  long long tot = 0;
+  for (int i = 0; i < 10; ++i) tot += h[i];
+  for (int i = 0; i < 10; ++i)
+    fprintf(stderr, "[mss] tail phase %-10s %14lld cycles %5.1f%%\n", nm[i], h[i], tot ? 100.0 * h[i] / tot : 0.0);
 }
 
 static int tailsm_launch(mss_ctx* ctx, int k) {

@@ -59,6 +59,8 @@ class Info(ctypes.Structure):
         ("true_rel_res", ctypes.c_double),
         ("bnorm2", ctypes.c_double),
         ("kernel_launches", ctypes.c_int64),
+        ("tail_level", ctypes.c_int),
+        ("tail_kind", ctypes.c_int),
     ]
 
 
@@ -156,6 +158,8 @@ class SolveReport:
     not_converged: bool
     true_rel_res: float
     kernel_launches: int
+    tail_level: int = -1
+    tail_kind: int = 0
 
 
 class Solver:
@@ -217,7 +221,7 @@ class Solver:
         L1 = inf.levels
         return SolveReport(0, list(inf.iters[:L1]), list(inf.calls[:L1]),
                            [tuple(inf.dims[k]) for k in range(L1)], bool(inf.not_converged),
-                           inf.true_rel_res, inf.kernel_launches)
+                           inf.true_rel_res, inf.kernel_launches, inf.tail_level, inf.tail_kind)
 
     def profile(self, enable: bool, max_level: int = 0):
         _check(self.lib.mss_profile(self.ctx, 1 if enable else 0, int(max_level)), "mss_profile")

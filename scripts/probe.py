@@ -39,7 +39,8 @@ for _ in range(args.reps):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / args.reps
-print(f"{args.config} n={w.n} levels={rep.dims} iters={rep.iters} calls={rep.calls} res={rep.true_rel_res:.2e}")
+print(f"{args.config} n={w.n} levels={rep.dims} iters={rep.iters} calls={rep.calls} res={rep.true_rel_res:.2e} "
+      f"tail level {rep.tail_level} kind {rep.tail_kind}")
 print(f"  solve {ms:.3f} ms  ->  {w.N / ms * 1e3:.4g} unknowns/s, launches/solve {rep.kernel_launches}")
 s.profile(True, args.prof_level)
 t0 = time.perf_counter()

@@ -264,6 +264,7 @@ def test_tail_kernel_matches_host_driven_levels(torch_mod, name):
     b = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params={"tail_cells": 1 << 20, **kw})
     xa, ra = a.solve(cu(torch, w.f), rel_tol=w.rel_tol)
     xb, rb = b.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    assert ra.tail_kind == 0 and rb.tail_kind in (1, 2), (ra.tail_kind, rb.tail_kind)
     assert ra.iters == rb.iters
     assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-12
     assert rb.kernel_launches < ra.kernel_launches
@@ -285,5 +286,6 @@ def test_smem_tail_matches_l2_tail(torch_mod, name, monkeypatch):
     b = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=kw)
     xa, ra = a.solve(cu(torch, w.f), rel_tol=w.rel_tol)
     xb, rb = b.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    assert ra.tail_kind == 1 and rb.tail_kind == 2, (ra.tail_kind, rb.tail_kind)
     assert ra.iters == rb.iters
     assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-12
