@@ -150,17 +150,32 @@ int mss_coarse_solve(mss_ctx* ctx, const double* b, double* x);   /* x = A_L^{-1
 /* b (O5) and x0 = P_bf (O6) for a source density f. */
 int mss_rhs_lift(mss_ctx* ctx, const double* f, double* b, double* x0);
 
-/* ---- distributed (z-slabs across ranks; NCCL over NVLink) ------------------------ */
-int mss_nccl_unique_id(unsigned char id[128]);
-/* Rank r owns global planes [z_begin, z_end) given by mss_slab_range; K_local, and the
- * f / x passed to mss_solve, are that rank's slab.  Levels with N_k < gather_below are
- * replicated on every rank (allgather of the restricted RHS). */
-int mss_slab_range(const int64_t n_global[3], int ndim, int scale, int depth, int rank,
+/* ---- distributed (z-slabs across ranks; NCCL over NVLink / NVSwitch) ---------------
+ * The global grid is split into z-slabs: rank r owns global planes [z_begin, z_end) of
+ * level 0 (mss_slab_range; boundaries are multiples of scale^ndist planes where ndist
+ * is the number of levels with N_k >= gather_below, level 0 always included, so the
+ * slabs stay aligned on every distributed level).  Coarser levels are replicated on
+ * every rank (allgather of the restricted RHS once per coarse call).  K_local, and the
+ * f / x passed to mss_solve, are the rank's slab (x fastest).  Every rank must call
+ * every mss_* function of its context in the same order (collectives inside).
+ * Design and readings: DESIGN.md §8. */
+int mss_nccl_unique_id(unsigned char id[128]);    /* rank 0; broadcast it to the others */
+int mss_slab_range(const int64_t n_global[3], int ndim, const mss_params* p, int depth, int rank,
                    int nranks, int64_t* z_begin, int64_t* z_end);
+/* NCCL transport: one process per GPU (the caller has selected the device). */
 int mss_setup_dist(mss_ctx** out, int rank, int nranks, const unsigned char id[128],
                    int ndim, const int64_t n_global[3], const double extent[3],
                    const double* K_local, int k_comp, const mss_bc bc[6], int depth,
                    const mss_params* p, void* stream);
+/* Loopback transport (testing the decomposition on ONE GPU): nranks host threads of one
+ * process, each calling mss_setup_loopback / mss_solve / mss_free with its own rank and
+ * stream; exchanges are device copies fenced by host barriers.  Destroy the group after
+ * every context using it is freed. */
+int mss_loopback_create(int nranks, void** group);
+int mss_loopback_destroy(void* group);
+int mss_setup_loopback(mss_ctx** out, void* group, int rank, int ndim, const int64_t n_global[3],
+                       const double extent[3], const double* K_local, int k_comp, const mss_bc bc[6],
+                       int depth, const mss_params* p, void* stream);
 
 /* ---- live per-kernel timing (bench.py's roofline) ----------------------------------
  * With profiling on, every launch of a kernel class on a level <= max_level is

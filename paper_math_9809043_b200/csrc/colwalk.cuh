@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
 template <int MINB>
 __global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L, int ncx, int ncy, int ncz, int s,
                                                                       int kind, const double* __restrict__ y,
-                                                                      double* __restrict__ z, int kchunk) {
+                                                                      double* __restrict__ z, int kchunk, int zc0) {
   const int m = blockIdx.x * kColX + threadIdx.x;
   const int j = blockIdx.y * kColY + threadIdx.y;
   const int k0 = blockIdx.z * kchunk;
@@ -262,8 +262,8 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L,
     const double wx0 = par ? wxb0 : wxa0, wx1 = par ? wxb1 : wxa1;
     int Z0, Z1;
     double wz0, wz1;
-    interp_w(k, ncz, s, kind, Z0, wz0, Z1, wz1);
-    auto Yv = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * cc); };
+    interp_w(k + L.z0, ncz, s, kind, Z0, wz0, Z1, wz1);
+    auto Yv = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * (cc - zc0)); };
     double acc = wy0 * (wx0 * Yv(X0, Y0, Z0) + wx1 * Yv(X1, Y0, Z0)) +
                  wy1 * (wx0 * Yv(X0, Y1, Z0) + wx1 * Yv(X1, Y1, Z0));
     acc *= wz0;

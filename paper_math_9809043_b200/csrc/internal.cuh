@@ -18,6 +18,7 @@
 #define MSS_DIRICHLET_KIND 1
 
 namespace mss {
+struct Comm;
 
 constexpr int kBlock = 256;           // threads per CTA for the streaming kernels
 constexpr int kSMs = 148;             // B200
@@ -38,7 +39,8 @@ struct Scal {
 // Plain-pointer view of one level handed to kernels by value.
 struct LevelDev {
   int nx, ny, nz;     // local dims (nz = 1 in 2-D)
-  int z0;             // global z offset of this slab (colour parity)
+  int z0;             // global z offset of this slab (colour parity, global BCs)
+  int nzg;            // global nz of this level
   int64_t plane;      // nx * ny
   int64_t N;          // nx * ny * nz
   const double* Tx;
@@ -48,20 +50,22 @@ struct LevelDev {
 
 struct Level {
   int nx = 0, ny = 0, nz = 0;
-  int z0 = 0;
+  int z0 = 0;                            // global z offset of this rank's slab
+  int nzg = 0;                           // global nz
+  bool dist = false;                     // true: z-slab distributed across ranks (ghost planes = halos)
   int64_t N = 0, plane = 0;
   double h[3] = {1, 1, 1};
   double *Tx = nullptr, *Ty = nullptr, *Tz = nullptr;
   // ghosted cell vectors (interior pointers)
   double *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *b = nullptr, *s = nullptr;
   double *p[2] = {nullptr, nullptr};
-  double *t1 = nullptr, *t2 = nullptr;   // restriction temporaries (to level+1)
+  double *t1 = nullptr, *t2 = nullptr;   // restriction temporaries (to level+1); t2 has 2 ghost planes
   void* w[3] = {nullptr, nullptr, nullptr};  // 1-D transfer weight tables (mss::W1) per axis, to level+1
   int pcur = 0;
   double thr = 0;                          // N_k f^k eps^2 for the current solve
   LevelDev dev() const {
     LevelDev d;
-    d.nx = nx; d.ny = ny; d.nz = nz; d.z0 = z0; d.plane = plane; d.N = N;
+    d.nx = nx; d.ny = ny; d.nz = nz; d.z0 = z0; d.nzg = nzg ? nzg : nz; d.plane = plane; d.N = N;
     d.Tx = Tx; d.Ty = Ty; d.Tz = Tz;
     return d;
   }
@@ -130,6 +134,11 @@ struct mss_ctx {
   std::vector<char> tsm_h;
   bool tsm_dirty = true;
   long long* tsm_phase = nullptr;
-  // distributed (rank/nranks == 0/1 single GPU)
+  // distributed z-slabs (rank/nranks == 0/1 single GPU): levels [0, ndist) are split
+  // across ranks, the rest are replicated on every rank
   int rank = 0, nranks = 1;
+  int ndist = 0;
+  int64_t slab_unit = 1;                   // slab boundaries are multiples of this many level-0 planes
+  mss::Comm* comm = nullptr;
+  void* loop_group = nullptr;              // loopback group (tests)
 };

@@ -147,18 +147,21 @@ __global__ void k_validate_K(const double* __restrict__ K, int64_t n, int* flag)
 
 // a1: faces along direction d from the cell K_d (P:341-346 harmonic mean; P:366-371
 // boundary types; P:381-383 T = (A/h) K).  Face dims: n + e_d.
+// In a z-slab (z0 = global offset, nzg = global nz) the z faces at the slab ends are
+// interior faces whose outer cell lives in the ghost plane of Kd (halo-exchanged K).
 __global__ void k_assemble_faces(const double* __restrict__ Kd, double* __restrict__ T,
                                  int nx, int ny, int nz, int d, double coef,
-                                 int dir_lo, int dir_hi) {
+                                 int dir_lo, int dir_hi, int z0, int nzg) {
   const int Dx = nx + (d == 0), Dy = ny + (d == 1), Dz = nz + (d == 2);
   const int64_t total = (int64_t)Dx * Dy * Dz;
-  const int nd = (d == 0) ? nx : (d == 1) ? ny : nz;
+  const int nd = (d == 0) ? nx : (d == 1) ? ny : nzg;
+  const int off = (d == 2) ? z0 : 0;
   for (int64_t t = gtid(); t < total; t += gstride()) {
     const int fi = (int)(t % Dx);
     const int64_t rr = t / Dx;
     const int fj = (int)(rr % Dy);
     const int fk = (int)(rr / Dy);
-    const int f = (d == 0) ? fi : (d == 1) ? fj : fk;   // face index along d
+    const int f = ((d == 0) ? fi : (d == 1) ? fj : fk) + off;   // global face index along d
     // cells on either side: f-1 and f along d
     int ci = fi, cj = fj, ck = fk;
     double val;
@@ -180,10 +183,12 @@ __global__ void k_assemble_faces(const double* __restrict__ Kd, double* __restri
 // a2: Reading B coarse faces:  1/T^c_F = sum_i w_i / sum_{rows} T_d(i, rows),
 // w_i = |CV_i ∩ CV_F| / |CV_i| over the staggered control volumes; a zero column sum
 // blocks the face.  One thread per coarse face.
+// Distributed z (d == 2): Tf is the interior pointer of a fine Tz with 2 ghost face
+// planes each side; z0f / nzgf are the fine slab offset / global nz, Z0c the coarse offset.
 __global__ void k_coarsen_faces(const double* __restrict__ Tf, double* __restrict__ Tc,
-                                int nfx, int nfy, int nfz,   // fine cell dims
-                                int ncx, int ncy, int ncz,   // coarse cell dims
-                                int d, int s, int ndim) {
+                                int nfx, int nfy, int nfz,   // fine cell dims (local)
+                                int ncx, int ncy, int ncz,   // coarse cell dims (local)
+                                int d, int s, int ndim, int z0f, int nzgf, int Z0c) {
   const int Cx = ncx + (d == 0), Cy = ncy + (d == 1), Cz = ncz + (d == 2);
   const int Fx = nfx + (d == 0), Fy = nfy + (d == 1);
   const int64_t total = (int64_t)Cx * Cy * Cz;
@@ -194,9 +199,11 @@ __global__ void k_coarsen_faces(const double* __restrict__ Tf, double* __restric
     const int64_t rr = t / Cx;
     c3[1] = (int)(rr % Cy);
     c3[2] = (int)(rr / Cy);
-    const int F = c3[d];
+    const int F = c3[d] + ((d == 2) ? Z0c : 0);                     // global coarse face
+    const int nf_g = (d == 2) ? nzgf : nf_d;                         // global fine count
+    const int ioff = (d == 2) ? z0f : 0;                             // global -> local fine face
     const double a = fmax(s * (double)F - 0.5 * s, 0.0);
-    const double b = fmin(s * (double)F + 0.5 * s, (double)nf_d);
+    const double b = fmin(s * (double)F + 0.5 * s, (double)nf_g);
     // the two transverse axes (in 2-D the z axis is a single row)
     const int e1 = (d == 0) ? 1 : 0;
     const int e2 = (d == 2) ? 1 : 2;
@@ -204,9 +211,9 @@ __global__ void k_coarsen_faces(const double* __restrict__ Tf, double* __restric
     const int r2_lo = (ndim == 3) ? c3[e2] * s : 0, r2_n = (ndim == 3) ? s : 1;
     double inv = 0.0;
     bool blocked = false;
-    const int ilo = max(0, s * F - s), ihi = min(nf_d, s * F + s);
+    const int ilo = max(0, s * F - s), ihi = min(nf_g, s * F + s);
     for (int i = ilo; i <= ihi; ++i) {
-      const double lo = fmax(i - 0.5, 0.0), hi = fmin(i + 0.5, (double)nf_d);
+      const double lo = fmax(i - 0.5, 0.0), hi = fmin(i + 0.5, (double)nf_g);
       const double ov = fmin(b, hi) - fmax(a, lo);
       if (!(ov > 0.0)) continue;
       const double w = ov / (hi - lo);
@@ -214,7 +221,7 @@ __global__ void k_coarsen_faces(const double* __restrict__ Tf, double* __restric
       for (int q2 = 0; q2 < r2_n; ++q2) {
         for (int q1 = 0; q1 < r1_n; ++q1) {
           int f3[3];
-          f3[d] = i;
+          f3[d] = i - ioff;
           f3[e1] = r1_lo + q1;
           f3[e2] = r2_lo + q2;
           cs += Tf[f3[0] + (int64_t)Fx * (f3[1] + (int64_t)Fy * f3[2])];
@@ -320,8 +327,8 @@ __global__ void k_rhs_lift(LevelDev L, const double* __restrict__ f, double* __r
     double t[6];
     load_faces<NDIM>(L, e, t);
     double v = f[c] * V;
-    const int idx[3] = {e.i, e.j, e.k};
-    const int nn[3] = {L.nx, L.ny, L.nz};
+    const int idx[3] = {e.i, e.j, e.k + L.z0};          // global index (z-slabs)
+    const int nn[3] = {L.nx, L.ny, L.nzg};
 #pragma unroll
     for (int d = 0; d < NDIM; ++d) {
       if (idx[d] == 0) {
@@ -414,8 +421,12 @@ __device__ __forceinline__ void interp_w(int i, int nc, int s, int kind, int& I0
 }
 
 // One output of the restriction R = E^T along `axis`: (n0,n1,n2) -> n_axis = nc.
+// in_off / out_off: global index of local fine / coarse index 0 along `axis`; nf_g /
+// nc_g: global fine / coarse counts (z-slabs; 0 = local == global).  Fine inputs up to
+// 2 planes outside the slab are read from the ghost planes of `in`.
 __device__ __forceinline__ void restrict_item(const double* __restrict__ in, double* __restrict__ out, int n0, int n1,
-                                              int n2, int axis, int nc, int s, int kind, int64_t t) {
+                                              int n2, int axis, int nc, int s, int kind, int64_t t,
+                                              int in_off = 0, int nf_g = 0, int out_off = 0, int nc_g = 0) {
   const int o0 = (axis == 0) ? nc : n0, o1 = (axis == 1) ? nc : n1;
   const int nf = (axis == 0) ? n0 : (axis == 1) ? n1 : n2;
   const int64_t stride_ax = (axis == 0) ? 1 : (axis == 1) ? (int64_t)n0 : (int64_t)n0 * n1;
@@ -424,18 +435,19 @@ __device__ __forceinline__ void restrict_item(const double* __restrict__ in, dou
   const int64_t rr = t / o0;
   q[1] = (int)(rr % o1);
   q[2] = (int)(rr / o1);
-  const int I = q[axis];
+  const int I = q[axis] + out_off;
+  const int nfg = nf_g ? nf_g : nf, ncg = nc_g ? nc_g : nc;
   q[axis] = 0;
   const int64_t base = q[0] + (int64_t)n0 * (q[1] + (int64_t)n1 * q[2]);
   double acc = 0.0;
-  const int ilo = max(0, s * (I - 1)), ihi = min(nf, s * (I + 2));
+  const int ilo = max(0, s * (I - 1)), ihi = min(nfg, s * (I + 2));
   for (int i = ilo; i < ihi; ++i) {
     int I0, I1; double w0, w1;
-    interp_w(i, nc, s, kind, I0, w0, I1, w1);
+    interp_w(i, ncg, s, kind, I0, w0, I1, w1);
     double w = 0.0;
     if (I0 == I) w += w0;
     if (I1 == I && I1 != I0) w += w1;
-    if (w != 0.0) acc += w * in[base + i * stride_ax];
+    if (w != 0.0) acc += w * in[base + (int64_t)(i - in_off) * stride_ax];
   }
   out[t] = acc;
 }
@@ -477,7 +489,7 @@ __device__ __forceinline__ void resid_restrict_x_item(const LevelDev& L, const d
 template <int NDIM>
 __device__ __forceinline__ void prolong_black_item(const LevelDev& L, uint32_t hx, int ncx, int ncy, int ncz, int s,
                                                    int kind, const double* __restrict__ y, double* __restrict__ z,
-                                                   uint32_t t) {
+                                                   uint32_t t, int zc0 = 0) {
   const uint32_t row = t / hx;
   const uint32_t m = t - row * hx;
   const uint32_t k = row / (uint32_t)L.ny;
@@ -488,9 +500,9 @@ __device__ __forceinline__ void prolong_black_item(const LevelDev& L, uint32_t h
   double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
   interp_w(i, ncx, s, kind, X0, wx0, X1, wx1);
   interp_w((int)j, ncy, s, kind, Y0, wy0, Y1, wy1);
-  if (NDIM == 3) interp_w((int)k, ncz, s, kind, Z0, wz0, Z1, wz1);
+  if (NDIM == 3) interp_w((int)k + L.z0, ncz, s, kind, Z0, wz0, Z1, wz1);
   const int64_t cp = (int64_t)ncx * ncy;
-  auto Y = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * cc); };
+  auto Y = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * (cc - zc0)); };
   double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
                wy1 * (wx0 * Y(X0, Y1, Z0) + wx1 * Y(X1, Y1, Z0));
   if (NDIM == 3) {
@@ -502,19 +514,21 @@ __device__ __forceinline__ void prolong_black_item(const LevelDev& L, uint32_t h
 }
 
 // z_c += (E y)_c for fine cell c if it has colour `colour` (-1 = all).
+// Coarse z index: global (fine global k = k + z0, coarse global count ncz) then local
+// (minus zc0, the coarse array's global offset; its ghost plane serves Z = zc0 - 1).
 template <int NDIM>
 __device__ __forceinline__ void prolong_item(const LevelDev& L, int ncx, int ncy, int ncz, int s, int kind,
                                              const double* __restrict__ y, double* __restrict__ z, int colour,
-                                             int64_t c) {
+                                             int64_t c, int zc0 = 0) {
   const Cell e = cell_of(L, c);
   if (colour >= 0 && (((e.i + e.j + e.k + L.z0) & 1) != colour)) return;
   int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
   double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
   interp_w(e.i, ncx, s, kind, X0, wx0, X1, wx1);
   interp_w(e.j, ncy, s, kind, Y0, wy0, Y1, wy1);
-  if (NDIM == 3) interp_w(e.k, ncz, s, kind, Z0, wz0, Z1, wz1);
+  if (NDIM == 3) interp_w(e.k + L.z0, ncz, s, kind, Z0, wz0, Z1, wz1);
   const int64_t cp = (int64_t)ncx * ncy;
-  auto Y = [&](int a, int bb, int cc) { return y[a + (int64_t)ncx * bb + cp * cc]; };
+  auto Y = [&](int a, int bb, int cc) { return y[a + (int64_t)ncx * bb + cp * (cc - zc0)]; };
   double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
                wy1 * (wx0 * Y(X0, Y1, Z0) + wx1 * Y(X1, Y1, Z0));
   if (NDIM == 3) {
@@ -593,24 +607,27 @@ __global__ void k_resid_restrict_x(LevelDev L, const double* __restrict__ r, con
 
 template <int NDIM>
 __global__ void k_prolong_black(LevelDev L, int ncx, int ncy, int ncz, int s, int kind,
-                                const double* __restrict__ y, double* __restrict__ z) {
+                                const double* __restrict__ y, double* __restrict__ z, int zc0) {
   const uint32_t hx = (uint32_t)(L.nx + 1) >> 1;
   const int64_t total = (int64_t)hx * L.ny * L.nz;
   for (int64_t t = gtid(); t < total; t += gstride())
-    prolong_black_item<NDIM>(L, hx, ncx, ncy, ncz, s, kind, y, z, (uint32_t)t);
+    prolong_black_item<NDIM>(L, hx, ncx, ncy, ncz, s, kind, y, z, (uint32_t)t, zc0);
 }
 
 __global__ void k_restrict_axis(const double* __restrict__ in, double* __restrict__ out,
-                                int n0, int n1, int n2, int axis, int nc, int s, int kind) {
+                                int n0, int n1, int n2, int axis, int nc, int s, int kind,
+                                int in_off, int nf_g, int out_off, int nc_g) {
   const int o0 = (axis == 0) ? nc : n0, o1 = (axis == 1) ? nc : n1, o2 = (axis == 2) ? nc : n2;
   const int64_t total = (int64_t)o0 * o1 * o2;
-  for (int64_t t = gtid(); t < total; t += gstride()) restrict_item(in, out, n0, n1, n2, axis, nc, s, kind, t);
+  for (int64_t t = gtid(); t < total; t += gstride())
+    restrict_item(in, out, n0, n1, n2, axis, nc, s, kind, t, in_off, nf_g, out_off, nc_g);
 }
 
 template <int NDIM>
 __global__ void k_prolong_add(LevelDev L, int ncx, int ncy, int ncz, int s, int kind,
-                              const double* __restrict__ y, double* __restrict__ z, int colour) {
-  for (int64_t c = gtid(); c < L.N; c += gstride()) prolong_item<NDIM>(L, ncx, ncy, ncz, s, kind, y, z, colour, c);
+                              const double* __restrict__ y, double* __restrict__ z, int colour, int zc0) {
+  for (int64_t c = gtid(); c < L.N; c += gstride())
+    prolong_item<NDIM>(L, ncx, ncy, ncz, s, kind, y, z, colour, c, zc0);
 }
 
 // a10: direction + SpMV + p.q in one pass (neighbours' p formed on the fly).
@@ -638,6 +655,28 @@ __global__ void k_dot(int64_t n, const double* __restrict__ a, const double* __r
   double acc = 0.0;
   for (int64_t c = gtid(); c < n; c += gstride()) acc += a[c] * b[c];
   grid_sum_finish(acc, ro);
+}
+
+// Distributed levels: the ghost planes of p_out = z + beta p_in are formed locally from
+// the ghost planes of z and p_in (both halo-current), bit-identical to what the owning
+// rank computes, so p never needs its own halo exchange.
+__global__ void k_p_ghost(int64_t plane, int nz, const double* __restrict__ z, const double* __restrict__ pin,
+                          double* __restrict__ pout, const Scal* sc, int first) {
+  const double beta = first ? 0.0 : sc->rho / sc->rho_prev;
+  for (int64_t t = gtid(); t < 2 * plane; t += gstride()) {
+    const int64_t c = (t < plane) ? t - plane : t - plane + (int64_t)nz * plane;
+    pout[c] = first ? z[c] : z[c] + beta * pin[c];
+  }
+}
+
+// Sum of n per-rank partials in rank order (allreduce = allgather + this, deterministic
+// and identical on every rank).
+__global__ void k_sum_ordered(const double* __restrict__ g, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += g[i];
+    *out = s;
+  }
 }
 
 __global__ void k_axpy(int64_t n, double* __restrict__ x, const double* __restrict__ y) {

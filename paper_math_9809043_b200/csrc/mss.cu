@@ -21,6 +21,7 @@
 #include "internal.cuh"
 #include "kernels.cuh"
 #include "colwalk.cuh"
+#include "comm.cuh"
 
 using namespace mss;
 
@@ -164,6 +165,29 @@ static bool col_grid(const void* kern, const Level& l, dim3* grid, int* kchunk) 
     ctx->launches++;                                                                     \
   } while (0)
 
+// ---- distributed levels (z-slabs): halo exchange and CG-scalar allreduce
+static bool dist_level(const mss_ctx* ctx, int k) {
+  return ctx->comm && ctx->comm->size > 1 && k < ctx->ndist;
+}
+static int do_halo(mss_ctx* ctx, int k, double* v, int depth = 1) {
+  if (!dist_level(ctx, k)) return MSS_OK;
+  const Level& l = ctx->lv[k];
+  return ctx->comm->halo(ctx->stream, v, l.plane, l.nz, depth);
+}
+static int do_allred(mss_ctx* ctx, int k, double* dev) {
+  if (!dist_level(ctx, k)) return MSS_OK;
+  return ctx->comm->allreduce_sum(ctx->stream, dev);
+}
+static double global_N(const Level& l) { return (double)l.nx * l.ny * (double)(l.nzg ? l.nzg : l.nz); }
+
+// Slab partition of the global planes in units of s^ndist planes (so every distributed
+// level's slab boundaries, and the first replicated level's, fall on whole planes).
+static void slab_of(int64_t nzg0, int64_t unit, int P, int r, int64_t* z0, int64_t* z1) {
+  const int64_t units = nzg0 / unit;
+  *z0 = unit * (units * r / P);
+  *z1 = unit * (units * (r + 1) / P);
+}
+
 #define DISPATCH(ndim, kern, grid, ...)                               \
   do {                                                                \
     if ((ndim) == 3) LAUNCH(kern<3>, grid, __VA_ARGS__);              \
@@ -240,17 +264,21 @@ static double cell_bytes(const mss_ctx* ctx, int cls) {
 
 // ============================================================================ kernels wrappers
 static int op_dot(mss_ctx* ctx, int level, int64_t n, const double* a, const double* b, double* out) {
-  ProfScope ps(ctx, KC_DOT, level, cell_bytes(ctx, KC_DOT) * n);
-  LAUNCH(k_dot, grid_for(n), n, a, b, red_to(ctx, out, level, 0));
-  return MSS_OK;
+  {
+    ProfScope ps(ctx, KC_DOT, level, cell_bytes(ctx, KC_DOT) * n);
+    LAUNCH(k_dot, grid_for(n), n, a, b, red_to(ctx, out, level, 0));
+  }
+  return do_allred(ctx, level, out);
 }
 
 static int op_residual(mss_ctx* ctx, int k, const double* b, const double* x, double* r, double* rr_out) {
   Level& l = ctx->lv[k];
   RedOut ro = red_to(ctx, rr_out, k, 0);
-  ProfScope ps(ctx, KC_RESID, k, cell_bytes(ctx, KC_RESID) * l.N);
-  DISPATCH(ctx->ndim, k_residual, grid_for(l.N), l.dev(), b, x, r, ro);
-  return MSS_OK;
+  {
+    ProfScope ps(ctx, KC_RESID, k, cell_bytes(ctx, KC_RESID) * l.N);
+    DISPATCH(ctx->ndim, k_residual, grid_for(l.N), l.dev(), b, x, r, ro);
+  }
+  return rr_out ? do_allred(ctx, k, rr_out) : MSS_OK;
 }
 
 static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int colour, bool first,
@@ -305,24 +333,53 @@ static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half
   for (int h = 0; h < n_half; ++h) {
     const int col = (first_colour + h) & 1;
     const bool first = z_zero && h == 0;
-    TRY(op_halfsweep(ctx, k, r, z, col, first, (h == n_half - 1 && !first) ? dot_last : nullptr));
+    double* dot = (h == n_half - 1 && !first) ? dot_last : nullptr;
+    TRY(op_halfsweep(ctx, k, r, z, col, first, dot));
+    TRY(do_halo(ctx, k, z));                     // the next sweep reads this colour's ghosts
+    if (dot) TRY(do_allred(ctx, k, dot));
   }
   return MSS_OK;
 }
 
 // y/z passes of R = E^T from the x-restricted t1 (level k) to the coarse vector.
+// Distributed fine level: the z-pass reads 2 ghost planes of t2 (halo-exchanged) and
+// uses global plane indices; if the coarse level is the first replicated one, each rank
+// writes its coarse planes into the full vector and the slabs are gathered.
 static int op_restrict_yz(mss_ctx* ctx, int k, double* coarse) {
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   const int S = ctx->prm.scale, kind = ctx->prm.interp;
-  const double rb = (ctx->ndim == 3) ? 8.0 * (2.0 * c.nx * f.ny * f.nz + 2.0 * c.nx * c.ny * f.nz + c.N)
-                                     : 8.0 * ((double)c.nx * f.ny + c.N);
-  ProfScope ps(ctx, KC_RESTRICT, k, rb);
-  if (ctx->ndim == 3) {
-    LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * c.ny * f.nz), f.t1, f.t2, c.nx, f.ny, f.nz, 1, c.ny, S, kind);
-    LAUNCH(k_restrict_axis, grid_for(c.N), f.t2, coarse, c.nx, c.ny, f.nz, 2, c.nz, S, kind);
-  } else {
-    LAUNCH(k_restrict_axis, grid_for(c.N), f.t1, coarse, c.nx, f.ny, 1, 1, c.ny, S, kind);
+  const bool fd = dist_level(ctx, k), cd = dist_level(ctx, k + 1);
+  const int nczl = fd ? f.nz / S : c.nz;                       // coarse planes this rank produces
+  const int zc0 = fd ? f.z0 / S : 0;                           // their global offset
+  const int64_t cplane = (int64_t)c.nx * c.ny;
+  double* out = (fd && !cd) ? coarse + (int64_t)zc0 * cplane : coarse;
+  {
+    const double rb = (ctx->ndim == 3) ? 8.0 * (2.0 * c.nx * f.ny * f.nz + 2.0 * c.nx * c.ny * f.nz + c.N)
+                                       : 8.0 * ((double)c.nx * f.ny + c.N);
+    ProfScope ps(ctx, KC_RESTRICT, k, rb);
+    if (ctx->ndim == 3) {
+      LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * c.ny * f.nz), f.t1, f.t2, c.nx, f.ny, f.nz, 1, c.ny, S, kind,
+             0, 0, 0, 0);
+      if (fd) TRY(ctx->comm->halo(ctx->stream, f.t2, cplane, f.nz, 2));
+      LAUNCH(k_restrict_axis, grid_for(cplane * nczl), f.t2, out, c.nx, c.ny, f.nz, 2, nczl, S, kind, f.z0,
+             f.nzg, zc0, c.nzg);
+    } else {
+      LAUNCH(k_restrict_axis, grid_for(c.N), f.t1, coarse, c.nx, f.ny, 1, 1, c.ny, S, kind, 0, 0, 0, 0);
+    }
+  }
+  if (fd && !cd) {
+    const int P = ctx->comm->size;
+    std::vector<int64_t> off(P), len(P);
+    for (int q = 0; q < P; ++q) {
+      int64_t z0, z1;
+      slab_of(ctx->lv[0].nzg, ctx->slab_unit, P, q, &z0, &z1);
+      int64_t sc = 1;
+      for (int e = 0; e <= k; ++e) sc *= S;
+      off[q] = (z0 / sc) * cplane;
+      len[q] = ((z1 - z0) / sc) * cplane;
+    }
+    TRY(ctx->comm->gather(ctx->stream, coarse, off, len));
   }
   return MSS_OK;
 }
@@ -357,30 +414,39 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * f.ny * f.nz), s, f.t1, f.nx, f.ny, f.nz, 0, c.nx,
-         ctx->prm.scale, ctx->prm.interp);
+         ctx->prm.scale, ctx->prm.interp, 0, 0, 0, 0);
   return op_restrict_yz(ctx, k, coarse);
 }
 
 // z += E y on cells of `colour` (1 = black, the solver's case; -1 = all, hooks).
+// Distributed coarse level: its ghost planes (1 each side) are refreshed first; a
+// replicated coarse level is indexed by global plane.  The fine ghosts are refreshed
+// after (the next red sweep reads black ghosts).
 static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int colour) {
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
-  ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
-  dim3 cgrid;
-  int kch = 0;
-  if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && col_grid((const void*)k_prolong_col<4>, f, &cgrid, &kch)) {
-    k_prolong_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
-                                                                     ctx->prm.interp, y, z, kch);
-    ctx->launches++;
-  } else if (colour == 1) {
-    const int64_t work = (int64_t)((f.nx + 1) / 2) * f.ny * f.nz;
-    DISPATCH(ctx->ndim, k_prolong_black, grid_for(work), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
-             ctx->prm.interp, y, z);
-  } else {
-    DISPATCH(ctx->ndim, k_prolong_add, grid_for(f.N), f.dev(), c.nx, c.ny, c.nz, ctx->prm.scale,
-             ctx->prm.interp, y, z, colour);
+  const bool cd = dist_level(ctx, k + 1);
+  if (cd) TRY(ctx->comm->halo(ctx->stream, const_cast<double*>(y), c.plane, c.nz, 1));
+  const int zc0 = cd ? c.z0 : 0;
+  const int nczg = c.nzg ? c.nzg : c.nz;
+  {
+    ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
+    dim3 cgrid;
+    int kch = 0;
+    if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && col_grid((const void*)k_prolong_col<4>, f, &cgrid, &kch)) {
+      k_prolong_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(f.dev(), c.nx, c.ny, nczg, ctx->prm.scale,
+                                                                       ctx->prm.interp, y, z, kch, zc0);
+      ctx->launches++;
+    } else if (colour == 1) {
+      const int64_t work = (int64_t)((f.nx + 1) / 2) * f.ny * f.nz;
+      DISPATCH(ctx->ndim, k_prolong_black, grid_for(work), f.dev(), c.nx, c.ny, nczg, ctx->prm.scale,
+               ctx->prm.interp, y, z, zc0);
+    } else {
+      DISPATCH(ctx->ndim, k_prolong_add, grid_for(f.N), f.dev(), c.nx, c.ny, nczg, ctx->prm.scale,
+               ctx->prm.interp, y, z, colour, zc0);
+    }
   }
-  return MSS_OK;
+  return do_halo(ctx, k, z);
 }
 
 static int op_coarse_solve(mss_ctx* ctx, const double* b, double* x) {
@@ -449,11 +515,16 @@ static int pcg_level(mss_ctx* ctx, int k) {
     DISPATCH(ctx->ndim, k_pdir_spmv_dot, grid_for(l.N), l.dev(), l.z, pin, pout, l.q, ds,
              it == 0 ? 1 : 0, red_to(ctx, &ds->pq, k, 0));                 // a10
     }
+    if (dist_level(ctx, k)) {
+      LAUNCH(k_p_ghost, grid_for(2 * l.plane), l.plane, l.nz, l.z, pin, pout, ds, it == 0 ? 1 : 0);
+      TRY(do_allred(ctx, k, &ds->pq));
+    }
     l.pcur ^= 1;
     {
     ProfScope ps(ctx, KC_AXPY, k, cell_bytes(ctx, KC_AXPY) * l.N);
     LAUNCH(k_axpy_norm, grid_for(l.N), l.N, l.x, l.r, pout, l.q, ds, red_to(ctx, &ds->rr, k, 1));  // a11
     }
+    TRY(do_allred(ctx, k, &ds->rr));
     TRY(read_scal(ctx, k));                                                // a12
     const Scal& h = ctx->hscal[k];
     it++;
@@ -477,7 +548,7 @@ static void set_thresholds(mss_ctx* ctx, double eps2) {
   tail_mark_dirty(ctx);
   double fk = 1.0;
   for (int k = 0; k <= ctx->L; ++k) {
-    ctx->lv[k].thr = (double)ctx->lv[k].N * fk * eps2;
+    ctx->lv[k].thr = global_N(ctx->lv[k]) * fk * eps2;
     fk *= ctx->prm.f;
   }
 }
@@ -525,6 +596,7 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
   if (!ctx->prm.use_lift) CK(cudaMemcpyAsync(l.x, x, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
   DISPATCH(ctx->ndim, k_rhs_lift, grid_for(l.N), l.dev(), f, l.b, ctx->prm.use_lift ? l.x : nullptr,
            cell_volume(ctx), bc);
+  TRY(do_halo(ctx, 0, l.x));
   TRY(op_dot(ctx, 0, l.N, l.b, l.b, &ds->bb));
   TRY(read_scal(ctx, 0));
   const double bb = ctx->hscal[0].bb;
@@ -533,7 +605,7 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
   if (bb == 0.0) {
     CK(cudaMemsetAsync(l.x, 0, sizeof(double) * l.N, ctx->stream));
   } else {
-    set_thresholds(ctx, rel_tol * rel_tol * bb / (double)l.N);
+    set_thresholds(ctx, rel_tol * rel_tol * bb / global_N(l));
     TRY(op_residual(ctx, 0, l.b, l.x, l.r, &ds->rr));                // r0 = b - A x0
     if (ctx->L == 0) {
       ctx->info.calls[0] += 1;
@@ -554,6 +626,7 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
     if (trc == MSS_EBREAKDOWN && rc == MSS_OK) rc = MSS_EBREAKDOWN;
   }
   // true residual (O15)
+  TRY(do_halo(ctx, 0, l.x));
   TRY(op_residual(ctx, 0, l.b, l.x, l.s, &ds->aux));
   TRY(read_scal(ctx, 0));
   ctx->info.true_rel_res = (bb > 0) ? std::sqrt(ctx->hscal[0].aux / bb) : std::sqrt(ctx->hscal[0].aux);
@@ -641,6 +714,10 @@ static int free_ctx(mss_ctx* ctx) {
   for (cudaEvent_t e : ctx->ev_free) cudaEventDestroy(e);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->hscal) cudaFreeHost(ctx->hscal);
+  if (ctx->comm) {
+    if (ctx->comm->gbuf) cudaFree(ctx->comm->gbuf);
+    delete ctx->comm;
+  }
   delete ctx;
   return MSS_OK;
 }
@@ -652,11 +729,33 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   TRY(build_hierarchy_dims(ndim, n, s, depth, ctx->prm.coarse_min, dims));
   ctx->L = (int)dims.size() - 1;
   ctx->lv.resize(dims.size());
+  // z-slab decomposition: levels with N_k >= gather_below are split into
+  // z-slabs (level 0 always, the coarsest never); the others are replicated on every rank.
+  int64_t z0_0 = 0, z1_0 = dims[0][2];
+  ctx->ndist = 0;
+  if (ctx->comm && ctx->comm->size > 1) {
+    if (ndim != 3) return set_err(MSS_EINVAL, "distributed solves need a 3-D grid (z-slabs)");
+    if (ctx->L < 1) return set_err(MSS_EINVAL, "distributed solves need at least one coarsening");
+    int nd = 1;
+    while (nd < ctx->L && dims[nd][0] * dims[nd][1] * dims[nd][2] >= ctx->prm.gather_below) nd++;
+    ctx->ndist = nd;
+    int64_t unit = 1;
+    for (int e = 0; e < nd; ++e) unit *= s;
+    ctx->slab_unit = unit;
+    if (dims[0][2] % unit != 0 || dims[0][2] / unit < ctx->comm->size)
+      return set_err(MSS_EINVAL, "n_z must be a multiple of scale^ndist with at least one unit per rank");
+    slab_of(dims[0][2], unit, ctx->comm->size, ctx->comm->rank, &z0_0, &z1_0);
+  }
   for (size_t k = 0; k < dims.size(); ++k) {
     Level& l = ctx->lv[k];
     l.nx = (int)dims[k][0];
     l.ny = (int)dims[k][1];
-    l.nz = (int)dims[k][2];
+    l.nzg = (int)dims[k][2];
+    int64_t sc = 1;
+    for (size_t e = 0; e < k; ++e) sc *= s;
+    l.dist = (int)k < ctx->ndist;
+    l.nz = l.dist ? (int)((z1_0 - z0_0) / sc) : l.nzg;
+    l.z0 = l.dist ? (int)(z0_0 / sc) : 0;
     l.plane = (int64_t)l.nx * l.ny;
     l.N = l.plane * l.nz;
     for (int d = 0; d < 3; ++d) l.h[d] = ctx->extent[d] / (double)dims[k][d];
@@ -678,7 +777,13 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     Level& f = ctx->lv[k];
     Level& c = ctx->lv[k + 1];
     TRY(dalloc(ctx, (void**)&f.t1, sizeof(double) * (size_t)c.nx * f.ny * f.nz));
-    TRY(dalloc(ctx, (void**)&f.t2, sizeof(double) * (size_t)c.nx * c.ny * f.nz));
+    {
+      const int64_t cp = (int64_t)c.nx * c.ny;   // t2: (ncx, ncy, nz_fine) + 2 ghost planes each side
+      void* p = nullptr;
+      TRY(dalloc(ctx, &p, sizeof(double) * (size_t)cp * (f.nz + 4)));
+      CK(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)cp * (f.nz + 4), ctx->stream));
+      f.t2 = reinterpret_cast<double*>(p) + 2 * cp;
+    }
   }
   // 1-D transfer weight tables, built on the host with the same rule as
   // interp_w and uploaded once; the cluster tail stages them in shared memory.
@@ -723,18 +828,72 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     const double coef = area / l0.h[d];
     double* T = (d == 0) ? l0.Tx : (d == 1) ? l0.Ty : l0.Tz;
     const int64_t nf = (int64_t)(l0.nx + (d == 0)) * (l0.ny + (d == 1)) * (l0.nz + (d == 2));
+    double* Kext = nullptr;
+    if (d == 2 && l0.dist) {
+      // the z faces at the slab ends need K of the neighbours' boundary planes
+      CK(cudaMalloc((void**)&Kext, sizeof(double) * (size_t)l0.plane * (l0.nz + 2)));
+      CK(cudaMemsetAsync(Kext, 0, sizeof(double) * (size_t)l0.plane * (l0.nz + 2), ctx->stream));
+      CK(cudaMemcpyAsync(Kext + l0.plane, Kd, sizeof(double) * l0.N, cudaMemcpyDeviceToDevice, ctx->stream));
+      TRY(ctx->comm->halo(ctx->stream, Kext + l0.plane, l0.plane, l0.nz, 1));
+      Kd = Kext + l0.plane;
+    }
     LAUNCH(k_assemble_faces, grid_for(nf), Kd, T, l0.nx, l0.ny, l0.nz, d, coef,
-           ctx->bc[2 * d].kind == 1, ctx->bc[2 * d + 1].kind == 1);
+           ctx->bc[2 * d].kind == 1, ctx->bc[2 * d + 1].kind == 1, l0.z0, l0.nzg);
+    if (Kext) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(Kext);
+    }
   }
   // a2: coarse faces, level by level
   for (int k = 1; k <= ctx->L; ++k) {
     Level& f = ctx->lv[k - 1];
     Level& c = ctx->lv[k];
+    const bool fd = f.dist, cd = c.dist;
+    // coarse planes this rank computes and their global offset (the local slab of c)
+    const int nczl = fd ? f.nz / s : c.nz;
+    const int Zc0 = fd ? f.z0 / s : 0;
+    double* Tzext = nullptr;
+    if (fd) {
+      // fine z faces with 2 ghost face planes each side (Reading-B control volumes
+      // of the coarse faces at the slab ends reach 2 fine faces into the neighbours)
+      const int64_t fp = f.plane;
+      CK(cudaMalloc((void**)&Tzext, sizeof(double) * (size_t)fp * (f.nz + 1 + 4)));
+      CK(cudaMemsetAsync(Tzext, 0, sizeof(double) * (size_t)fp * (f.nz + 1 + 4), ctx->stream));
+      double* ti = Tzext + 2 * fp;
+      CK(cudaMemcpyAsync(ti, f.Tz, sizeof(double) * (size_t)fp * (f.nz + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+      TRY(ctx->comm->exch(ctx->stream, ti + fp, ti - 2 * fp, ti + (int64_t)(f.nz - 2) * fp,
+                          ti + (int64_t)(f.nz + 1) * fp, (size_t)2 * fp));
+    }
     for (int d = 0; d < ndim; ++d) {
       const double* Tf = (d == 0) ? f.Tx : (d == 1) ? f.Ty : f.Tz;
+      if (d == 2 && fd) Tf = Tzext + 2 * f.plane;
       double* Tc = (d == 0) ? c.Tx : (d == 1) ? c.Ty : c.Tz;
-      const int64_t nf = (int64_t)(c.nx + (d == 0)) * (c.ny + (d == 1)) * (c.nz + (d == 2));
-      LAUNCH(k_coarsen_faces, grid_for(nf), Tf, Tc, f.nx, f.ny, f.nz, c.nx, c.ny, c.nz, d, s, ndim);
+      const int64_t cpl = (int64_t)(c.nx + (d == 0)) * (c.ny + (d == 1));   // elements per coarse face plane
+      if (fd && !cd) Tc += (int64_t)Zc0 * cpl;                               // this rank's segment of the full array
+      const int64_t nf = cpl * (nczl + (d == 2));
+      LAUNCH(k_coarsen_faces, grid_for(nf), Tf, Tc, f.nx, f.ny, f.nz, c.nx, c.ny, nczl, d, s, ndim, f.z0, f.nzg, Zc0);
+    }
+    if (fd && !cd) {
+      // first replicated level: gather every rank's slab of the coarse faces
+      const int P = ctx->comm->size;
+      for (int d = 0; d < ndim; ++d) {
+        double* Tc = (d == 0) ? c.Tx : (d == 1) ? c.Ty : c.Tz;
+        const int64_t cpl = (int64_t)(c.nx + (d == 0)) * (c.ny + (d == 1));
+        std::vector<int64_t> off(P), len(P);
+        for (int q = 0; q < P; ++q) {
+          int64_t a, b;
+          slab_of(ctx->lv[0].nzg, ctx->slab_unit, P, q, &a, &b);
+          int64_t sc = 1;
+          for (int e = 0; e < k; ++e) sc *= s;
+          off[q] = (a / sc) * cpl;
+          len[q] = ((b - a) / sc + ((d == 2 && q == P - 1) ? 1 : 0)) * cpl;
+        }
+        TRY(ctx->comm->gather(ctx->stream, Tc, off, len));
+      }
+    }
+    if (Tzext) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(Tzext);
     }
   }
   // a3: dense coarsest matrix, Cholesky, inverse
@@ -804,8 +963,11 @@ const char* mss_strerror(int code) {
 
 const char* mss_last_error(void) { return g_err.c_str(); }
 
-int mss_setup(mss_ctx** out, int ndim, const int64_t n[3], const double extent[3], const double* K,
-              int k_comp, const mss_bc bc[6], int depth, const mss_params* p, void* stream) {
+// Common setup: comm == nullptr is the single-GPU context; otherwise n is the GLOBAL
+// grid, K the rank's z-slab, and the context owns `comm`.
+static int setup_common(mss_ctx** out, mss::Comm* comm, int ndim, const int64_t n[3], const double extent[3],
+                        const double* K, int k_comp, const mss_bc bc[6], int depth, const mss_params* p,
+                        void* stream) {
   if (!out) return set_err(MSS_EINVAL, "out is NULL");
   *out = nullptr;
   if (ndim != 2 && ndim != 3) return set_err(MSS_EINVAL, "ndim must be 2 or 3");
@@ -831,11 +993,22 @@ int mss_setup(mss_ctx** out, int ndim, const int64_t n[3], const double extent[3
   mss_ctx* ctx = new mss_ctx();
   ctx->ndim = ndim;
   ctx->prm = prm;
+  ctx->comm = comm;
+  if (comm) {
+    ctx->rank = comm->rank;
+    ctx->nranks = comm->size;
+  }
   for (int s = 0; s < 6; ++s) ctx->bc[s] = (s < 2 * ndim) ? bc[s] : mss_bc{0, 0.0};
   for (int d = 0; d < 3; ++d) ctx->extent[d] = (extent && d < ndim) ? extent[d] : 1.0;
   ctx->stream = reinterpret_cast<cudaStream_t>(stream);
   cudaGetDevice(&ctx->device);
   memset(&ctx->info, 0, sizeof(ctx->info));
+  if (comm && comm->size > 1 && !comm->gbuf) {
+    if (cudaMalloc((void**)&comm->gbuf, sizeof(double) * comm->size) != cudaSuccess) {
+      delete ctx;
+      return set_err(MSS_ENOMEM, "comm buffer");
+    }
+  }
   int rc = setup_impl(ctx, n, K, k_comp, depth);
   if (rc != MSS_OK) {
     free_ctx(ctx);
@@ -845,10 +1018,15 @@ int mss_setup(mss_ctx** out, int ndim, const int64_t n[3], const double extent[3
   for (int k = 0; k <= ctx->L; ++k) {
     ctx->info.dims[k][0] = ctx->lv[k].nx;
     ctx->info.dims[k][1] = ctx->lv[k].ny;
-    ctx->info.dims[k][2] = ctx->lv[k].nz;
+    ctx->info.dims[k][2] = ctx->lv[k].nzg;
   }
   *out = ctx;
   return MSS_OK;
+}
+
+int mss_setup(mss_ctx** out, int ndim, const int64_t n[3], const double extent[3], const double* K,
+              int k_comp, const mss_bc bc[6], int depth, const mss_params* p, void* stream) {
+  return setup_common(out, nullptr, ndim, n, extent, K, k_comp, bc, depth, p, stream);
 }
 
 int mss_free(mss_ctx* ctx) { return free_ctx(ctx); }
@@ -1048,27 +1226,88 @@ int mss_rhs_lift(mss_ctx* ctx, const double* f, double* b, double* x0) {
 
 }  // extern "C"
 
-// ---- distributed entry points (z-slabs over NCCL) — see dist.cu
+// ---- distributed entry points (z-slabs; comm.cuh)
+static int compute_ndist_unit(int ndim, const int64_t n[3], const mss_params* p, int depth, int64_t* unit) {
+  mss_params prm;
+  mss_default_params(&prm);
+  if (p) prm = *p;
+  std::vector<std::array<int64_t, 3>> dims;
+  TRY(build_hierarchy_dims(ndim, n, prm.scale, depth, prm.coarse_min, dims));
+  const int L = (int)dims.size() - 1;
+  if (L < 1) return set_err(MSS_EINVAL, "distributed solves need at least one coarsening");
+  int nd = 1;
+  while (nd < L && dims[nd][0] * dims[nd][1] * dims[nd][2] >= prm.gather_below) nd++;
+  *unit = 1;
+  for (int e = 0; e < nd; ++e) *unit *= prm.scale;
+  return nd;
+}
+
 extern "C" {
 int mss_nccl_unique_id(unsigned char id[128]) {
+#ifdef MSS_WITH_NCCL
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return set_err(MSS_ENCCL, "ncclGetUniqueId failed");
+  static_assert(sizeof(u) == 128, "NCCL unique id size");
+  memcpy(id, &u, 128);
+  return MSS_OK;
+#else
   (void)id;
-  return set_err(MSS_EUNSUPPORTED, "distributed build not enabled");
+  return set_err(MSS_EUNSUPPORTED, "built without NCCL");
+#endif
 }
-int mss_slab_range(const int64_t n_global[3], int ndim, int scale, int depth, int rank, int nranks,
+
+int mss_slab_range(const int64_t n_global[3], int ndim, const mss_params* p, int depth, int rank, int nranks,
                    int64_t* z_begin, int64_t* z_end) {
   if (!n_global || !z_begin || !z_end || nranks < 1 || rank < 0 || rank >= nranks || ndim != 3)
     return set_err(MSS_EINVAL, "bad slab arguments");
-  (void)scale; (void)depth;
-  const int64_t nz = n_global[2];
-  *z_begin = nz * rank / nranks;
-  *z_end = nz * (rank + 1) / nranks;
+  int64_t unit = 1;
+  const int nd = compute_ndist_unit(ndim, n_global, p, depth, &unit);
+  if (nd < 0) return nd;
+  if (n_global[2] % unit != 0 || n_global[2] / unit < nranks)
+    return set_err(MSS_EINVAL, "n_z must be a multiple of scale^ndist with at least one unit per rank");
+  slab_of(n_global[2], unit, nranks, rank, z_begin, z_end);
   return MSS_OK;
 }
+
 int mss_setup_dist(mss_ctx** out, int rank, int nranks, const unsigned char id[128], int ndim,
                    const int64_t n_global[3], const double extent[3], const double* K_local, int k_comp,
                    const mss_bc bc[6], int depth, const mss_params* p, void* stream) {
+#ifdef MSS_WITH_NCCL
+  if (!out || !id || nranks < 1 || rank < 0 || rank >= nranks) return set_err(MSS_EINVAL, "bad rank arguments");
+  mss::NcclComm* c = new mss::NcclComm();
+  c->rank = rank;
+  c->size = nranks;
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  if (ncclCommInitRank(&c->c, nranks, u, rank) != ncclSuccess) {
+    delete c;
+    return set_err(MSS_ENCCL, "ncclCommInitRank failed");
+  }
+  return setup_common(out, c, ndim, n_global, extent, K_local, k_comp, bc, depth, p, stream);
+#else
   (void)out; (void)rank; (void)nranks; (void)id; (void)ndim; (void)n_global; (void)extent;
   (void)K_local; (void)k_comp; (void)bc; (void)depth; (void)p; (void)stream;
-  return set_err(MSS_EUNSUPPORTED, "distributed build not enabled");
+  return set_err(MSS_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int mss_loopback_create(int nranks, void** group) {
+  if (!group || nranks < 1) return set_err(MSS_EINVAL, "bad loopback arguments");
+  *group = new mss::LoopGroup(nranks);
+  return MSS_OK;
+}
+
+int mss_loopback_destroy(void* group) {
+  delete reinterpret_cast<mss::LoopGroup*>(group);
+  return MSS_OK;
+}
+
+int mss_setup_loopback(mss_ctx** out, void* group, int rank, int ndim, const int64_t n_global[3],
+                       const double extent[3], const double* K_local, int k_comp, const mss_bc bc[6], int depth,
+                       const mss_params* p, void* stream) {
+  mss::LoopGroup* g = reinterpret_cast<mss::LoopGroup*>(group);
+  if (!g || rank < 0 || rank >= g->size) return set_err(MSS_EINVAL, "bad loopback rank");
+  mss::LoopComm* c = new mss::LoopComm(g, rank);
+  return setup_common(out, c, ndim, n_global, extent, K_local, k_comp, bc, depth, p, stream);
 }
 }

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const TailArgs* __rest
 // ============================================================================ host side
 static int tail_setup(mss_ctx* ctx) {
   ctx->tail_cs = 0;
-  if (ctx->prm.tail_cells <= 0 || ctx->nranks > 1) return MSS_OK;
+  if (ctx->prm.tail_cells <= 0) return MSS_OK;
   auto kern = (ctx->ndim == 3) ? (void*)mss::k_tail<3> : (void*)mss::k_tail<2>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   for (int cs : {16, 8, 4}) {
@@ -297,7 +297,7 @@ static int tail_setup(mss_ctx* ctx) {
 }
 
 static bool tail_supported(mss_ctx* ctx, int k) {
-  return ctx->tail_cs > 0 && k >= 1 && k < ctx->L && ctx->lv[k].N <= ctx->prm.tail_cells;
+  return ctx->tail_cs > 0 && k >= 1 && k >= ctx->ndist && k < ctx->L && ctx->lv[k].N <= ctx->prm.tail_cells;
 }
 
 static void tail_mark_dirty(mss_ctx* ctx) {

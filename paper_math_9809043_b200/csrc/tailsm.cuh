@@ -14,6 +14,7 @@
 // operand order): half-sweep P:353-357, residual O4, transfer P:412-428, CG P:440-441.
 #pragma once
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -651,10 +652,10 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
 static void tailsm_setup(mss_ctx* ctx) {
   const bool dbg = getenv("MSS_DEBUG") != nullptr;
   ctx->tsm_L0 = -1;
-  if (ctx->prm.tail_cells <= 0 || ctx->nranks > 1 || ctx->L < 1) return;
+  if (ctx->prm.tail_cells <= 0 || ctx->L < 1) return;
   if (getenv("MSS_NO_TAILSM")) return;
   int L0 = -1;
-  for (int q = 1; q < ctx->L; ++q)
+  for (int q = std::max(1, ctx->ndist); q < ctx->L; ++q)
     if (ctx->lv[q].N <= ctx->prm.tail_cells) { L0 = q; break; }
   if (L0 < 0) return;
   const int cs = 16;

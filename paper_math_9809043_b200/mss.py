@@ -91,8 +91,13 @@ SIGNATURES = [
     ("mss_coarse_solve", ctypes.c_int, [P, P, P]),
     ("mss_rhs_lift", ctypes.c_int, [P, P, P, P]),
     ("mss_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
-    ("mss_slab_range", ctypes.c_int, [I64P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+    ("mss_slab_range", ctypes.c_int, [I64P, ctypes.c_int, ctypes.POINTER(Params), ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, I64P, I64P]),
+    ("mss_loopback_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(P)]),
+    ("mss_loopback_destroy", ctypes.c_int, [P]),
+    ("mss_setup_loopback", ctypes.c_int, [ctypes.POINTER(P), P, ctypes.c_int, ctypes.c_int, I64P, DP, P,
+                                          ctypes.c_int, ctypes.POINTER(BC), ctypes.c_int, ctypes.POINTER(Params),
+                                          P]),
     ("mss_setup_dist", ctypes.c_int, [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                       ctypes.c_int, I64P, DP, P, ctypes.c_int, ctypes.POINTER(BC),
                                       ctypes.c_int, ctypes.POINTER(Params), P]),
@@ -149,6 +154,40 @@ def default_params(**kw) -> Params:
     return p
 
 
+def slab_range(n_global, rank: int, nranks: int, params: Optional[dict] = None, depth: Optional[int] = None):
+    """[z_begin, z_end) of level-0 planes owned by `rank` (mss_slab_range)."""
+    lib = load_library()
+    prm = default_params(**(params or {}))
+    nn = (ctypes.c_int64 * 3)(*[int(v) for v in n_global])
+    zb, ze = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.mss_slab_range(nn, 3, ctypes.byref(prm), -1 if depth is None else int(depth), int(rank), int(nranks),
+                              ctypes.byref(zb), ctypes.byref(ze)), "mss_slab_range", allow_nc=False)
+    return zb.value, ze.value
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.mss_nccl_unique_id(buf), "mss_nccl_unique_id", allow_nc=False)
+    return buf.raw
+
+
+class LoopbackGroup:
+    """P ranks as host threads of one process on one GPU (tests of the decomposition)."""
+
+    def __init__(self, size: int):
+        self.lib = load_library()
+        self.size = size
+        h = P()
+        _check(self.lib.mss_loopback_create(int(size), ctypes.byref(h)), "mss_loopback_create", allow_nc=False)
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            self.lib.mss_loopback_destroy(self.handle)
+            self.handle = None
+
+
 @dataclass
 class SolveReport:
     rc: int
@@ -166,14 +205,27 @@ class Solver:
     """mss_setup / mss_solve / mss_free on CUDA tensors (see include/mss.h)."""
 
     def __init__(self, ndim: int, n: Sequence[int], K: torch.Tensor, bc, depth: Optional[int] = None,
-                 params: Optional[dict] = None, extent: Optional[Sequence[float]] = None, stream=None):
+                 params: Optional[dict] = None, extent: Optional[Sequence[float]] = None, stream=None,
+                 comm=None):
+        """n: global grid.  comm: None (one GPU), ("nccl", rank, nranks, id_bytes) or
+        ("loop", LoopbackGroup, rank); with a comm, K is the rank's z-slab (mss_slab_range)
+        and solve() takes / returns the rank's slab of f and x."""
         lib = load_library()
         self.lib = lib
         self.ndim = ndim
         nx, ny = int(n[0]), int(n[1])
         nz = int(n[2]) if ndim == 3 else 1
-        self.n = (nx, ny, nz)
-        self.N = nx * ny * nz
+        self.n_global = (nx, ny, nz)
+        depth_arg = -1 if depth is None else int(depth)
+        prm = default_params(**(params or {}))
+        self.z_range = (0, nz)
+        if comm is not None:
+            rank = comm[2] if comm[0] == "loop" else comm[1]
+            nranks = comm[1].size if comm[0] == "loop" else comm[2]
+            self.z_range = slab_range((nx, ny, nz), rank, nranks, params=params, depth=depth)
+        nzl = self.z_range[1] - self.z_range[0]
+        self.n = (nx, ny, nzl)
+        self.N = nx * ny * nzl
         if K.dim() == ndim:
             K = K.unsqueeze(0)
         K = K.contiguous()
@@ -181,14 +233,27 @@ class Solver:
         _dev_ptr(K, k_comp * self.N)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         bcs = (BC * 6)(*[BC(int(k), float(v)) for k, v in bc] + [BC(0, 0.0)] * (6 - len(bc)))
-        prm = default_params(**(params or {}))
         nn = (ctypes.c_int64 * 3)(nx, ny, nz)
         ext = (ctypes.c_double * 3)(*(list(extent) + [1.0] * (3 - len(extent)))) if extent else None
         ctx = P()
-        rc = lib.mss_setup(ctypes.byref(ctx), ndim, nn, ext, K.data_ptr(), k_comp, bcs,
-                           -1 if depth is None else int(depth), ctypes.byref(prm),
-                           ctypes.c_void_p(self.stream.cuda_stream))
-        _check(rc, "mss_setup", allow_nc=False)
+        st = ctypes.c_void_p(self.stream.cuda_stream)
+        if comm is None:
+            rc = lib.mss_setup(ctypes.byref(ctx), ndim, nn, ext, K.data_ptr(), k_comp, bcs, depth_arg,
+                               ctypes.byref(prm), st)
+            where = "mss_setup"
+        elif comm[0] == "loop":
+            rc = lib.mss_setup_loopback(ctypes.byref(ctx), comm[1].handle, int(comm[2]), ndim, nn, ext, K.data_ptr(),
+                                        k_comp, bcs, depth_arg, ctypes.byref(prm), st)
+            where = "mss_setup_loopback"
+        elif comm[0] == "nccl":
+            idb = bytes(comm[3])
+            assert len(idb) == 128
+            rc = lib.mss_setup_dist(ctypes.byref(ctx), int(comm[1]), int(comm[2]), idb, ndim, nn, ext,
+                                    K.data_ptr(), k_comp, bcs, depth_arg, ctypes.byref(prm), st)
+            where = "mss_setup_dist"
+        else:
+            raise ValueError(comm)
+        _check(rc, where, allow_nc=False)
         self.ctx = ctx
         L1 = ctypes.c_int()
         lib.mss_num_levels(ctx, ctypes.byref(L1))

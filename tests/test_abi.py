@@ -56,11 +56,11 @@ def test_sass_is_sm100a(lib_path):
 def test_slab_range_partitions(lib_path):
     from paper_math_9809043_b200 import mss
     lib = mss.load_library()
-    n = (ctypes.c_int64 * 3)(64, 64, 512)
+    n = (ctypes.c_int64 * 3)(512, 512, 512)
     ends = []
     for r in range(8):
         zb, ze = ctypes.c_int64(), ctypes.c_int64()
-        assert lib.mss_slab_range(n, 3, 4, -1, r, 8, ctypes.byref(zb), ctypes.byref(ze)) == 0
+        assert lib.mss_slab_range(n, 3, None, -1, r, 8, ctypes.byref(zb), ctypes.byref(ze)) == 0
         ends.append((zb.value, ze.value))
     assert ends[0][0] == 0 and ends[-1][1] == 512
     assert all(ends[i][1] == ends[i + 1][0] for i in range(7))
