@@ -326,10 +326,61 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   return MSS_OK;
 }
 
+// Temporally fused pair of half-sweeps (colour col1 then the other) zin -> zout.
+static bool pair_ok(const mss_ctx* ctx, int k) {
+  // opt-in (MSS_PAIR=1) until it beats two single sweeps
+  static int enabled = -1;
+  if (enabled < 0) enabled = getenv("MSS_PAIR") ? 1 : 0;
+  return enabled && col_ok(ctx, ctx->lv[k]) && !dist_level(ctx, k);
+}
+
+static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, double* zout, int col1, bool first) {
+  Level& l = ctx->lv[k];
+  const int hx = l.nx / 2;
+  const int bx = (hx + kPX - 3) / (kPX - 2), by = (l.ny + kPY - 3) / (kPY - 2);
+  int nch = (l.nz + kColChunk - 1) / kColChunk;
+  if ((int64_t)nch * bx * by > kMaxPartials) nch = std::max(1, kMaxPartials / (bx * by));
+  const int kch = (l.nz + nch - 1) / nch;
+  nch = (l.nz + kch - 1) / kch;
+  // algorithmic bytes: T + r + zout (+ zin when not from zero), 2 half-sweeps per pass
+  ProfScope ps(ctx, first ? KC_SWEEP0 : KC_SWEEP, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
+  const dim3 grid(bx, by, nch), blk(kPX, kPY);
+  if (first) k_sweep2_col<true><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
+  else k_sweep2_col<false><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
+  ctx->launches++;
+  return MSS_OK;
+}
+
 // n_half alternating half-sweeps starting with `first_colour`; the last one also
-// reduces r.z into *dot_last when given.
+// reduces r.z into *dot_last when given.  On pair-eligible levels consecutive half-sweeps
+// run as fused pairs ping-ponging between the level's z and s buffers (the Level's z
+// pointer is swapped when the result lands in s, so z must be the level's own z).
 static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero,
                      double* dot_last = nullptr) {
+  Level& l = ctx->lv[k];
+  if (z == l.z && n_half >= 2 && pair_ok(ctx, k)) {
+    const int npairs = (n_half - (dot_last ? 1 : 0)) / 2;
+    double* cur = l.z;
+    double* oth = l.s;
+    for (int pi = 0; pi < npairs; ++pi) {
+      const int col1 = (first_colour + 2 * pi) & 1;
+      TRY(op_pair(ctx, k, r, cur, oth, col1, z_zero && pi == 0));
+      std::swap(cur, oth);
+    }
+    if (cur != l.z) {
+      l.s = l.z;
+      l.z = cur;
+      tail_mark_dirty(ctx);
+    }
+    for (int h = 2 * npairs; h < n_half; ++h) {
+      const int col = (first_colour + h) & 1;
+      const bool first = z_zero && h == 0;
+      double* dot = (h == n_half - 1 && !first) ? dot_last : nullptr;
+      TRY(op_halfsweep(ctx, k, r, l.z, col, first, dot));
+      if (dot) TRY(do_allred(ctx, k, dot));
+    }
+    return MSS_OK;
+  }
   for (int h = 0; h < n_half; ++h) {
     const int col = (first_colour + h) & 1;
     const bool first = z_zero && h == 0;

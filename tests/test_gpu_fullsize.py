@@ -1,0 +1,159 @@
+"""GPU parity at BASELINE.json's full sizes, in the configuration bench.py times.
+
+At 512^3 the oracle cannot run whole, so it is evaluated cell by cell: for each sampled
+cell the oracle assembles the faces of the 3x3x3 block of cells around it (with the
+global boundary conditions where the block touches the domain boundary) and applies its
+operator / half-sweep there; the centre value depends only on faces between the centre
+and its neighbours, so it is exact.  Full solves are checked through properties that hold
+at any size: the library's true residual, and an independent per-cell residual from the
+oracle's formulas on the sampled cells.
+"""
+import numpy as np
+import pytest
+
+from oracle import mss_oracle as O
+from workloads import make_workload
+
+pytestmark = pytest.mark.gpu
+
+
+def local_block(w, i, j, k):
+    """K sub-block around (i,j,k), its BC table, and the slices / centre position."""
+    nx, ny, nz = w.n
+    lo = [max(0, i - 1), max(0, j - 1), max(0, k - 1)]
+    hi = [min(nx, i + 2), min(ny, j + 2), min(nz, k + 2)]
+    sl = (slice(lo[2], hi[2]), slice(lo[1], hi[1]), slice(lo[0], hi[0]))
+    bc = []
+    for d in range(3):
+        bc.append(w.bc[2 * d] if lo[d] == 0 else (0, 0.0))                       # artificial side: Neumann
+        bc.append(w.bc[2 * d + 1] if hi[d] == w.n[d] else (0, 0.0))
+    # spacing must be the global one: scale the block's "unit box" so h matches
+    n_sub = (hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2])
+    centre = (k - lo[2], j - lo[1], i - lo[0])
+    return sl, bc, n_sub, centre
+
+
+def oracle_faces_local(w, sl, bc, n_sub):
+    """Faces of the sub-block with the GLOBAL spacing h = 1/n (the oracle's geometry
+    takes h = 1/n_sub, so rescale: T = (A/h) K scales as h in 3-D -> multiply by
+    h_global/h_sub)."""
+    Ksub = w.K[(slice(None),) + sl]
+    T = O.assemble_faces(3, n_sub, Ksub, bc)
+    scale = [(1.0 / w.n[d]) / (1.0 / n_sub[d]) for d in range(3)]
+    out = []
+    for d in range(3):
+        # T_d = (h_e h_f / h_d) K: apply the ratio of the three spacings
+        e, f = [a for a in range(3) if a != d]
+        out.append(T[d] * scale[e] * scale[f] / scale[d])
+    return out
+
+
+@pytest.fixture(scope="module")
+def c5():
+    import torch
+    from paper_math_9809043_b200 import build
+    build.build()
+    from paper_math_9809043_b200.mss import Solver
+    w = make_workload("C5")
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth)
+    return torch, w, s
+
+
+def samples(w, n=96, seed=5):
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = w.n
+    pts = [(rng.integers(0, nx), rng.integers(0, ny), rng.integers(0, nz)) for _ in range(n)]
+    # include faces, edges and corners of the domain
+    pts += [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (0, ny // 2, nz // 3), (nx - 1, 5, 0), (7, 0, nz - 1)]
+    return pts
+
+
+def test_fullsize_apply_A_sampled(c5):
+    torch, w, s = c5
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(w.shape)
+    y = s.apply_A(0, torch.from_numpy(x.ravel()).cuda()).cpu().numpy().reshape(w.shape)
+    worst = 0.0
+    for (i, j, k) in samples(w):
+        sl, bc, n_sub, cen = local_block(w, i, j, k)
+        T = oracle_faces_local(w, sl, bc, n_sub)
+        ref = O.apply_A(T, x[sl])[cen]
+        worst = max(worst, abs(y[k, j, i] - ref) / (abs(ref) + 1e-300))
+    assert worst <= 1e-12, worst
+
+
+def test_fullsize_halfsweep_sampled(c5):
+    """One black half-sweep from a random z at 512^3 (the column-walk kernel bench.py
+    times) against the oracle's half-sweep formula on sampled black cells."""
+    torch, w, s = c5
+    rng = np.random.default_rng(2)
+    r = rng.standard_normal(w.shape)
+    z0 = rng.standard_normal(w.shape)
+    z1 = s.smooth(0, torch.from_numpy(r.ravel()).cuda(), torch.from_numpy(z0.ravel()).cuda(), 1, 1)
+    z1 = z1.cpu().numpy().reshape(w.shape)
+    worst = 0.0
+    for (i, j, k) in samples(w):
+        sl, bc, n_sub, cen = local_block(w, i, j, k)
+        T = oracle_faces_local(w, sl, bc, n_sub)
+        zz = z0[sl].copy()
+        dg = O.diagonal(T, zz.shape)
+        O.halfsweep(T, dg, r[sl], zz, 1, O.colour_mask(zz.shape, 1, zoff=(i - cen[2]) + (j - cen[1]) + (k - cen[0])))
+        ref = zz[cen]
+        got = z1[k, j, i]
+        if (i + j + k) % 2 == 0:
+            assert got == z0[k, j, i]            # red cells untouched by a black half-sweep
+            continue
+        worst = max(worst, abs(got - ref) / (abs(ref) + 1e-300))
+    assert worst <= 1e-12, worst
+
+
+def test_fullsize_solve_properties(c5):
+    """The bench workload solved to rel 1e-10: the library's true residual, and the
+    per-cell residual b - A x from the oracle's formulas at sampled cells."""
+    torch, w, s = c5
+    x, rep = s.solve(torch.from_numpy(w.f.ravel()).cuda(), rel_tol=w.rel_tol)
+    assert not rep.not_converged
+    assert rep.true_rel_res <= 1e-10
+    x = x.cpu().numpy().reshape(w.shape)
+    # ||b||: f = 0, so b is the Dirichlet boundary source only (O5)
+    T0 = None
+    bnorm2 = 0.0
+    nx, ny, nz = w.n
+    h = 1.0 / nx
+    Kx = w.K[0]
+    # boundary faces on x-: T = 2 (A/h) K with A/h = h (cubic cells), g = 1; x+: g = 0
+    bnorm2 = float(np.sum((2.0 * h * Kx[:, :, 0] * 1.0) ** 2))
+    worst = 0.0
+    for (i, j, k) in samples(w, n=64, seed=9):
+        sl, bc, n_sub, cen = local_block(w, i, j, k)
+        T = oracle_faces_local(w, sl, bc, n_sub)
+        xs = x[sl]
+        ax = O.apply_A(T, xs)[cen]
+        # b at the centre: boundary terms of the faces on the GLOBAL boundary
+        bc_c = 0.0
+        if i == 0:
+            bc_c += T[0][cen[0], cen[1], 0] * w.bc[0][1]
+        if i == nx - 1:
+            bc_c += T[0][cen[0], cen[1], -1] * w.bc[1][1]
+        worst = max(worst, abs(bc_c - ax))
+    assert worst <= 1e-10 * np.sqrt(bnorm2), (worst, np.sqrt(bnorm2))
+
+
+@pytest.mark.slow
+def test_fullsize_C4_against_oracle():
+    """C4 at its BASELINE size (128^3, anisotropic, contrast 1e9): the oracle runs whole
+    (~1 min); solution within 1e-8, residual 1e-10, counts reported."""
+    import torch
+    from paper_math_9809043_b200.mss import Solver
+    w = make_workload("C4")
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth)
+    xg, rep = s.solve(torch.from_numpy(w.f.ravel()).cuda(), rel_tol=w.rel_tol)
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth)
+    xo, info = o.solve(w.f, w.rel_tol)
+    print("C4 full: gpu iters", rep.iters, "oracle", info.iters)
+    assert rep.true_rel_res <= 1e-10
+    assert rep.iters[0] == info.iters[0]
+    for a, b in zip(rep.iters[1:], info.iters[1:]):
+        assert abs(a - b) <= max(2, 0.01 * b)
+    err = np.linalg.norm(xg.cpu().numpy() - xo.ravel()) / np.linalg.norm(xo)
+    assert err <= 1e-8
