@@ -23,11 +23,26 @@ __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_ca
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double sel(const double2& v, int par) { return par ? v.y : v.x; }
 
+// Matrix-free faces for a scalar-K level 0: the transmissibility of a face is recomputed
+// from the two cell K values with exactly the expression of k_assemble_faces (harmonic
+// mean P:345-346, T = (A/h) K P:381-383, Dirichlet half-cell 2 (A/h) K, Neumann 0), so it
+// is bit-identical to the stored T while the kernel streams 1 word of K per cell instead
+// of 3 words of faces (HBM traffic traded for fp64 divisions, which the half-sweep has
+// spare: it is bandwidth-bound at ~0.3 flop/B).
+struct KFaces {
+  const double* K;        // scalar K with ghost planes (interior pointer)
+  double cx, cy, cz;      // A_d / h_d
+  int dxl, dxh, dyl, dyh, dzl, dzh;   // Dirichlet flags of the six sides
+};
+__device__ __forceinline__ double hmf(double ka, double kb, double coef) { return coef * (2.0 * ka * kb / (ka + kb)); }
+__device__ __forceinline__ double bndf(int dir, double coef, double k) { return dir ? 2.0 * coef * k : 0.0; }
+
 // Half-sweep of colour `colour` over planes [blockIdx.z * kchunk, +kchunk).
-template <bool FIRST, bool DOT, int MINB>
+// KF: faces recomputed from scalar K (KFaces) instead of loaded from the face arrays.
+template <bool FIRST, bool DOT, int MINB, bool KF = false>
 __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, const double* __restrict__ r,
                                                               double* __restrict__ z, int colour, int kchunk,
-                                                              RedOut ro) {
+                                                              RedOut ro, KFaces kf = KFaces()) {
   const int m = blockIdx.x * kColX + threadIdx.x;
   const int j = blockIdx.y * kColY + threadIdx.y;
   const int k0 = blockIdx.z * kchunk;
@@ -44,18 +59,44 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, c
       zdn = ld2(z + c - plane);            // plane k0-1 (ghost plane when k0 == 0)
       zc = ld2(z + c);
     }
-    double2 tzl = ldg2(L.Tz + c);
+    double2 tzl = make_double2(0.0, 0.0), Kd = make_double2(0.0, 0.0), Kc = make_double2(0.0, 0.0);
+    if (KF) {
+      Kd = ldg2(kf.K + c - plane);
+      Kc = ldg2(kf.K + c);
+    } else {
+      tzl = ldg2(L.Tz + c);
+    }
     for (int k = k0; k < k1; ++k) {
       const int par = (i0 + j + k + L.z0 + colour) & 1;   // updated cell: i0 + par
-      const int64_t row = j + (int64_t)ny * k;
-      const int64_t fx = c + row;
-      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
-      const int64_t fy = c + (int64_t)nx * k;
-      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
-      const double2 tzu = ldg2(L.Tz + c + plane);
+      double txl, txh, t2, t3, t4, t5;
+      double2 tzu = make_double2(0.0, 0.0), Ku = make_double2(0.0, 0.0);
+      if (KF) {
+        const int kg = k + L.z0;
+        Ku = ldg2(kf.K + c + plane);
+        const double kc = sel(Kc, par);
+        if (par) {
+          txl = hmf(Kc.x, Kc.y, kf.cx);
+          txh = hasR ? hmf(Kc.y, __ldg(kf.K + c + 2), kf.cx) : bndf(kf.dxh, kf.cx, Kc.y);
+        } else {
+          txl = hasL ? hmf(__ldg(kf.K + c - 1), Kc.x, kf.cx) : bndf(kf.dxl, kf.cx, Kc.x);
+          txh = hmf(Kc.x, Kc.y, kf.cx);
+        }
+        t2 = hasS ? hmf(sel(ldg2(kf.K + c - nx), par), kc, kf.cy) : bndf(kf.dyl, kf.cy, kc);
+        t3 = hasN ? hmf(kc, sel(ldg2(kf.K + c + nx), par), kf.cy) : bndf(kf.dyh, kf.cy, kc);
+        t4 = (kg > 0) ? hmf(sel(Kd, par), kc, kf.cz) : bndf(kf.dzl, kf.cz, kc);
+        t5 = (kg < L.nzg - 1) ? hmf(kc, sel(Ku, par), kf.cz) : bndf(kf.dzh, kf.cz, kc);
+      } else {
+        const int64_t row = j + (int64_t)ny * k;
+        const int64_t fx = c + row;
+        const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
+        const int64_t fy = c + (int64_t)nx * k;
+        const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
+        tzu = ldg2(L.Tz + c + plane);
+        txl = par ? tx1 : tx0;
+        txh = par ? tx2 : tx1;
+        t2 = sel(tyl, par); t3 = sel(tyu, par); t4 = sel(tzl, par); t5 = sel(tzu, par);
+      }
       const double2 rr = ld2(r + c);
-      const double txl = par ? tx1 : tx0, txh = par ? tx2 : tx1;
-      const double t2 = sel(tyl, par), t3 = sel(tyu, par), t4 = sel(tzl, par), t5 = sel(tzu, par);
       const double rp = sel(rr, par);
       double zup_x = 0.0, zup_y = 0.0;
       double acc_c = rp;
@@ -82,7 +123,12 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, c
         zdn = zc;
         zc = make_double2(zup_x, zup_y);
       }
-      tzl = tzu;
+      if (KF) {
+        Kd = Kc;
+        Kc = Ku;
+      } else {
+        tzl = tzu;
+      }
       c += plane;
     }
   }
@@ -92,11 +138,11 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, c
 // a10 column-walk: p_out = z + beta p_in (p = z when first); q = A p_out; p.q reduced.
 // Neighbour p values are formed on the fly from z and p_in (never from p_out), so the
 // pass has no intra-launch dependency.
-template <int MINB>
+template <int MINB, bool KF = false>
 __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, const double* __restrict__ z,
                                                              const double* __restrict__ pin, double* __restrict__ pout,
                                                              double* __restrict__ q, const Scal* sc, int first,
-                                                             int kchunk, RedOut ro) {
+                                                             int kchunk, RedOut ro, KFaces kf = KFaces()) {
   const int m = blockIdx.x * kColX + threadIdx.x;
   const int j = blockIdx.y * kColY + threadIdx.y;
   const int k0 = blockIdx.z * kchunk;
@@ -118,14 +164,47 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
     auto P1 = [&](int64_t idx) { return first ? z[idx] : z[idx] + beta * pin[idx]; };
     double2 pdn = P2(c - plane);
     double2 pc = P2(c);
-    double2 tzl = ldg2(L.Tz + c);
+    double2 tzl = make_double2(0.0, 0.0), Kd = make_double2(0.0, 0.0), Kc = make_double2(0.0, 0.0);
+    if (KF) {
+      Kd = ldg2(kf.K + c - plane);
+      Kc = ldg2(kf.K + c);
+      const int kg = k0 + L.z0;
+      tzl = (kg > 0) ? make_double2(hmf(Kd.x, Kc.x, kf.cz), hmf(Kd.y, Kc.y, kf.cz))
+                     : make_double2(bndf(kf.dzl, kf.cz, Kc.x), bndf(kf.dzl, kf.cz, Kc.y));
+    } else {
+      tzl = ldg2(L.Tz + c);
+    }
     for (int k = k0; k < k1; ++k) {
-      const int64_t row = j + (int64_t)ny * k;
-      const int64_t fx = c + row;
-      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
-      const int64_t fy = c + (int64_t)nx * k;
-      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
-      const double2 tzu = ldg2(L.Tz + c + plane);
+      double tx0, tx1, tx2;
+      double2 tyl, tyu, tzu, Ku = make_double2(0.0, 0.0);
+      if (KF) {
+        const int kg = k + L.z0;
+        Ku = ldg2(kf.K + c + plane);
+        tx0 = hasL ? hmf(__ldg(kf.K + c - 1), Kc.x, kf.cx) : bndf(kf.dxl, kf.cx, Kc.x);
+        tx1 = hmf(Kc.x, Kc.y, kf.cx);
+        tx2 = hasR ? hmf(Kc.y, __ldg(kf.K + c + 2), kf.cx) : bndf(kf.dxh, kf.cx, Kc.y);
+        if (hasS) {
+          const double2 Ks = ldg2(kf.K + c - nx);
+          tyl = make_double2(hmf(Ks.x, Kc.x, kf.cy), hmf(Ks.y, Kc.y, kf.cy));
+        } else {
+          tyl = make_double2(bndf(kf.dyl, kf.cy, Kc.x), bndf(kf.dyl, kf.cy, Kc.y));
+        }
+        if (hasN) {
+          const double2 Kn = ldg2(kf.K + c + nx);
+          tyu = make_double2(hmf(Kc.x, Kn.x, kf.cy), hmf(Kc.y, Kn.y, kf.cy));
+        } else {
+          tyu = make_double2(bndf(kf.dyh, kf.cy, Kc.x), bndf(kf.dyh, kf.cy, Kc.y));
+        }
+        tzu = (kg < L.nzg - 1) ? make_double2(hmf(Kc.x, Ku.x, kf.cz), hmf(Kc.y, Ku.y, kf.cz))
+                               : make_double2(bndf(kf.dzh, kf.cz, Kc.x), bndf(kf.dzh, kf.cz, Kc.y));
+      } else {
+        const int64_t row = j + (int64_t)ny * k;
+        const int64_t fx = c + row;
+        tx0 = __ldg(L.Tx + fx); tx1 = __ldg(L.Tx + fx + 1); tx2 = __ldg(L.Tx + fx + 2);
+        const int64_t fy = c + (int64_t)nx * k;
+        tyl = ldg2(L.Ty + fy); tyu = ldg2(L.Ty + fy + nx);
+        tzu = ldg2(L.Tz + c + plane);
+      }
       const double2 pup = P2(c + plane);
       const double2 ps = hasS ? P2(c - nx) : make_double2(0.0, 0.0);
       const double2 pn = hasN ? P2(c + nx) : make_double2(0.0, 0.0);
@@ -143,6 +222,10 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
       pdn = pc;
       pc = pup;
       tzl = tzu;
+      if (KF) {
+        Kd = Kc;
+        Kc = Ku;
+      }
       c += plane;
     }
   }
@@ -154,11 +237,11 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
 // (the red residual is zero after the closing red sweep); the x-weighted
 // contributions meet in shared memory and thread I sums the pairs of coarse cell I in
 // a fixed order (deterministic).  t1 has dims (ncx, ny, nz).
-template <int MINB>
+template <int MINB, bool KF = false>
 __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, const double* __restrict__ r,
                                                                   const double* __restrict__ z,
                                                                   double* __restrict__ t1, int ncx, int s, int kind,
-                                                                  int kchunk) {
+                                                                  int kchunk, KFaces kf = KFaces()) {
   extern __shared__ double shc[];             // [2 * hx] contributions
   int* shi = reinterpret_cast<int*>(shc + 2 * blockDim.x);   // [2 * hx] coarse indices (per parity: 4 * hx)
   const int nx = L.nx, ny = L.ny;
@@ -182,25 +265,50 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
   const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
   int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
   double2 zdn = make_double2(0, 0), zc = make_double2(0, 0), tzl = make_double2(0, 0);
+  double2 Kd = make_double2(0, 0), Kc = make_double2(0, 0);
   if (act && k0 < k1) {
     zdn = ld2(z + c - plane);
     zc = ld2(z + c);
-    tzl = ldg2(L.Tz + c);
+    if (KF) {
+      Kd = ldg2(kf.K + c - plane);
+      Kc = ldg2(kf.K + c);
+    } else {
+      tzl = ldg2(L.Tz + c);
+    }
   }
   for (int k = k0; k < k1; ++k) {
     const int par = (i0 + j + k + L.z0 + 1) & 1;   // black cell of the pair: i0 + par
-    double2 zup = make_double2(0, 0), tzu = make_double2(0, 0);
+    double2 zup = make_double2(0, 0), tzu = make_double2(0, 0), Ku = make_double2(0, 0);
     if (act) {
-      const int64_t row = j + (int64_t)ny * k;
-      const int64_t fx = c + row;
-      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
-      const int64_t fy = c + (int64_t)nx * k;
-      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
-      tzu = ldg2(L.Tz + c + plane);
+      double txl, txh, t2, t3, t4, t5;
+      if (KF) {
+        const int kg = k + L.z0;
+        Ku = ldg2(kf.K + c + plane);
+        const double kc = sel(Kc, par);
+        if (par) {
+          txl = hmf(Kc.x, Kc.y, kf.cx);
+          txh = hasR ? hmf(Kc.y, __ldg(kf.K + c + 2), kf.cx) : bndf(kf.dxh, kf.cx, Kc.y);
+        } else {
+          txl = hasL ? hmf(__ldg(kf.K + c - 1), Kc.x, kf.cx) : bndf(kf.dxl, kf.cx, Kc.x);
+          txh = hmf(Kc.x, Kc.y, kf.cx);
+        }
+        t2 = hasS ? hmf(sel(ldg2(kf.K + c - nx), par), kc, kf.cy) : bndf(kf.dyl, kf.cy, kc);
+        t3 = hasN ? hmf(kc, sel(ldg2(kf.K + c + nx), par), kf.cy) : bndf(kf.dyh, kf.cy, kc);
+        t4 = (kg > 0) ? hmf(sel(Kd, par), kc, kf.cz) : bndf(kf.dzl, kf.cz, kc);
+        t5 = (kg < L.nzg - 1) ? hmf(kc, sel(Ku, par), kf.cz) : bndf(kf.dzh, kf.cz, kc);
+      } else {
+        const int64_t row = j + (int64_t)ny * k;
+        const int64_t fx = c + row;
+        const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
+        const int64_t fy = c + (int64_t)nx * k;
+        const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
+        tzu = ldg2(L.Tz + c + plane);
+        txl = par ? tx1 : tx0;
+        txh = par ? tx2 : tx1;
+        t2 = sel(tyl, par); t3 = sel(tyu, par); t4 = sel(tzl, par); t5 = sel(tzu, par);
+      }
       const double2 rr = ld2(r + c);
       zup = ld2(z + c + plane);
-      const double txl = par ? tx1 : tx0, txh = par ? tx2 : tx1;
-      const double t2 = sel(tyl, par), t3 = sel(tyu, par), t4 = sel(tzl, par), t5 = sel(tzu, par);
       double xl, xh;
       if (par) {
         xl = zc.x;
@@ -233,6 +341,10 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
     zdn = zc;
     zc = zup;
     tzl = tzu;
+    if (KF) {
+      Kd = Kc;
+      Kc = Ku;
+    }
     c += plane;
   }
 }

@@ -134,6 +134,11 @@ struct mss_ctx {
   std::vector<char> tsm_h;
   bool tsm_dirty = true;
   long long* tsm_phase = nullptr;
+  // matrix-free level-0 faces from scalar K (colwalk.cuh KFaces)
+  bool kfaces = false;
+  double* kf_K = nullptr;                  // ghosted copy of K on level 0
+  double kf_c[3] = {0, 0, 0};
+  int kf_dir[6] = {0, 0, 0, 0, 0, 0};
   // distributed z-slabs (rank/nranks == 0/1 single GPU): levels [0, ndist) are split
   // across ranks, the rest are replicated on every rank
   int rank = 0, nranks = 1;

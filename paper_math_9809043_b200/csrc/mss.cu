@@ -188,6 +188,18 @@ static void slab_of(int64_t nzg0, int64_t unit, int P, int r, int64_t* z0, int64
   *z1 = unit * (units * (r + 1) / P);
 }
 
+static KFaces kfaces_of(const mss_ctx* ctx) {
+  KFaces f;
+  f.K = ctx->kf_K;
+  f.cx = ctx->kf_c[0];
+  f.cy = ctx->kf_c[1];
+  f.cz = ctx->kf_c[2];
+  f.dxl = ctx->kf_dir[0]; f.dxh = ctx->kf_dir[1];
+  f.dyl = ctx->kf_dir[2]; f.dyh = ctx->kf_dir[3];
+  f.dzl = ctx->kf_dir[4]; f.dzh = ctx->kf_dir[5];
+  return f;
+}
+
 #define DISPATCH(ndim, kern, grid, ...)                               \
   do {                                                                \
     if ((ndim) == 3) LAUNCH(kern<3>, grid, __VA_ARGS__);              \
@@ -248,8 +260,9 @@ struct ProfScope {
 
 // Algorithmic bytes per cell (fp64 words x 8) of each kernel with the interleaved
 // layout (SURVEY §8(d) "interleaved" column): T = ndim words per cell.
-static double cell_bytes(const mss_ctx* ctx, int cls) {
-  const double T = ctx->ndim;
+static double cell_bytes(const mss_ctx* ctx, int cls, int k = -1) {
+  // faces: ndim words per cell, or 1 word of K when level 0 recomputes them (kfaces)
+  const double T = (k == 0 && ctx->kfaces) ? 1.0 : (double)ctx->ndim;
   switch (cls) {
     case KC_SWEEP: return 8.0 * (T + 3);    // T + r + z(nbr lines) + z write (r.z fused: same lines)
     case KC_SWEEP0: return 8.0 * (T + 2);   // T + r + z write
@@ -287,29 +300,31 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   const int64_t work = (int64_t)((l.nx + 1) / 2) * l.ny * l.nz;
   const int g = grid_for(work);
   const int cls = first ? KC_SWEEP0 : KC_SWEEP;
-  ProfScope ps(ctx, cls, k, cell_bytes(ctx, cls) * l.N);
+  ProfScope ps(ctx, cls, k, cell_bytes(ctx, cls, k) * l.N);
   RedOut ro = red_to(ctx, dot_out, k, 0);
   const LevelDev d = l.dev();
   if (col_ok(ctx, l)) {
     static int minb = -1;
     if (minb < 0) minb = getenv("MSS_COL_MINB") ? atoi(getenv("MSS_COL_MINB")) : 4;  // 64 regs: measured best
-#define SWEEPCOL(MB)                                                                                        \
+#define SWEEPCOL(MB, KFB)                                                                                   \
     {                                                                                                       \
-      const void* kern = first ? (const void*)k_sweep_col<true, false, MB>                                 \
-                               : (dot_out ? (const void*)k_sweep_col<false, true, MB>                       \
-                                          : (const void*)k_sweep_col<false, false, MB>);                    \
+      const void* kern = first ? (const void*)k_sweep_col<true, false, MB, KFB>                            \
+                               : (dot_out ? (const void*)k_sweep_col<false, true, MB, KFB>                  \
+                                          : (const void*)k_sweep_col<false, false, MB, KFB>);               \
       dim3 grid;                                                                                            \
       int kch = 0;                                                                                          \
       if (col_grid(kern, l, &grid, &kch)) {                                                                 \
         const dim3 blk(kColX, kColY);                                                                       \
-        if (first) k_sweep_col<true, false, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);   \
-        else if (dot_out) k_sweep_col<false, true, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro); \
-        else k_sweep_col<false, false, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro);       \
+        const KFaces kfs = kfaces_of(ctx);                                                                  \
+        if (first) k_sweep_col<true, false, MB, KFB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro, kfs); \
+        else if (dot_out) k_sweep_col<false, true, MB, KFB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro, kfs); \
+        else k_sweep_col<false, false, MB, KFB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro, kfs); \
         ctx->launches++;                                                                                    \
         return MSS_OK;                                                                                      \
       }                                                                                                     \
     }
-    if (minb <= 3) SWEEPCOL(3) else if (minb == 4) SWEEPCOL(4) else SWEEPCOL(5)
+    if (k == 0 && ctx->kfaces) SWEEPCOL(4, true)
+    else if (minb <= 3) SWEEPCOL(3, false) else if (minb == 4) SWEEPCOL(4, false) else SWEEPCOL(5, false)
 #undef SWEEPCOL
   }
 #define HS(ND, F, D) LAUNCH((k_halfsweep<ND, F, D>), g, d, r, z, colour, ro)
@@ -440,7 +455,7 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   {
-    const double by = 8.0 * (ctx->ndim + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
+    const double by = 8.0 * ((k == 0 && ctx->kfaces ? 1 : ctx->ndim) + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
     ProfScope ps(ctx, KC_RESID, k, by);
     const int hx = f.nx / 2;
     if (black_only && col_ok(ctx, f) && hx >= 32 && hx <= 512) {
@@ -450,8 +465,12 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
       const int kch = (f.nz + nch - 1) / nch;
       nch = (f.nz + kch - 1) / kch;
       const size_t shm = (size_t)bt * 2 * (sizeof(double) + sizeof(int));
-      k_resid_restrict_col<2><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(f.dev(), r, z, f.t1, c.nx, ctx->prm.scale,
-                                                                          ctx->prm.interp, kch);
+      if (k == 0 && ctx->kfaces)
+        k_resid_restrict_col<2, true><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(
+            f.dev(), r, z, f.t1, c.nx, ctx->prm.scale, ctx->prm.interp, kch, kfaces_of(ctx));
+      else
+        k_resid_restrict_col<2><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(f.dev(), r, z, f.t1, c.nx, ctx->prm.scale,
+                                                                            ctx->prm.interp, kch);
       ctx->launches++;
     } else
     DISPATCH(ctx->ndim, k_resid_restrict_x, grid_for((int64_t)c.nx * f.ny * f.nz), f.dev(), r, z, f.t1, c.nx,
@@ -555,10 +574,15 @@ static int pcg_level(mss_ctx* ctx, int k) {
     double* pin = l.p[l.pcur];
     double* pout = l.p[l.pcur ^ 1];
     {
-    ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV) * l.N);
+    ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV, k) * l.N);
     dim3 cgrid;
     int kch = 0;
-    if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
+    if (k == 0 && ctx->kfaces && col_grid((const void*)k_spmv_col<4, true>, l, &cgrid, &kch)) {
+      k_spmv_col<4, true><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds,
+                                                                       it == 0 ? 1 : 0, kch,
+                                                                       red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
+      ctx->launches++;
+    } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
       k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
                                                                  kch, red_to(ctx, &ds->pq, k, 0));
       ctx->launches++;
@@ -894,6 +918,21 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaStreamSynchronize(ctx->stream));
       cudaFree(Kext);
     }
+  }
+  // matrix-free level-0 faces (scalar K, 3-D, even n_x): keep a ghosted copy of K
+  ctx->kfaces = false;
+  if (ndim == 3 && k_comp == 1 && (l0.nx % 2) == 0 && !getenv("MSS_NO_KFACES")) {
+    TRY(valloc(ctx, l0, &ctx->kf_K));
+    CK(cudaMemcpyAsync(ctx->kf_K, K, sizeof(double) * l0.N, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (l0.dist) TRY(ctx->comm->halo(ctx->stream, ctx->kf_K, l0.plane, l0.nz, 1));
+    for (int d = 0; d < 3; ++d) {
+      double area = 1.0;
+      for (int e = 0; e < 3; ++e)
+        if (e != d) area *= l0.h[e];
+      ctx->kf_c[d] = area / l0.h[d];
+    }
+    for (int sd = 0; sd < 6; ++sd) ctx->kf_dir[sd] = ctx->bc[sd].kind == 1;
+    ctx->kfaces = true;
   }
   // a2: coarse faces, level by level
   for (int k = 1; k <= ctx->L; ++k) {
