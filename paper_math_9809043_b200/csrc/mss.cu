@@ -323,7 +323,8 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
         return MSS_OK;                                                                                      \
       }                                                                                                     \
     }
-    if (k == 0 && ctx->kfaces) SWEEPCOL(4, true)
+    if (k == 0 && ctx->kfaces && minb <= 2) SWEEPCOL(2, true)
+    else if (k == 0 && ctx->kfaces) SWEEPCOL(4, true)
     else if (minb <= 3) SWEEPCOL(3, false) else if (minb == 4) SWEEPCOL(4, false) else SWEEPCOL(5, false)
 #undef SWEEPCOL
   }
@@ -921,7 +922,9 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   }
   // matrix-free level-0 faces (scalar K, 3-D, even n_x): keep a ghosted copy of K
   ctx->kfaces = false;
-  if (ndim == 3 && k_comp == 1 && (l0.nx % 2) == 0 && !getenv("MSS_NO_KFACES")) {
+  // opt-in (MSS_KFACES=1): measured slower on B200 (the 6 IEEE divisions per updated cell
+  // make the sweep latency-bound, 1.44 ms vs 0.99 ms per 512^3 half-sweep)
+  if (ndim == 3 && k_comp == 1 && (l0.nx % 2) == 0 && getenv("MSS_KFACES")) {
     TRY(valloc(ctx, l0, &ctx->kf_K));
     CK(cudaMemcpyAsync(ctx->kf_K, K, sizeof(double) * l0.N, cudaMemcpyDeviceToDevice, ctx->stream));
     if (l0.dist) TRY(ctx->comm->halo(ctx->stream, ctx->kf_K, l0.plane, l0.nz, 1));
