@@ -27,6 +27,10 @@ Parity status per function (DESIGN.md §5 lists the pins):
   precond (Eq. 2.10) ................................... pinned (P6)
   pcg / solve .......................................... pinned (P2, P7, P9)
   general_dims_chain (non-integer scale, NEXT-2) ....... pinned (P8, Table 1)
+  comparison methods (NEXT-1): Tatebe MG preconditioner
+    (Eq. 2.9), polynomial preconditioner (§2.1), standard
+    multigrid iteration ................................ pinned (P10, dense Eq. 2.9 /
+                                                          series matrices, dense solve)
 """
 from __future__ import annotations
 
@@ -420,9 +424,14 @@ class MultiScaleOracle:
     m = s, per-level tolerance factor f = 0.1, linear or
     piecewise-constant extension."""
 
+    METHODS = ("multiscale", "tatebe", "polynomial", "multigrid")
+
     def __init__(self, ndim, n, K, bc, depth=None, s=4, m=None, f=0.1,
                  interp="linear", max_iter=500, coarse_min=512, use_lift=True,
-                 log_events=False):
+                 log_events=False, method="multiscale"):
+        if method not in self.METHODS:
+            raise OracleError(f"unknown method {method}")
+        self.method = method
         self.ndim = ndim
         self.n0 = tuple(n)
         self.bc = list(bc)
@@ -517,6 +526,59 @@ class MultiScaleOracle:
         self.smooth(k, r, z, 2 * self.m + 1)
         return z
 
+    # ------------------------------------------------------------------ NEXT-1 comparison methods
+    def precond_tatebe(self, k, r):
+        """Tatebe's multigrid preconditioner, Eq. 2.9:
+        M_k^{-1} = H^m (E M_{k+1}^{-1} R) H^{mT} + sum_{j<2m} H^j P^{-1}, M_L^{-1} = A_L^{-1},
+        evaluated as z = 0; m SGS steps; z += E M_{k+1}^{-1} R (r - A z); m SGS steps -- one
+        V-cycle per application, no inner CG on the coarse levels."""
+        lv = self.levels[k]
+        if k > 0:                      # level-0 applications are counted by the outer loop
+            self.iters[k] += 1
+            self.calls[k] += 1
+        if k == self.L:
+            return self.coarse_solve(r)
+        z = np.zeros(lv.shape)
+        self.smooth(k, r, z, 2 * self.m + 1)
+        bc = restrict(r - self.A(k, z), self.E[k])
+        y = self.precond_tatebe(k + 1, bc)
+        z = z + prolong(y, self.E[k])
+        self.smooth(k, r, z, 2 * self.m + 1)
+        return z
+
+    def precond_poly(self, k, r):
+        """Polynomial preconditioner (§2.1): W = P^{-1} in Eq. 2.6, i.e. the
+        first 2m+1 terms of the series Eq. 2.4 = 2m+1 SGS steps from zero = 4m+3
+        alternating half-sweeps."""
+        z = np.zeros(self.levels[k].shape)
+        self.smooth(k, r, z, 2 * (2 * self.m + 1) + 1)
+        return z
+
+    def apply_M(self, k, r):
+        if self.method in ("tatebe", "multigrid"):
+            return self.precond_tatebe(k, r)
+        if self.method == "polynomial":
+            return self.precond_poly(k, r)
+        return self.precond(k, r)
+
+    def stationary_mg(self, b, x0):
+        """Standard multigrid: x <- x + M_0^{-1}(b - A x) with Tatebe's
+        M_0^{-1}, stopped by the level-0 criterion of P:448-456 or max_iter."""
+        lv = self.levels[0]
+        thr = lv.N * self.eps2
+        x = x0.copy()
+        r = b - self.A(0, x)
+        it = 0
+        self.calls[0] += 1
+        while float(np.dot(r.ravel(), r.ravel())) >= thr:
+            if it >= self.max_iter:
+                self.not_converged = True
+                break
+            x = x + self.precond_tatebe(0, r)
+            r = b - self.A(0, x)
+            it += 1
+        return x, it
+
     # ------------------------------------------------------------------ O14
     def pcg(self, k, b, x0=None):
         """O14: conventional PCG (Templates Fig. 2.5), stopping on the
@@ -543,7 +605,7 @@ class MultiScaleOracle:
         p = None
         rho_prev = None
         while True:
-            z = self.precond(k, r)
+            z = self.apply_M(k, r) if k == 0 else self.precond(k, r)
             rho = float(np.dot(r.ravel(), z.ravel()))
             if not rho > 0:
                 raise Breakdown(f"rho={rho} at level {k} iteration {it}")
@@ -605,6 +667,9 @@ class MultiScaleOracle:
             else:
                 self.iters[0] += 1
                 x = x0 + self.coarse_solve(r0)
+        elif self.method == "multigrid":
+            x, it = self.stationary_mg(b, x0)
+            self.iters[0] = it
         else:
             x, _ = self.pcg(0, b, x0)
         res = b - self.A(0, x)

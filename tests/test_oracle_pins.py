@@ -512,3 +512,85 @@ def test_errors():
         O.MultiScaleOracle(2, (8, 8, 1), np.ones((1, 8, 8)), bc_table(2, {}))        # all Neumann
     with pytest.raises(O.OracleError):
         O.MultiScaleOracle(2, (8, 8, 1), -np.ones((1, 8, 8)), BC_MIXED2)
+
+
+# ---------------------------------------------------------------- P10 comparison methods (NEXT-1)
+def _dense_level_ops(o, k):
+    lv = o.levels[k]
+    A = dense_from_oracle(lv.T, lv.shape)
+    P, Q = sgs_split(A, rb_perm(lv.shape))
+    return A, P, Q
+
+
+def test_P10_tatebe_equals_dense_eq_2_9_three_levels():
+    """Eq. 2.9 built densely and recursively (M_L^{-1} = A_L^{-1}) equals the oracle's
+    V-cycle evaluation on a 3-level hierarchy."""
+    w = small_problem(2, (16, 16, 1), seed=12, bc=BC_MIXED2)
+    m = 2
+    o = O.MultiScaleOracle(2, w.n, w.K, w.bc, depth=2, m=m, method="tatebe")
+    o.iters = [0] * 3
+    o.calls = [0] * 3
+    Minv = None
+    for k in (2, 1, 0):
+        A, P, Q = _dense_level_ops(o, k)
+        if k == 2:
+            Minv = np.linalg.inv(A)
+            continue
+        E = O.interp_1d(o.levels[k].n[0], 4)
+        E = np.kron(O.interp_1d(o.levels[k].n[1], 4), E)
+        Pi = np.linalg.inv(P)
+        H = Pi @ Q
+        Hm = np.linalg.matrix_power(H, m)
+        Minv = Hm @ (E @ Minv @ E.T) @ np.linalg.matrix_power(Q @ Pi, m) + \
+            sum(np.linalg.matrix_power(H, j) @ Pi for j in range(2 * m))
+    N = o.levels[0].N
+    I = np.eye(N)
+    cols = np.array([o.precond_tatebe(0, I[c].reshape(o.levels[0].shape)).ravel() for c in range(N)]).T
+    assert np.allclose(cols, Minv, atol=1e-11 * np.abs(Minv).max())
+    assert np.allclose(cols, cols.T, atol=1e-11 * np.abs(cols).max())
+
+
+def test_P10_polynomial_equals_series():
+    """W = P^{-1}: M^{-1} = sum_{j<=2m} (P^{-1} Q)^j P^{-1}, the first 2m+1 terms of Eq. 2.4."""
+    w = small_problem(2, (6, 6, 1), seed=13, bc=BC_MIXED2)
+    for m in (1, 2):
+        o = O.MultiScaleOracle(2, w.n, w.K, w.bc, depth=0, m=m, method="polynomial")
+        A, P, Q = _dense_level_ops(o, 0)
+        Pi = np.linalg.inv(P)
+        H = Pi @ Q
+        S = sum(np.linalg.matrix_power(H, j) @ Pi for j in range(2 * m + 1))
+        N = o.levels[0].N
+        I = np.eye(N)
+        cols = np.array([o.precond_poly(0, I[c].reshape(o.levels[0].shape)).ravel() for c in range(N)]).T
+        assert np.allclose(cols, S, atol=1e-12 * np.abs(S).max())
+
+
+@pytest.mark.parametrize("method", ["tatebe", "polynomial", "multigrid"])
+def test_P10_comparison_methods_solve(method):
+    w = small_problem(2, (16, 16, 1), seed=14, bc=BC_MIXED2, contrast=1e2)
+    o = O.MultiScaleOracle(2, w.n, w.K, w.bc, depth=1, method=method, max_iter=2000)
+    x, info = o.solve(w.f, rel_tol=1e-10)
+    A = brute_force_dense(2, w.n, w.K, w.bc)
+    b = O.rhs(2, w.n, o.levels[0].T, w.f, w.bc)
+    xd = np.linalg.solve(A, b.ravel())
+    assert not info.not_converged
+    assert info.true_rel_res <= 1e-10
+    assert np.linalg.norm(x.ravel() - xd) <= 1e-8 * np.linalg.norm(xd)
+
+
+def test_P10_method_ordering_on_C1():
+    """With an exact coarsest solve two-level Tatebe == multiscale; on C1's 3 levels the
+    recursive multiscale PCG needs no more fine iterations than Tatebe, and the
+    polynomial preconditioner needs the most."""
+    w = make_workload("C1")
+    its = {}
+    for meth in ["multiscale", "tatebe", "polynomial", "multigrid"]:
+        o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth, method=meth, max_iter=500)
+        x, info = o.solve(w.f, w.rel_tol)
+        assert info.true_rel_res <= 1e-10
+        its[meth] = info.iters
+    assert its["multiscale"][0] <= its["tatebe"][0] <= its["polynomial"][0]
+    w2 = make_workload("C2", n=32)
+    a = O.MultiScaleOracle(w2.ndim, w2.n, w2.K, w2.bc, method="tatebe").solve(w2.f, 1e-10)[1].iters
+    b = O.MultiScaleOracle(w2.ndim, w2.n, w2.K, w2.bc, method="multiscale").solve(w2.f, 1e-10)[1].iters
+    assert a[0] == b[0]
