@@ -59,6 +59,11 @@ typedef struct {
   int64_t tail_cells;   /* levels with N_k <= tail_cells run inside one persistent cluster
                            kernel per call (device-resident control); default 65536; 0 = off  */
   int64_t gather_below; /* distributed: levels with N_k < gather_below are replicated; 64^3     */
+  int     method;       /* 0 = recursive multi-scale PCG, Eq. 2.10 (default);
+                           1 = Tatebe multigrid-preconditioned CG, Eq. 2.9;
+                           2 = polynomial-preconditioned CG, W = P^{-1};
+                           3 = standard multigrid iteration with M_0^{-1}.
+                           1-3 are the paper's comparison methods.           */
 } mss_params;
 
 /* Per-solve report (the schema of the paper's Tables 1-2). */

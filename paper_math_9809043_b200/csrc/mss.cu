@@ -560,6 +560,43 @@ static int precond(mss_ctx* ctx, int k) {
   return MSS_OK;
 }
 
+// ---- the paper's comparison methods, same kernels
+// Tatebe's multigrid preconditioner, Eq. 2.9: z_k = M_k^{-1} r_k with ONE
+// recursive application of M_{k+1}^{-1} (no inner CG), exact on the coarsest level.
+static int precond_tatebe(mss_ctx* ctx, int k) {
+  Level& l = ctx->lv[k];
+  if (k > 0) {
+    ctx->info.iters[k] += 1;
+    ctx->info.calls[k] += 1;
+  }
+  if (k == ctx->L) return op_coarse_solve(ctx, l.r, l.z);
+  Level& c = ctx->lv[k + 1];
+  const int nh = 2 * ctx->prm.m + 1;
+  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));
+  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, 1));
+  TRY(precond_tatebe(ctx, k + 1));
+  TRY(op_prolong_add(ctx, k, c.z, l.z, 1));
+  return op_smooth(ctx, k, l.r, l.z, nh, 0, false, k == 0 ? &ctx->dscal[0].rho : nullptr);
+}
+
+// Polynomial preconditioner: the first 2m+1 terms of Eq. 2.4 = 2m+1 SGS steps
+// from zero = 4m+3 alternating half-sweeps (rho = r.z fused into the last).
+static int precond_poly(mss_ctx* ctx, int k) {
+  Level& l = ctx->lv[k];
+  return op_smooth(ctx, k, l.r, l.z, 2 * (2 * ctx->prm.m + 1) + 1, 0, true, &ctx->dscal[k].rho);
+}
+
+static int precond(mss_ctx* ctx, int k);
+// the level-0 preconditioner of the selected method (z_0 and rho = r.z on exit)
+static int apply_precond0(mss_ctx* ctx) {
+  switch (ctx->prm.method) {
+    case 1:
+    case 3: return precond_tatebe(ctx, 0);
+    case 2: return precond_poly(ctx, 0);
+    default: return precond(ctx, 0);
+  }
+}
+
 // PCG on level k; on entry r_k holds the residual of the current x_k (x_k = 0 and
 // r_k = b_k for k > 0).  Level thresholds are precomputed in l.thr.
 static int pcg_level(mss_ctx* ctx, int k) {
@@ -571,7 +608,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
   if (ctx->hscal[k].rr < l.thr) return MSS_OK;
   int64_t it = 0;
   for (;;) {
-    TRY(precond(ctx, k));                                                  // z = M r, rho = r.z
+    TRY(k == 0 ? apply_precond0(ctx) : precond(ctx, k));                 // z = M r, rho = r.z
     double* pin = l.p[l.pcur];
     double* pout = l.p[l.pcur ^ 1];
     {
@@ -691,6 +728,24 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
         LAUNCH(k_axpy, grid_for(l.N), l.N, l.x, l.z);
         ctx->info.iters[0] += 1;
       }
+    } else if (ctx->prm.method == 3) {
+      // standard multigrid: x <- x + M_0^{-1} (b - A x)
+      ctx->info.calls[0] += 1;
+      int64_t it = 0;
+      for (;;) {
+        TRY(read_scal(ctx, 0));
+        if (ctx->hscal[0].rr < l.thr) break;
+        if (it >= ctx->prm.max_iter) {
+          ctx->info.not_converged = 1;
+          break;
+        }
+        TRY(precond_tatebe(ctx, 0));
+        LAUNCH(k_axpy, grid_for(l.N), l.N, l.x, l.z);
+        TRY(do_halo(ctx, 0, l.x));
+        TRY(op_residual(ctx, 0, l.b, l.x, l.r, &ds->rr));
+        it++;
+      }
+      ctx->info.iters[0] += it;
     } else {
       rc = pcg_level(ctx, 0);
       if (rc < 0 && rc != MSS_EBREAKDOWN) return rc;
@@ -1036,6 +1091,7 @@ int mss_default_params(mss_params* p) {
   p->use_lift = 1;
   p->tail_cells = 65536;
   p->gather_below = (int64_t)64 * 64 * 64;
+  p->method = 0;
   return MSS_OK;
 }
 
@@ -1076,6 +1132,7 @@ static int setup_common(mss_ctx** out, mss::Comm* comm, int ndim, const int64_t 
   if (prm.scale < 2) return set_err(MSS_EINVAL, "scale < 2");
   if (prm.m < 0 || prm.max_iter < 1 || !(prm.f > 0) || prm.coarse_min < 1) return set_err(MSS_EINVAL, "bad params");
   if (prm.interp != 0 && prm.interp != 1) return set_err(MSS_EINVAL, "interp must be 0 or 1");
+  if (prm.method < 0 || prm.method > 3) return set_err(MSS_EINVAL, "method must be 0..3");
   bool any_dir = false;
   for (int s = 0; s < 2 * ndim; ++s) {
     if (bc[s].kind != 0 && bc[s].kind != 1) return set_err(MSS_EINVAL, "bad BC kind");

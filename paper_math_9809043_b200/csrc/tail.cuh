@@ -297,7 +297,8 @@ static int tail_setup(mss_ctx* ctx) {
 }
 
 static bool tail_supported(mss_ctx* ctx, int k) {
-  return ctx->tail_cs > 0 && k >= 1 && k >= ctx->ndist && k < ctx->L && ctx->lv[k].N <= ctx->prm.tail_cells;
+  return ctx->prm.method == 0 && ctx->tail_cs > 0 && k >= 1 && k >= ctx->ndist && k < ctx->L &&
+         ctx->lv[k].N <= ctx->prm.tail_cells;
 }
 
 static void tail_mark_dirty(mss_ctx* ctx) {

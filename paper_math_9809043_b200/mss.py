@@ -45,7 +45,10 @@ class Params(ctypes.Structure):
         ("use_lift", ctypes.c_int),
         ("tail_cells", ctypes.c_int64),
         ("gather_below", ctypes.c_int64),
+        ("method", ctypes.c_int),
     ]
+
+METHODS = {"multiscale": 0, "tatebe": 1, "polynomial": 2, "multigrid": 3}
 
 
 class Info(ctypes.Structure):

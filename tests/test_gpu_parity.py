@@ -289,3 +289,33 @@ def test_smem_tail_matches_l2_tail(torch_mod, name, monkeypatch):
     assert ra.tail_kind == 1 and rb.tail_kind == 2, (ra.tail_kind, rb.tail_kind)
     assert ra.iters == rb.iters
     assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-12
+
+
+METHOD_CASES = [
+    ("C1", lambda: make_workload("C1")),
+    ("C2_32", lambda: make_workload("C2", n=32)),
+    ("C5_64", lambda: make_workload("C5", n=64)),
+    ("2d_ragged", CASES[0][1]),
+]
+
+
+@pytest.mark.parametrize("method", ["tatebe", "polynomial", "multigrid"])
+@pytest.mark.parametrize("name,mk", METHOD_CASES, ids=[c[0] for c in METHOD_CASES])
+def test_comparison_methods(torch_mod, name, mk, method):
+    """The paper's comparison methods on the GPU against the oracle:
+    Tatebe MG-PCG (Eq. 2.9), polynomial PCG (§2.1), standard multigrid."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver, METHODS
+    w = mk()
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth,
+               params={"method": METHODS[method], "max_iter": 400})
+    xg, rep = s.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth, method=method, max_iter=400)
+    xo, info = o.solve(w.f, w.rel_tol)
+    print(f"{name} {method}: gpu {rep.iters} oracle {info.iters} nc {rep.not_converged}/{info.not_converged}")
+    assert rep.not_converged == info.not_converged
+    if info.not_converged:
+        return
+    assert rep.true_rel_res <= 1e-10
+    assert rep.iters == info.iters
+    assert rel(xg.cpu().numpy(), xo) <= 1e-8
