@@ -571,6 +571,8 @@ class MultiScaleOracle:
         it = 0
         self.calls[0] += 1
         while float(np.dot(r.ravel(), r.ravel())) >= thr:
+            if not np.isfinite(float(np.dot(r.ravel(), r.ravel()))):
+                raise Breakdown("standard multigrid iteration diverged")
             if it >= self.max_iter:
                 self.not_converged = True
                 break

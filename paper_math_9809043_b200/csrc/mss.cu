@@ -641,10 +641,11 @@ static int pcg_level(mss_ctx* ctx, int k) {
     TRY(read_scal(ctx, k));                                                // a12
     const Scal& h = ctx->hscal[k];
     it++;
-    if (!(h.rho > 0.0) || !(h.pq > 0.0)) {
+    if (!(h.rho > 0.0) || !(h.pq > 0.0) || !std::isfinite(h.rr)) {
       ctx->info.iters[k] += it;
       ctx->info.breakdown_level = k;
-      return set_err(MSS_EBREAKDOWN, "PCG breakdown (rho or pAp <= 0) at level " + std::to_string(k));
+      return set_err(MSS_EBREAKDOWN, "PCG breakdown (rho or pAp <= 0, or non-finite residual) at level " +
+                                         std::to_string(k));
     }
     if (h.rr < l.thr) break;
     if (it >= ctx->prm.max_iter) {
@@ -735,6 +736,13 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
       for (;;) {
         TRY(read_scal(ctx, 0));
         if (ctx->hscal[0].rr < l.thr) break;
+        if (!std::isfinite(ctx->hscal[0].rr)) {   // diverged (SPEC divergence guard)
+          ctx->info.not_converged = 1;
+          ctx->info.breakdown_level = 0;
+          rc = MSS_EBREAKDOWN;
+          set_err(rc, "standard multigrid iteration diverged (non-finite residual)");
+          break;
+        }
         if (it >= ctx->prm.max_iter) {
           ctx->info.not_converged = 1;
           break;
