@@ -319,3 +319,34 @@ def test_comparison_methods(torch_mod, name, mk, method):
     assert rep.true_rel_res <= 1e-10
     assert rep.iters == info.iters
     assert rel(xg.cpu().numpy(), xo) <= 1e-8
+
+
+SCALE_CASES = [
+    ("s2_3d", 3, (32, 32, 32), 2, None),
+    ("s3_3d", 3, (27, 27, 27), 3, None),
+    ("s5_3d", 3, (50, 50, 50), 5, None),
+    ("s3_2d", 2, (81, 81, 1), 3, None),
+    ("s4_m2", 3, (64, 64, 64), 4, 2),
+    ("s2_m1_2d", 2, (64, 64, 1), 2, 1),
+]
+
+
+@pytest.mark.parametrize("name,ndim,n,s,m", SCALE_CASES, ids=[c[0] for c in SCALE_CASES])
+def test_scale_factor_and_m(torch_mod, name, ndim, n, s, m):
+    """Scale factors 2, 3, 5 and smoothing degrees m != s (the paper's sweep, P:602-615,
+    SURVEY NEXT-3): GPU vs oracle counts and solution."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = random_problem(ndim, n, seed=21, contrast=1e4, ell=2.0)
+    mm = s if m is None else m
+    sv = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, params={"scale": s, "m": mm})
+    xg, rep = sv.solve(cu(torch, w.f), rel_tol=1e-10)
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, s=s, m=mm)
+    xo, info = o.solve(w.f, 1e-10)
+    print(f"{name}: dims {[lv.n for lv in o.levels]} gpu {rep.iters} oracle {info.iters}")
+    assert sv.levels == o.L + 1 and sv.levels >= 2
+    assert rep.true_rel_res <= 1e-10
+    assert rep.iters[0] == info.iters[0]
+    for a, b in zip(rep.iters[1:], info.iters[1:]):
+        assert abs(a - b) <= max(2, 0.01 * b)
+    assert rel(xg.cpu().numpy(), xo) <= 1e-8
