@@ -27,6 +27,7 @@ Parity status per function (DESIGN.md §5 lists the pins):
   precond (Eq. 2.10) ................................... pinned (P6)
   pcg / solve .......................................... pinned (P2, P7, P9)
   general_dims_chain (non-integer scale, NEXT-2) ....... pinned (P8, Table 1)
+  modified Jacobi splitting P = 2D (NEXT-3) ............ pinned (P11, dense Eq. 2.10)
   comparison methods (NEXT-1): Tatebe MG preconditioner
     (Eq. 2.9), polynomial preconditioner (§2.1), standard
     multigrid iteration ................................ pinned (P10, dense Eq. 2.9 /
@@ -428,10 +429,13 @@ class MultiScaleOracle:
 
     def __init__(self, ndim, n, K, bc, depth=None, s=4, m=None, f=0.1,
                  interp="linear", max_iter=500, coarse_min=512, use_lift=True,
-                 log_events=False, method="multiscale"):
+                 log_events=False, method="multiscale", splitting="sgs"):
         if method not in self.METHODS:
             raise OracleError(f"unknown method {method}")
+        if splitting not in ("sgs", "jacobi"):
+            raise OracleError(f"unknown splitting {splitting}")
         self.method = method
+        self.splitting = splitting
         self.ndim = ndim
         self.n0 = tuple(n)
         self.bc = list(bc)
@@ -491,10 +495,22 @@ class MultiScaleOracle:
         return y.reshape(b.shape)
 
     # ------------------------------------------------------------------ O13
+    def jacobi_steps(self, k, r, z, msteps):
+        """Modified Jacobi splitting: P = 2D, Q = D - U - L; one step is
+        z <- z + P^{-1}(r - A z) = z + (r - A z) / (2 diag)."""
+        lv = self.levels[k]
+        for _ in range(msteps):
+            z[...] = z + (r - self.A(k, z)) / (2.0 * lv.diag)
+        return z
+
     def smooth(self, k, r, z, nhalf):
         """nhalf alternating half-sweeps starting on red: one SGS step of the
-        red-black splitting P = (D+L)D^{-1}(D+U) equals R, B, R."""
+        red-black splitting P = (D+L)D^{-1}(D+U) equals R, B, R.
+        With the modified Jacobi splitting the m = (nhalf-1)/2 SGS steps become m
+        Jacobi steps."""
         lv = self.levels[k]
+        if self.splitting == "jacobi":
+            return self.jacobi_steps(k, r, z, (nhalf - 1) // 2)
         for h in range(nhalf):
             if h % 2 == 0:
                 halfsweep(lv.T, lv.diag, r, z, 0, lv.red)

@@ -594,3 +594,49 @@ def test_P10_method_ordering_on_C1():
     a = O.MultiScaleOracle(w2.ndim, w2.n, w2.K, w2.bc, method="tatebe").solve(w2.f, 1e-10)[1].iters
     b = O.MultiScaleOracle(w2.ndim, w2.n, w2.K, w2.bc, method="multiscale").solve(w2.f, 1e-10)[1].iters
     assert a[0] == b[0]
+
+
+# ---------------------------------------------------------------- P11 modified Jacobi splitting (NEXT-3)
+@pytest.mark.parametrize("m", [1, 3])
+def test_P11_jacobi_precond_equals_eq_2_10(m):
+    """Eq. 2.10 with the modified Jacobi splitting P = 2D, Q = D - U - L built
+    densely equals the oracle's sequence evaluation (m Jacobi steps, exact coarse
+    correction, m Jacobi steps)."""
+    w = small_problem(2, (16, 16, 1), seed=15, bc=BC_MIXED2)
+    o = O.MultiScaleOracle(2, w.n, w.K, w.bc, depth=1, m=m, splitting="jacobi")
+    o.iters = [0, 0]
+    o.calls = [0, 0]
+    A = dense_from_oracle(o.levels[0].T, o.levels[0].shape)
+    Ac = dense_from_oracle(o.levels[1].T, o.levels[1].shape)
+    D = np.diag(np.diag(A))
+    P = 2 * D
+    Q = P - A
+    assert np.allclose(Q, D - np.tril(A, -1) - np.triu(A, 1))
+    E = np.kron(O.interp_1d(16, 4), O.interp_1d(16, 4))
+    Pi = np.linalg.inv(P)
+    H = Pi @ Q
+    W = E @ np.linalg.inv(Ac) @ E.T
+    Minv = np.linalg.matrix_power(H, m) @ W @ np.linalg.matrix_power(Q @ Pi, m) + \
+        sum(np.linalg.matrix_power(H, j) @ Pi for j in range(2 * m))
+    N = o.levels[0].N
+    Acinv = np.linalg.inv(Ac)
+    I = np.eye(N)
+    cols = np.array([o.precond(0, I[c].reshape(o.levels[0].shape),
+                               coarse=lambda b: (Acinv @ b.ravel()).reshape(b.shape)).ravel()
+                     for c in range(N)]).T
+    assert np.allclose(cols, Minv, atol=1e-11 * np.abs(Minv).max())
+    # the modified (not the plain) Jacobi damps the checkerboard mode (P:360-361)
+    cb = np.indices((16, 16)).sum(axis=0) % 2 * 2.0 - 1.0
+    Hcb = H @ cb.ravel()
+    assert np.linalg.norm(Hcb) < np.linalg.norm(cb.ravel())
+
+
+def test_P11_jacobi_solve_matches_dense():
+    w = small_problem(3, (16, 16, 16), seed=16, bc=BC_MIXED3, contrast=1e3)
+    o = O.MultiScaleOracle(3, w.n, w.K, w.bc, depth=1, splitting="jacobi")
+    x, info = o.solve(w.f, rel_tol=1e-10)
+    A = brute_force_dense(3, w.n, w.K, w.bc)
+    b = O.rhs(3, w.n, o.levels[0].T, w.f, w.bc)
+    xd = np.linalg.solve(A, b.ravel())
+    assert info.true_rel_res <= 1e-10
+    assert np.linalg.norm(x.ravel() - xd) <= 1e-8 * np.linalg.norm(xd)
