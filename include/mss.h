@@ -64,6 +64,8 @@ typedef struct {
                            2 = polynomial-preconditioned CG, W = P^{-1};
                            3 = standard multigrid iteration with M_0^{-1}.
                            1-3 are the paper's comparison methods.           */
+  int     splitting;    /* 0 = symmetric Gauss-Seidel, red-black (default);
+                           1 = modified Jacobi, P = 2D, Q = D - U - L           */
 } mss_params;
 
 /* Per-solve report (the schema of the paper's Tables 1-2). */

@@ -564,7 +564,34 @@ __device__ __forceinline__ double axpy_item(double* __restrict__ x, double* __re
   return rv * rv;
 }
 
+// Modified Jacobi step: z_out = z_in + (r - A z_in) / (2 diag); first: z_in = 0.
+template <int NDIM>
+__device__ __forceinline__ double jacobi_item(const LevelDev& L, int64_t c, const double* __restrict__ r,
+                                              const double* __restrict__ zin, double* __restrict__ zout, int first) {
+  const Cell e = cell_of(L, c);
+  double t[6];
+  load_faces<NDIM>(L, e, t);
+  const double d = diag_of<NDIM>(t);
+  double zn;
+  if (first) {
+    zn = r[c] / (2.0 * d);
+  } else {
+    const double az = d * zin[c] - nbr_sum<NDIM>(L, e, t, [&](int64_t q) { return zin[q]; });
+    zn = zin[c] + (r[c] - az) / (2.0 * d);
+  }
+  zout[c] = zn;
+  return r[c] * zn;
+}
+
 // ------------------------------------------------------------------ grid kernels
+template <int NDIM>
+__global__ void k_jacobi(LevelDev L, const double* __restrict__ r, const double* __restrict__ zin,
+                         double* __restrict__ zout, int first, RedOut ro) {
+  double acc = 0.0;
+  for (int64_t c = gtid(); c < L.N; c += gstride()) acc += jacobi_item<NDIM>(L, c, r, zin, zout, first);
+  if (ro.out) grid_sum_finish(acc, ro);
+}
+
 // r = b - A x, with ||r||^2 reduced when ro.out != nullptr.
 template <int NDIM>
 __global__ void k_residual(LevelDev L, const double* __restrict__ b, const double* __restrict__ x,

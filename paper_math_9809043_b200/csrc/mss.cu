@@ -374,6 +374,25 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
 static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero,
                      double* dot_last = nullptr) {
   Level& l = ctx->lv[k];
+  if (ctx->prm.splitting == 1) {
+    // modified Jacobi: the m = (n_half-1)/2 SGS steps become m Jacobi steps,
+    // ping-ponging between the level's z and s buffers (z must be the level's z)
+    const int steps = (n_half - 1) / 2;
+    if (z != l.z) return set_err(MSS_EINVAL, "Jacobi smoothing needs the level's own z");
+    for (int st = 0; st < steps; ++st) {
+      double* dot = (st == steps - 1) ? dot_last : nullptr;
+      {
+        ProfScope ps(ctx, KC_SWEEP, k, cell_bytes(ctx, KC_SWEEP, k) * l.N);
+        DISPATCH(ctx->ndim, k_jacobi, grid_for(l.N), l.dev(), r, l.z, l.s, (z_zero && st == 0) ? 1 : 0,
+                 red_to(ctx, dot, k, 0));
+      }
+      std::swap(l.z, l.s);
+      tail_mark_dirty(ctx);
+      TRY(do_halo(ctx, k, l.z));
+      if (dot) TRY(do_allred(ctx, k, dot));
+    }
+    return MSS_OK;
+  }
   if (z == l.z && n_half >= 2 && pair_ok(ctx, k)) {
     const int npairs = (n_half - (dot_last ? 1 : 0)) / 2;
     double* cur = l.z;
@@ -543,7 +562,8 @@ static int precond(mss_ctx* ctx, int k) {
   Level& c = ctx->lv[k + 1];
   const int nh = 2 * ctx->prm.m + 1;
   TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));                 // pre-smoothing (a5)
-  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, 1));              // b_{k+1} = R (r - A z) (a6)
+  const int sgs = ctx->prm.splitting == 0;
+  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs));            // b_{k+1} = R (r - A z) (a6)
   if (k + 1 == ctx->L) {                                         // coarsest: exact (a7)
     TRY(op_coarse_solve(ctx, c.r, c.x));
     ctx->info.iters[k + 1] += 1;
@@ -555,7 +575,7 @@ static int precond(mss_ctx* ctx, int k) {
     CK(cudaMemsetAsync(c.x, 0, sizeof(double) * c.N, ctx->stream));
     TRY(pcg_level(ctx, k + 1));
   }
-  TRY(op_prolong_add(ctx, k, c.x, l.z, 1));                      // z_black += (E y) (a8)
+  TRY(op_prolong_add(ctx, k, c.x, l.z, sgs ? 1 : -1));           // z_black += (E y) (a8)
   TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho));  // post-smoothing (a9), rho = r.z
   return MSS_OK;
 }
@@ -572,10 +592,11 @@ static int precond_tatebe(mss_ctx* ctx, int k) {
   if (k == ctx->L) return op_coarse_solve(ctx, l.r, l.z);
   Level& c = ctx->lv[k + 1];
   const int nh = 2 * ctx->prm.m + 1;
+  const int sgs = ctx->prm.splitting == 0;
   TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));
-  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, 1));
+  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs));
   TRY(precond_tatebe(ctx, k + 1));
-  TRY(op_prolong_add(ctx, k, c.z, l.z, 1));
+  TRY(op_prolong_add(ctx, k, c.z, l.z, sgs ? 1 : -1));
   return op_smooth(ctx, k, l.r, l.z, nh, 0, false, k == 0 ? &ctx->dscal[0].rho : nullptr);
 }
 
@@ -1100,6 +1121,7 @@ int mss_default_params(mss_params* p) {
   p->tail_cells = 65536;
   p->gather_below = (int64_t)64 * 64 * 64;
   p->method = 0;
+  p->splitting = 0;
   return MSS_OK;
 }
 
@@ -1141,6 +1163,7 @@ static int setup_common(mss_ctx** out, mss::Comm* comm, int ndim, const int64_t 
   if (prm.m < 0 || prm.max_iter < 1 || !(prm.f > 0) || prm.coarse_min < 1) return set_err(MSS_EINVAL, "bad params");
   if (prm.interp != 0 && prm.interp != 1) return set_err(MSS_EINVAL, "interp must be 0 or 1");
   if (prm.method < 0 || prm.method > 3) return set_err(MSS_EINVAL, "method must be 0..3");
+  if (prm.splitting != 0 && prm.splitting != 1) return set_err(MSS_EINVAL, "splitting must be 0 or 1");
   bool any_dir = false;
   for (int s = 0; s < 2 * ndim; ++s) {
     if (bc[s].kind != 0 && bc[s].kind != 1) return set_err(MSS_EINVAL, "bad BC kind");

@@ -297,7 +297,7 @@ static int tail_setup(mss_ctx* ctx) {
 }
 
 static bool tail_supported(mss_ctx* ctx, int k) {
-  return ctx->prm.method == 0 && ctx->tail_cs > 0 && k >= 1 && k >= ctx->ndist && k < ctx->L &&
+  return ctx->prm.method == 0 && ctx->prm.splitting == 0 && ctx->tail_cs > 0 && k >= 1 && k >= ctx->ndist && k < ctx->L &&
          ctx->lv[k].N <= ctx->prm.tail_cells;
 }
 

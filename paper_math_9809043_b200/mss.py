@@ -46,6 +46,7 @@ class Params(ctypes.Structure):
         ("tail_cells", ctypes.c_int64),
         ("gather_below", ctypes.c_int64),
         ("method", ctypes.c_int),
+        ("splitting", ctypes.c_int),
     ]
 
 METHODS = {"multiscale": 0, "tatebe": 1, "polynomial": 2, "multigrid": 3}

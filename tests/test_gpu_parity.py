@@ -350,3 +350,25 @@ def test_scale_factor_and_m(torch_mod, name, ndim, n, s, m):
     for a, b in zip(rep.iters[1:], info.iters[1:]):
         assert abs(a - b) <= max(2, 0.01 * b)
     assert rel(xg.cpu().numpy(), xo) <= 1e-8
+
+
+@pytest.mark.parametrize("method", ["multiscale", "tatebe"])
+@pytest.mark.parametrize("name,mk", METHOD_CASES, ids=[c[0] for c in METHOD_CASES])
+def test_jacobi_splitting(torch_mod, name, mk, method):
+    """Modified Jacobi splitting P = 2D on the GPU vs oracle."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver, METHODS
+    w = mk()
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth,
+               params={"method": METHODS[method], "splitting": 1, "max_iter": 1000})
+    xg, rep = s.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth, method=method, splitting="jacobi",
+                           max_iter=1000)
+    xo, info = o.solve(w.f, w.rel_tol)
+    print(f"{name} jacobi {method}: gpu {rep.iters} oracle {info.iters}")
+    assert not rep.not_converged and not info.not_converged
+    assert rep.true_rel_res <= 1e-10
+    assert rep.iters[0] == info.iters[0]
+    for a, b in zip(rep.iters[1:], info.iters[1:]):
+        assert abs(a - b) <= max(2, 0.01 * b)
+    assert rel(xg.cpu().numpy(), xo) <= 1e-8
