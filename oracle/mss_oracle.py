@@ -259,28 +259,61 @@ def hierarchy_dims(n, ndim, s=4, depth=None, coarse_min=512):
     return dims
 
 
+def _round_half_up(x):
+    return int(math.floor(x + 0.5))
+
+
 def general_dims_chain(n0, nL, L):
-    """General non-integer scale-factor rule (Q9; NEXT-2 helper):
-    s_eff = (n0/nL)^(1/L), n_k = round(n0 / s_eff^k).  Reproduces Table 1's
-    1001, 252, 63, 16, 4 (P:563-567)."""
+    """General non-integer scale-factor rule (Q9; NEXT-2):
+    s_eff = (n0/nL)^(1/L), n_k = round(n0 / s_eff^k) (halves round up).  Reproduces
+    Table 1's 1001, 252, 63, 16, 4."""
     s_eff = (n0 / nL) ** (1.0 / L)
-    return [int(round(n0 / s_eff ** k)) for k in range(L + 1)]
+    return [_round_half_up(n0 / s_eff ** k) for k in range(L + 1)]
+
+
+def geometric_hierarchy_dims(n, ndim, s=4, depth=None, coarse_min=512):
+    """NEXT-2 hierarchy ("the effective scale factor between adjacent levels
+    may vary slightly in order to obtain an integer grid dimension"): the coarsest
+    dims are n_L,d = max(1, round(n_0,d / s^L)) with L = depth, or the smallest L whose
+    coarsest level has N_L <= coarse_min; every axis then follows its own geometric
+    chain round(n_0,d / s_eff,d^k), s_eff,d = (n_0,d / n_L,d)^(1/L)."""
+    def coarsest(L):
+        return [max(1, _round_half_up(n[d] / s ** L)) for d in range(ndim)]
+    if depth is None:
+        L = 0
+        while int(np.prod([n[d] for d in range(ndim)])) > coarse_min:
+            L += 1
+            if int(np.prod(coarsest(L))) <= coarse_min or L > 10:
+                break
+    else:
+        L = depth
+    if L == 0:
+        return [tuple(n)]
+    nL = coarsest(L)
+    chains = [general_dims_chain(n[d], nL[d], L) for d in range(ndim)]
+    dims = []
+    for k in range(L + 1):
+        t = [chains[d][k] for d in range(ndim)] + [1] * (3 - ndim)
+        dims.append(tuple(t))
+    return dims
 
 
 # ----------------------------------------------------------------------------- O9
-def face_cv_weights(n, s):
+def face_cv_weights(n, s, n_c=None):
     """w[F, i] = |CV_i ∩ CV_F| / |CV_i| (Reading B, Q2).
 
     Positions in fine-cell units; fine face i sits at i with control volume
-    [i-1/2, i+1/2] clipped to [0, n]; coarse face F sits at s F with control volume
-    [s F - s/2, s F + s/2] clipped to [0, n] (the segment between the two coarse
-    cell centres, or between a centre and the boundary)."""
-    Nc = n // s
+    [i-1/2, i+1/2] clipped to [0, n]; coarse face F sits at rho F (rho = n / n_c, = s
+    for an integer scale factor) with control volume [rho (F - 1/2), rho (F + 1/2)]
+    clipped to [0, n] (the segment between the two coarse cell centres, or between a
+    centre and the boundary)."""
+    Nc = n // s if n_c is None else n_c
+    rho = n / Nc
     W = np.zeros((Nc + 1, n + 1))
     for F in range(Nc + 1):
-        a = max(s * F - s / 2.0, 0.0)
-        b = min(s * F + s / 2.0, float(n))
-        for i in range(max(0, s * F - s), min(n, s * F + s) + 1):
+        a = max(rho * F - rho / 2.0, 0.0)
+        b = min(rho * F + rho / 2.0, float(n))
+        for i in range(max(0, int(math.floor(a)) - 1), min(n, int(math.ceil(b)) + 1) + 1):
             lo = max(i - 0.5, 0.0)
             hi = min(i + 0.5, float(n))
             ov = min(b, hi) - max(a, lo)
@@ -289,32 +322,60 @@ def face_cv_weights(n, s):
     return W
 
 
-def coarsen_faces(T, ndim, s):
+def row_fractions(n_f, n_c):
+    """phi[J, j] = |[j, j+1) ∩ [J rho, (J+1) rho)|: the fraction of fine row j's height
+    inside coarse row J ("scaled by the fraction of the height in the
+    overlap"); 1 or 0 for an integer scale factor."""
+    rho = n_f / n_c
+    P = np.zeros((n_c, n_f))
+    for J in range(n_c):
+        a, b = J * rho, (J + 1) * rho
+        for j in range(max(0, int(math.floor(a))), min(n_f, int(math.ceil(b)))):
+            ov = min(b, j + 1.0) - max(a, float(j))
+            if ov > 0:
+                P[J, j] = ov
+    return P
+
+
+def coarsen_faces(T, ndim, s, nc=None):
     """O9, Reading B of P:384-396: for the coarse face F along d,
 
-        1/T^c_F = sum_i  w_i / ( sum_{fine rows j in the coarse row} T_d(i, j) )
+        1/T^c_F = sum_i  w_i / ( sum_{fine rows j} phi_j T_d(i, j) )
 
-    i runs over the fine faces (along d) in F's staggered control volume, j over
-    the s^(ndim-1) fine rows across.  A zero column sum blocks the face (T^c = 0).
-    The coarse operator stays diagonal and keeps Laplace form."""
+    i runs over the fine faces (along d) in F's staggered control volume (weights w),
+    j over the fine rows across, each weighted by the fraction phi of its height inside
+    the coarse row (phi = 1 for an integer scale factor s).  A zero column
+    sum blocks the face (T^c = 0).  The coarse operator stays diagonal and keeps Laplace
+    form.  nc: coarse cells per direction (default n/s)."""
     Tc = []
+    cell_shape = list(T[0].shape)
+    cell_shape[axis_of(ndim, 0)] -= 1
+    nf = [cell_shape[axis_of(ndim, d)] for d in range(ndim)]
+    if nc is None:
+        for d in range(ndim):
+            if nf[d] % s != 0:
+                raise OracleError("non-divisible axis in coarsening")
+        nc = [nf[d] // s for d in range(ndim)]
+    integer = all(nf[d] == s * nc[d] for d in range(ndim))
     for d in range(ndim):
         ax = axis_of(ndim, d)
         Td = T[d]
-        # column sums over blocks of s fine rows along every other axis (phi = 1).
         cs = Td
         for e in range(ndim):
             if e == d:
                 continue
             bx = axis_of(ndim, e)
             ne = cs.shape[bx]
-            if ne % s != 0:
-                raise OracleError("non-divisible axis in coarsening")
-            newshape = list(cs.shape[:bx]) + [ne // s, s] + list(cs.shape[bx + 1:])
-            cs = cs.reshape(newshape).sum(axis=bx + 1)
+            if integer:
+                # column sums over blocks of s fine rows (phi = 1)
+                newshape = list(cs.shape[:bx]) + [ne // s, s] + list(cs.shape[bx + 1:])
+                cs = cs.reshape(newshape).sum(axis=bx + 1)
+            else:
+                Phi = row_fractions(ne, nc[e])
+                cs = np.moveaxis(np.tensordot(Phi, cs, axes=([1], [bx])), 0, bx)
         nfaces = Td.shape[ax]
         n = nfaces - 1
-        W = face_cv_weights(n, s)
+        W = face_cv_weights(n, s, n_c=nc[d])
         csm = np.moveaxis(cs, ax, 0)                    # (n+1, rest...)
         out = np.zeros((W.shape[0],) + csm.shape[1:])
         for F in range(W.shape[0]):
@@ -329,19 +390,21 @@ def coarsen_faces(T, ndim, s):
 
 
 # ----------------------------------------------------------------------------- O10
-def interp_1d(n_f, s, kind="linear"):
+def interp_1d(n_f, s, kind="linear", n_c=None):
     """O10: 1-D extension matrix E (n_f x n_c) between cell centres.
 
-    linear: interpolate between the two nearest coarse centres; fine cells beyond
-    the outermost coarse centres take the end value (zero slope at the boundary,
-    P:416-418, Q12).  constant: fine cell i -> coarse cell i // s (P:414)."""
-    n_c = n_f // s
+    linear: interpolate between the two nearest coarse centres X_I = rho (I + 1/2)
+    (rho = n_f / n_c, = s for an integer scale factor); fine cells beyond the outermost
+    coarse centres take the end value (zero slope at the boundary, Q12).
+    constant: fine cell i -> the coarse cell containing its centre."""
+    n_c = n_f // s if n_c is None else n_c
+    rho = n_f / n_c
     E = np.zeros((n_f, n_c))
     if kind == "constant":
         for i in range(n_f):
-            E[i, i // s] = 1.0
+            E[i, min(int(math.floor((i + 0.5) / rho)), n_c - 1)] = 1.0
         return E
-    X = s * (np.arange(n_c) + 0.5)                     # coarse centres, fine units
+    X = rho * (np.arange(n_c) + 0.5)                   # coarse centres, fine units
     for i in range(n_f):
         x = i + 0.5
         if x <= X[0]:
@@ -349,8 +412,8 @@ def interp_1d(n_f, s, kind="linear"):
         elif x >= X[-1]:
             E[i, n_c - 1] = 1.0
         else:
-            I = int(math.floor((x - X[0]) / s))
-            t = (x - X[I]) / s
+            I = int(math.floor((x - X[0]) / rho))
+            t = (x - X[I]) / rho
             E[i, I] += 1.0 - t
             E[i, I + 1] += t
     return E
@@ -429,7 +492,8 @@ class MultiScaleOracle:
 
     def __init__(self, ndim, n, K, bc, depth=None, s=4, m=None, f=0.1,
                  interp="linear", max_iter=500, coarse_min=512, use_lift=True,
-                 log_events=False, method="multiscale", splitting="sgs"):
+                 log_events=False, method="multiscale", splitting="sgs", dims_mode="integer",
+                 level_dims=None):
         if method not in self.METHODS:
             raise OracleError(f"unknown method {method}")
         if splitting not in ("sgs", "jacobi"):
@@ -453,12 +517,18 @@ class MultiScaleOracle:
             raise OracleError("K must be finite and > 0")
         if not any(k == DIRICHLET for k, _ in bc):
             raise OracleError("all-Neumann operator is singular")
-        dims = hierarchy_dims(self.n0, ndim, s, depth, coarse_min)
+        if level_dims is not None:
+            dims = [tuple(list(d) + [1] * (3 - len(d))) for d in level_dims]
+        elif dims_mode == "geometric":
+            dims = geometric_hierarchy_dims(self.n0, ndim, s, depth, coarse_min)
+        else:
+            dims = hierarchy_dims(self.n0, ndim, s, depth, coarse_min)
+        self.dims = dims
         T = assemble_faces(ndim, self.n0, K, bc)                              # a1
         self.levels: List[Level] = []
         for k, nk in enumerate(dims):
             if k > 0:
-                T = coarsen_faces(T, ndim, s)                                  # a2
+                T = coarsen_faces(T, ndim, s, nc=[nk[d] for d in range(ndim)])  # a2
             shape = shape_of(ndim, nk)
             dg = diagonal(T, shape)
             if np.any(dg <= 0):
@@ -470,7 +540,8 @@ class MultiScaleOracle:
         self.E = []
         for k in range(self.L):
             nk = self.levels[k].n
-            self.E.append([interp_1d(nk[d], s, interp) for d in range(ndim)])
+            nc = self.levels[k + 1].n
+            self.E.append([interp_1d(nk[d], s, interp, n_c=nc[d]) for d in range(ndim)])
         # coarsest level: dense A_L and its Cholesky factor (a3, O11)
         lv = self.levels[self.L]
         self.A_L = self.dense_operator(self.L)

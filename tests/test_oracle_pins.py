@@ -640,3 +640,70 @@ def test_P11_jacobi_solve_matches_dense():
     xd = np.linalg.solve(A, b.ravel())
     assert info.true_rel_res <= 1e-10
     assert np.linalg.norm(x.ravel() - xd) <= 1e-8 * np.linalg.norm(xd)
+
+
+# ---------------------------------------------------------------- P12 non-integer scale factors (NEXT-2)
+def test_P12_table1_chain_from_geometric_rule():
+    dims = O.geometric_hierarchy_dims((1001, 1001, 1), 2, s=4, depth=4)
+    assert [d[:2] for d in dims] == [(1001, 1001), (252, 252), (63, 63), (16, 16), (4, 4)]
+    auto = O.geometric_hierarchy_dims((1001, 1001, 1), 2, s=4, coarse_min=16)
+    assert auto[-1][:2] == (4, 4)
+
+
+@pytest.mark.parametrize("nf,nc", [(50, 13), (101, 25), (23, 6), (16, 4)])
+def test_P12_weights_partition_of_unity(nf, nc):
+    W = O.face_cv_weights(nf, 4, n_c=nc)
+    assert np.allclose(W.sum(axis=0), 1.0)          # every fine face fully covered
+    P = O.row_fractions(nf, nc)
+    assert np.allclose(P.sum(axis=0), 1.0)          # every fine row split among coarse rows
+    assert np.allclose(P.sum(axis=1), nf / nc)      # coarse rows of height rho
+    E = O.interp_1d(nf, 4, n_c=nc)
+    assert np.allclose(E.sum(axis=1), 1.0)
+
+
+@pytest.mark.parametrize("ndim,n,nc", [(2, (50, 30, 1), (13, 7, 1)), (3, (23, 18, 20), (6, 5, 4))])
+def test_P12_uniform_coarse_equals_rediscretised_non_integer(ndim, n, nc):
+    """Partial-overlap coarsening keeps the Laplace form exactly for uniform K,
+    boundary conductances included, at a non-integer scale factor."""
+    bc = bc_table(ndim, {"x-": (DIRICHLET, 1.0), "y+": (DIRICHLET, 0.0)})
+    shape = O.shape_of(ndim, n)
+    Tc = O.coarsen_faces(O.assemble_faces(ndim, n, np.full((1,) + shape, 2.5), bc), ndim, 4,
+                         nc=[nc[d] for d in range(ndim)])
+    Tr = O.assemble_faces(ndim, nc, np.full((1,) + O.shape_of(ndim, nc), 2.5), bc)
+    for d in range(ndim):
+        assert np.allclose(Tc[d], Tr[d], rtol=1e-13, atol=0)
+
+
+def test_P12_layers_parallel_weighted_mean():
+    """Parallel layers across a non-integer coarse row: the coarse conductance is the
+    overlap-weighted sum of the fine rows (conductors in parallel)."""
+    nx, ny, ncx, ncy = 20, 21, 5, 6
+    rng = np.random.default_rng(3)
+    ky = 10 ** rng.uniform(-2, 2, ny)
+    K = np.broadcast_to(ky[:, None], (ny, nx))[None].copy()
+    bc = bc_table(2, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})
+    Tc = O.coarsen_faces(O.assemble_faces(2, (nx, ny, 1), K, bc), 2, 4, nc=[ncx, ncy])
+    Phi = O.row_fractions(ny, ncy)
+    hx, hy = 1 / nx, 1 / ny
+    rowsum = Phi @ (ky * hy / hx)                    # sum_j phi_j T_x(j) of interior fine faces
+    rho_x = nx / ncx
+    expect = rowsum / rho_x                          # interior CV covers rho_x fine faces
+    assert np.allclose(Tc[0][:, 1:-1], np.broadcast_to(expect[:, None], (ncy, ncx - 1)), rtol=1e-13)
+
+
+@pytest.mark.parametrize("ndim,n,depth", [(2, (23, 17, 1), 1), (3, (13, 11, 10), 1), (2, (61, 61, 1), 2)])
+def test_P12_solve_matches_dense_non_integer(ndim, n, depth):
+    bc = BC_MIXED2 if ndim == 2 else BC_MIXED3
+    w = small_problem(ndim, n, seed=17, bc=bc, contrast=1e3)
+    o = O.MultiScaleOracle(ndim, n, w.K, bc, depth=depth, dims_mode="geometric")
+    assert any(o.levels[0].n[d] % o.levels[1].n[d] for d in range(ndim))   # really non-integer
+    x, info = o.solve(w.f, rel_tol=1e-10)
+    A = brute_force_dense(ndim, n, w.K, bc)
+    b = O.rhs(ndim, n, o.levels[0].T, w.f, bc)
+    xd = np.linalg.solve(A, b.ravel())
+    assert info.true_rel_res <= 1e-10
+    assert np.linalg.norm(x.ravel() - xd) <= 1e-8 * np.linalg.norm(xd)
+    for lv in o.levels:
+        if lv.N <= 600:
+            Ad = dense_from_oracle(lv.T, lv.shape)
+            assert np.linalg.eigvalsh(Ad).min() > 0
