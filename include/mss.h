@@ -66,6 +66,13 @@ typedef struct {
                            1-3 are the paper's comparison methods.           */
   int     splitting;    /* 0 = symmetric Gauss-Seidel, red-black (default);
                            1 = modified Jacobi, P = 2D, Q = D - U - L           */
+  int     dims_mode;    /* level dims: 0 = n_k / scale exactly (default; axes must divide);
+                           1 = geometric per-axis chain n_k = round(n_0 / s_eff^k), s_eff =
+                               (n_0 / n_L)^(1/L), non-integer ratios with partial-overlap
+                               weights (Table 1's 1001..4 chain);
+                           2 = explicit: level_dims[0..n_level_dims-1] (level 0 = n)       */
+  int     n_level_dims;
+  int64_t level_dims[MSS_MAX_LEVELS][3];
 } mss_params;
 
 /* Per-solve report (the schema of the paper's Tables 1-2). */

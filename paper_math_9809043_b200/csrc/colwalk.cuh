@@ -363,9 +363,11 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L,
   const int i0 = 2 * m;
   int Xa0, Xa1, Xb0, Xb1, Y0, Y1;
   double wxa0, wxa1, wxb0, wxb1, wy0, wy1;
-  interp_w(i0, ncx, s, kind, Xa0, wxa0, Xa1, wxa1);
-  interp_w(i0 + 1, ncx, s, kind, Xb0, wxb0, Xb1, wxb1);
-  interp_w(j, ncy, s, kind, Y0, wy0, Y1, wy1);
+  const double rx = (double)nx / ncx, ry = (double)ny / ncy, rz = (double)L.nzg / ncz;
+  (void)s;
+  interp_w(i0, ncx, rx, kind, Xa0, wxa0, Xa1, wxa1);
+  interp_w(i0 + 1, ncx, rx, kind, Xb0, wxb0, Xb1, wxb1);
+  interp_w(j, ncy, ry, kind, Y0, wy0, Y1, wy1);
   const int64_t cp = (int64_t)ncx * ncy;
   int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
   for (int k = k0; k < k1; ++k) {
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L,
     const double wx0 = par ? wxb0 : wxa0, wx1 = par ? wxb1 : wxa1;
     int Z0, Z1;
     double wz0, wz1;
-    interp_w(k + L.z0, ncz, s, kind, Z0, wz0, Z1, wz1);
+    interp_w(k + L.z0, ncz, rz, kind, Z0, wz0, Z1, wz1);
     auto Yv = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * (cc - zc0)); };
     double acc = wy0 * (wx0 * Yv(X0, Y0, Z0) + wx1 * Yv(X1, Y0, Z0)) +
                  wy1 * (wx0 * Yv(X0, Y1, Z0) + wx1 * Yv(X1, Y1, Z0));

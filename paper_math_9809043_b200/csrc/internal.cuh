@@ -53,6 +53,7 @@ struct Level {
   int z0 = 0;                            // global z offset of this rank's slab
   int nzg = 0;                           // global nz
   bool dist = false;                     // true: z-slab distributed across ranks (ghost planes = halos)
+  bool uniform = true;                   // transfer to level+1 is an integer scale factor on every axis
   int64_t N = 0, plane = 0;
   double h[3] = {1, 1, 1};
   double *Tx = nullptr, *Ty = nullptr, *Tz = nullptr;

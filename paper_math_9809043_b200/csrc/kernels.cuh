@@ -202,29 +202,46 @@ __global__ void k_coarsen_faces(const double* __restrict__ Tf, double* __restric
     const int F = c3[d] + ((d == 2) ? Z0c : 0);                     // global coarse face
     const int nf_g = (d == 2) ? nzgf : nf_d;                         // global fine count
     const int ioff = (d == 2) ? z0f : 0;                             // global -> local fine face
-    const double a = fmax(s * (double)F - 0.5 * s, 0.0);
-    const double b = fmin(s * (double)F + 0.5 * s, (double)nf_g);
+    // ratios n_f / n_c per axis (s for an integer scale factor; P:403-410 otherwise)
+    const int nfa[3] = {nfx, nfy, (d == 2) ? nzgf : nfz};
+    const int nca[3] = {ncx, ncy, (d == 2) ? (nzgf * ncz) / (nfz ? nfz : 1) : ncz};
+    const double rho = (double)nf_g / (double)((d == 0) ? ncx : (d == 1) ? ncy : nca[2]);
+    const double a = fmax(rho * F - 0.5 * rho, 0.0);
+    const double b = fmin(rho * F + 0.5 * rho, (double)nf_g);
     // the two transverse axes (in 2-D the z axis is a single row)
     const int e1 = (d == 0) ? 1 : 0;
     const int e2 = (d == 2) ? 1 : 2;
-    const int r1_lo = c3[e1] * s, r1_n = s;
-    const int r2_lo = (ndim == 3) ? c3[e2] * s : 0, r2_n = (ndim == 3) ? s : 1;
+    const double r1 = (double)nfa[e1] / nca[e1];
+    const double r2 = (ndim == 3) ? (double)nfa[e2] / nca[e2] : 1.0;
+    // fine rows overlapping the coarse row, with height fractions phi
+    const int J1 = c3[e1], J2 = (ndim == 3) ? c3[e2] : 0;
+    const int q1lo = (int)floor(J1 * r1), q1hi = min(nfa[e1], (int)ceil((J1 + 1) * r1));
+    const int q2lo = (ndim == 3) ? (int)floor(J2 * r2) : 0;
+    const int q2hi = (ndim == 3) ? min(nfa[e2], (int)ceil((J2 + 1) * r2)) : 1;
+    const bool integer_rows = (r1 == floor(r1)) && (r2 == floor(r2));
     double inv = 0.0;
     bool blocked = false;
-    const int ilo = max(0, s * F - s), ihi = min(nf_g, s * F + s);
+    const int ilo = max(0, (int)floor(a) - 1), ihi = min(nf_g, (int)ceil(b) + 1);
     for (int i = ilo; i <= ihi; ++i) {
       const double lo = fmax(i - 0.5, 0.0), hi = fmin(i + 0.5, (double)nf_g);
       const double ov = fmin(b, hi) - fmax(a, lo);
       if (!(ov > 0.0)) continue;
       const double w = ov / (hi - lo);
       double cs = 0.0;
-      for (int q2 = 0; q2 < r2_n; ++q2) {
-        for (int q1 = 0; q1 < r1_n; ++q1) {
+      for (int q2 = q2lo; q2 < q2hi; ++q2) {
+        const double p2 = integer_rows ? 1.0 : fmin((J2 + 1) * r2, q2 + 1.0) - fmax(J2 * r2, (double)q2);
+        for (int q1 = q1lo; q1 < q1hi; ++q1) {
           int f3[3];
           f3[d] = i - ioff;
-          f3[e1] = r1_lo + q1;
-          f3[e2] = r2_lo + q2;
-          cs += Tf[f3[0] + (int64_t)Fx * (f3[1] + (int64_t)Fy * f3[2])];
+          f3[e1] = q1;
+          f3[e2] = (ndim == 3) ? q2 : 0;                             // local (transverse) index
+          const double tv = Tf[f3[0] + (int64_t)Fx * (f3[1] + (int64_t)Fy * f3[2])];
+          if (integer_rows) {
+            cs += tv;
+          } else {
+            const double p1 = fmin((J1 + 1) * r1, q1 + 1.0) - fmax(J1 * r1, (double)q1);
+            cs += (p1 * p2) * tv;
+          }
         }
       }
       if (cs == 0.0) blocked = true;
@@ -406,18 +423,27 @@ __device__ __forceinline__ double sweep_item(const LevelDev& L, uint32_t hx, uin
 }
 
 // 1-D weights of fine cell i onto coarse cells: (I0, w0) + (I1, w1).
-__device__ __forceinline__ void interp_w(int i, int nc, int s, int kind, int& I0, double& w0, int& I1, double& w1) {
-  if (kind == 1 || nc == 1) {   // piecewise constant
-    I0 = min(i / s, nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
+// rho = n_fine / n_coarse along the axis (= s for an integer scale factor; non-integer
+// ratios, place the coarse centres at rho (I + 1/2)).
+__device__ __forceinline__ void interp_w(int i, int nc, double rho, int kind, int& I0, double& w0, int& I1,
+                                         double& w1) {
+  if (kind == 1 || nc == 1) {   // piecewise constant: the coarse cell holding the centre
+    I0 = min((int)floor((i + 0.5) / rho), nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
     return;
   }
   const double x = i + 0.5;                   // fine centre in fine-cell units
-  const double X0 = 0.5 * s, Xl = s * (nc - 0.5);
+  const double X0 = 0.5 * rho, Xl = rho * (nc - 0.5);
   if (x <= X0) { I0 = 0; w0 = 1.0; I1 = 0; w1 = 0.0; return; }          // zero slope
   if (x >= Xl) { I0 = nc - 1; w0 = 1.0; I1 = nc - 1; w1 = 0.0; return; }
-  const int I = (int)floor((x - X0) / s);
-  const double tt = (x - s * (I + 0.5)) / s;
+  const int I = (int)floor((x - X0) / rho);
+  const double tt = (x - rho * (I + 0.5)) / rho;
   I0 = I; w0 = 1.0 - tt; I1 = I + 1; w1 = tt;
+}
+
+// fine-index window [lo, hi) that can touch coarse cell I (rho = n_f / n_c)
+__device__ __forceinline__ void fine_window(int I, double rho, int nf, int& lo, int& hi) {
+  lo = max(0, (int)floor(rho * (I - 1)));
+  hi = min(nf, (int)ceil(rho * (I + 2)));
 }
 
 // One output of the restriction R = E^T along `axis`: (n0,n1,n2) -> n_axis = nc.
@@ -437,13 +463,16 @@ __device__ __forceinline__ void restrict_item(const double* __restrict__ in, dou
   q[2] = (int)(rr / o1);
   const int I = q[axis] + out_off;
   const int nfg = nf_g ? nf_g : nf, ncg = nc_g ? nc_g : nc;
+  const double rho = (double)nfg / (double)ncg;
+  (void)s;
   q[axis] = 0;
   const int64_t base = q[0] + (int64_t)n0 * (q[1] + (int64_t)n1 * q[2]);
   double acc = 0.0;
-  const int ilo = max(0, s * (I - 1)), ihi = min(nfg, s * (I + 2));
+  int ilo, ihi;
+  fine_window(I, rho, nfg, ilo, ihi);
   for (int i = ilo; i < ihi; ++i) {
     int I0, I1; double w0, w1;
-    interp_w(i, ncg, s, kind, I0, w0, I1, w1);
+    interp_w(i, ncg, rho, kind, I0, w0, I1, w1);
     double w = 0.0;
     if (I0 == I) w += w0;
     if (I1 == I && I1 != I0) w += w1;
@@ -464,12 +493,15 @@ __device__ __forceinline__ void resid_restrict_x_item(const LevelDev& L, const d
   const uint32_t k = row / (uint32_t)L.ny;
   const uint32_t j = row - k * (uint32_t)L.ny;
   const int64_t rowoff = (int64_t)L.nx * row;
-  const int ilo = max(0, s * (I - 1)), ihi = min(L.nx, s * (I + 2));
+  const double rho = (double)L.nx / (double)ncx;
+  (void)s;
+  int ilo, ihi;
+  fine_window(I, rho, L.nx, ilo, ihi);
   double acc = 0.0;
   for (int i = ilo; i < ihi; ++i) {
     if (black_only && (((uint32_t)i + j + k + (uint32_t)L.z0) & 1u) == 0u) continue;
     int I0, I1; double w0, w1;
-    interp_w(i, ncx, s, kind, I0, w0, I1, w1);
+    interp_w(i, ncx, rho, kind, I0, w0, I1, w1);
     double w = 0.0;
     if (I0 == I) w += w0;
     if (I1 == I && I1 != I0) w += w1;
@@ -498,9 +530,10 @@ __device__ __forceinline__ void prolong_black_item(const LevelDev& L, uint32_t h
   if (i >= L.nx) return;
   int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
   double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
-  interp_w(i, ncx, s, kind, X0, wx0, X1, wx1);
-  interp_w((int)j, ncy, s, kind, Y0, wy0, Y1, wy1);
-  if (NDIM == 3) interp_w((int)k + L.z0, ncz, s, kind, Z0, wz0, Z1, wz1);
+  (void)s;
+  interp_w(i, ncx, (double)L.nx / ncx, kind, X0, wx0, X1, wx1);
+  interp_w((int)j, ncy, (double)L.ny / ncy, kind, Y0, wy0, Y1, wy1);
+  if (NDIM == 3) interp_w((int)k + L.z0, ncz, (double)L.nzg / ncz, kind, Z0, wz0, Z1, wz1);
   const int64_t cp = (int64_t)ncx * ncy;
   auto Y = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * (cc - zc0)); };
   double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +
@@ -524,9 +557,10 @@ __device__ __forceinline__ void prolong_item(const LevelDev& L, int ncx, int ncy
   if (colour >= 0 && (((e.i + e.j + e.k + L.z0) & 1) != colour)) return;
   int X0, X1, Y0, Y1, Z0 = 0, Z1 = 0;
   double wx0, wx1, wy0, wy1, wz0 = 1.0, wz1 = 0.0;
-  interp_w(e.i, ncx, s, kind, X0, wx0, X1, wx1);
-  interp_w(e.j, ncy, s, kind, Y0, wy0, Y1, wy1);
-  if (NDIM == 3) interp_w(e.k + L.z0, ncz, s, kind, Z0, wz0, Z1, wz1);
+  (void)s;
+  interp_w(e.i, ncx, (double)L.nx / ncx, kind, X0, wx0, X1, wx1);
+  interp_w(e.j, ncy, (double)L.ny / ncy, kind, Y0, wy0, Y1, wy1);
+  if (NDIM == 3) interp_w(e.k + L.z0, ncz, (double)L.nzg / ncz, kind, Z0, wz0, Z1, wz1);
   const int64_t cp = (int64_t)ncx * ncy;
   auto Y = [&](int a, int bb, int cc) { return y[a + (int64_t)ncx * bb + cp * (cc - zc0)]; };
   double acc = wy0 * (wx0 * Y(X0, Y0, Z0) + wx1 * Y(X1, Y0, Z0)) +

@@ -478,7 +478,7 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
     const double by = 8.0 * ((k == 0 && ctx->kfaces ? 1 : ctx->ndim) + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
     ProfScope ps(ctx, KC_RESID, k, by);
     const int hx = f.nx / 2;
-    if (black_only && col_ok(ctx, f) && hx >= 32 && hx <= 512) {
+    if (black_only && f.uniform && col_ok(ctx, f) && hx >= 32 && hx <= 512) {
       const int bt = (hx + 31) / 32 * 32;
       int nch = (f.nz + kColChunk - 1) / kColChunk;
       if ((int64_t)nch * f.ny < 2 * kSMs * 4) nch = std::min<int>(f.nz, (2 * kSMs * 4 + f.ny - 1) / f.ny);
@@ -802,22 +802,73 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
 
 // ============================================================================ setup
 // Host mirror of interp_w (kernels.cuh): 1-D extension weights of fine cell i.
-static void interp_host(int i, int nc, int s, int kind, int& I0, double& w0, int& I1, double& w1) {
+static void interp_host(int i, int nc, double rho, int kind, int& I0, double& w0, int& I1, double& w1) {
   if (kind == 1 || nc == 1) {
-    I0 = std::min(i / s, nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
+    I0 = std::min((int)std::floor((i + 0.5) / rho), nc - 1); w0 = 1.0; I1 = I0; w1 = 0.0;
     return;
   }
   const double x = i + 0.5;
-  const double X0 = 0.5 * s, Xl = s * (nc - 0.5);
+  const double X0 = 0.5 * rho, Xl = rho * (nc - 0.5);
   if (x <= X0) { I0 = 0; w0 = 1.0; I1 = 0; w1 = 0.0; return; }
   if (x >= Xl) { I0 = nc - 1; w0 = 1.0; I1 = nc - 1; w1 = 0.0; return; }
-  const int I = (int)std::floor((x - X0) / s);
-  const double tt = (x - s * (I + 0.5)) / s;
+  const int I = (int)std::floor((x - X0) / rho);
+  const double tt = (x - rho * (I + 0.5)) / rho;
   I0 = I; w0 = 1.0 - tt; I1 = I + 1; w1 = tt;
 }
 
-static int build_hierarchy_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min,
+static int64_t round_half_up(double x) { return (int64_t)std::floor(x + 0.5); }
+
+// NEXT-2 geometric rule (mirrors the oracle's geometric_hierarchy_dims): coarsest
+// n_L,d = max(1, round(n_0,d / s^L)), per-axis chain round(n_0,d / s_eff,d^k).
+static int build_geometric_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min,
                                 std::vector<std::array<int64_t, 3>>& dims) {
+  auto coarsest = [&](int L, int64_t out[3]) {
+    for (int d = 0; d < 3; ++d) out[d] = 1;
+    for (int d = 0; d < ndim; ++d) out[d] = std::max<int64_t>(1, round_half_up((double)n[d] / std::pow((double)s, L)));
+  };
+  int L = 0;
+  if (depth >= 0) {
+    L = depth;
+  } else {
+    int64_t N0 = 1;
+    for (int d = 0; d < ndim; ++d) N0 *= n[d];
+    while (N0 > coarse_min) {
+      L++;
+      int64_t c[3];
+      coarsest(L, c);
+      if (c[0] * c[1] * c[2] <= coarse_min || L > 10) break;
+    }
+  }
+  if (L + 1 > MSS_MAX_LEVELS) return set_err(MSS_EINVAL, "too many levels");
+  int64_t nL[3];
+  coarsest(L, nL);
+  for (int k = 0; k <= L; ++k) {
+    std::array<int64_t, 3> cur = {1, 1, 1};
+    for (int d = 0; d < ndim; ++d) {
+      const double seff = std::pow((double)n[d] / (double)nL[d], 1.0 / (L ? L : 1));
+      cur[d] = (k == 0) ? n[d] : round_half_up((double)n[d] / std::pow(seff, k));
+    }
+    dims.push_back(cur);
+  }
+  return MSS_OK;
+}
+
+static int build_hierarchy_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min,
+                                std::vector<std::array<int64_t, 3>>& dims, const mss_params* prm = nullptr) {
+  if (prm && prm->dims_mode == 1) return build_geometric_dims(ndim, n, s, depth, coarse_min, dims);
+  if (prm && prm->dims_mode == 2) {
+    if (prm->n_level_dims < 1 || prm->n_level_dims > MSS_MAX_LEVELS) return set_err(MSS_EINVAL, "bad n_level_dims");
+    for (int k = 0; k < prm->n_level_dims; ++k) {
+      std::array<int64_t, 3> cur = {1, 1, 1};
+      for (int d = 0; d < ndim; ++d) {
+        cur[d] = prm->level_dims[k][d];
+        if (cur[d] < 1 || (k == 0 && cur[d] != n[d]) || (k > 0 && cur[d] > dims[k - 1][d]))
+          return set_err(MSS_EINVAL, "explicit level dims must start at n and not grow");
+      }
+      dims.push_back(cur);
+    }
+    return MSS_OK;
+  }
   std::array<int64_t, 3> cur = {n[0], n[1], ndim == 3 ? n[2] : 1};
   dims.push_back(cur);
   for (;;) {
@@ -886,7 +937,7 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   const int ndim = ctx->ndim;
   const int s = ctx->prm.scale;
   std::vector<std::array<int64_t, 3>> dims;
-  TRY(build_hierarchy_dims(ndim, n, s, depth, ctx->prm.coarse_min, dims));
+  TRY(build_hierarchy_dims(ndim, n, s, depth, ctx->prm.coarse_min, dims, &ctx->prm));
   ctx->L = (int)dims.size() - 1;
   ctx->lv.resize(dims.size());
   // z-slab decomposition: levels with N_k >= gather_below are split into
@@ -933,6 +984,15 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     if (k == 0) TRY(valloc(ctx, l, &l.b));
     else l.b = l.r;
   }
+  for (int k = 0; k <= ctx->L; ++k) {
+    Level& f = ctx->lv[k];
+    f.uniform = true;
+    if (k < ctx->L)
+      for (int d = 0; d < ndim; ++d) f.uniform = f.uniform && (dims[k][d] == (int64_t)s * dims[k + 1][d]);
+  }
+  if (ctx->ndist > 0)
+    for (int k = 0; k < ctx->L; ++k)
+      if (!ctx->lv[k].uniform) return set_err(MSS_EINVAL, "distributed solves need an integer scale factor");
   for (int k = 0; k < ctx->L; ++k) {
     Level& f = ctx->lv[k];
     Level& c = ctx->lv[k + 1];
@@ -955,7 +1015,7 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       std::vector<W1> tab(nf[d]);
       for (int i = 0; i < nf[d]; ++i) {
         W1& e = tab[i];
-        interp_host(i, ncs[d], s, ctx->prm.interp, e.I0, e.w0, e.I1, e.w1);
+        interp_host(i, ncs[d], (double)nf[d] / ncs[d], ctx->prm.interp, e.I0, e.w0, e.I1, e.w1);
         if (e.I1 == e.I0) e.w1 = 0.0;
       }
       TRY(dalloc(ctx, &f.w[d], sizeof(W1) * tab.size()));
@@ -1122,6 +1182,9 @@ int mss_default_params(mss_params* p) {
   p->gather_below = (int64_t)64 * 64 * 64;
   p->method = 0;
   p->splitting = 0;
+  p->dims_mode = 0;
+  p->n_level_dims = 0;
+  memset(p->level_dims, 0, sizeof(p->level_dims));
   return MSS_OK;
 }
 

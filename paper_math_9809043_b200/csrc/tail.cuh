@@ -296,7 +296,14 @@ static int tail_setup(mss_ctx* ctx) {
   return MSS_OK;
 }
 
+static bool levels_uniform_from(const mss_ctx* ctx, int k) {
+  for (int q = k; q < ctx->L; ++q)
+    if (!ctx->lv[q].uniform) return false;
+  return true;
+}
+
 static bool tail_supported(mss_ctx* ctx, int k) {
+  if (!levels_uniform_from(ctx, k)) return false;
   return ctx->prm.method == 0 && ctx->prm.splitting == 0 && ctx->tail_cs > 0 && k >= 1 && k >= ctx->ndist && k < ctx->L &&
          ctx->lv[k].N <= ctx->prm.tail_cells;
 }

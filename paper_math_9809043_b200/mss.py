@@ -47,6 +47,9 @@ class Params(ctypes.Structure):
         ("gather_below", ctypes.c_int64),
         ("method", ctypes.c_int),
         ("splitting", ctypes.c_int),
+        ("dims_mode", ctypes.c_int),
+        ("n_level_dims", ctypes.c_int),
+        ("level_dims", (ctypes.c_int64 * 3) * MAX_LEVELS),
     ]
 
 METHODS = {"multiscale": 0, "tatebe": 1, "polynomial": 2, "multigrid": 3}
@@ -154,6 +157,15 @@ def default_params(**kw) -> Params:
     for k, v in kw.items():
         if not hasattr(p, k):
             raise KeyError(k)
+        if k == "level_dims":
+            for i, dd in enumerate(v):
+                dd = list(dd) + [1] * (3 - len(dd))
+                for a in range(3):
+                    p.level_dims[i][a] = int(dd[a])
+            p.n_level_dims = len(v)
+            if "dims_mode" not in kw:
+                p.dims_mode = 2
+            continue
         setattr(p, k, v)
     return p
 

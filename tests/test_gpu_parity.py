@@ -372,3 +372,55 @@ def test_jacobi_splitting(torch_mod, name, mk, method):
     for a, b in zip(rep.iters[1:], info.iters[1:]):
         assert abs(a - b) <= max(2, 0.01 * b)
     assert rel(xg.cpu().numpy(), xo) <= 1e-8
+
+
+NONINT_CASES = [
+    ("geo_2d_61", 2, (61, 61, 1), {"dims_mode": 1, "depth": 2}),
+    ("geo_3d_45x38x30", 3, (45, 38, 30), {"dims_mode": 1, "depth": 2}),
+    ("geo_2d_101_auto", 2, (101, 101, 1), {"dims_mode": 1}),
+    ("explicit_semicoarsen_2d", 2, (96, 24, 1), {"level_dims": [(96, 24), (96, 6), (24, 2)]}),
+    ("explicit_3d", 3, (40, 30, 24), {"level_dims": [(40, 30, 24), (12, 9, 7), (3, 3, 2)]}),
+]
+
+
+@pytest.mark.parametrize("name,ndim,n,kw", NONINT_CASES, ids=[c[0] for c in NONINT_CASES])
+def test_non_integer_scale_factors(torch_mod, name, ndim, n, kw):
+    """Non-integer scale factors with partial-overlap weights and semi-coarsening
+    (SURVEY NEXT-2): faces on every level, and the
+    solve, against the oracle."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = random_problem(ndim, n, seed=31, contrast=1e4, ell=2.0)
+    kw = dict(kw)
+    depth = kw.pop("depth", None)
+    sv = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=depth, params=kw)
+    if "level_dims" in kw:
+        o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, level_dims=kw["level_dims"])
+    else:
+        o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=depth, dims_mode="geometric")
+    assert sv.levels == o.L + 1
+    for k, lv in enumerate(o.levels):
+        assert sv.level_dims(k)[:ndim] == lv.n[:ndim]
+        for d in range(ndim):
+            assert rel(sv.faces(k, d).cpu().numpy(), lv.T[d]) <= 1e-12, (k, d)
+    xg, rep = sv.solve(cu(torch, w.f), rel_tol=1e-10)
+    xo, info = o.solve(w.f, 1e-10)
+    print(f"{name}: dims {[lv.n[:ndim] for lv in o.levels]} gpu {rep.iters} oracle {info.iters}")
+    assert rep.true_rel_res <= 1e-10
+    assert rep.iters[0] == info.iters[0]
+    for a, b in zip(rep.iters[1:], info.iters[1:]):
+        assert abs(a - b) <= max(2, 0.01 * b)
+    assert rel(xg.cpu().numpy(), xo) <= 1e-8
+
+
+def test_table1_chain_on_gpu(torch_mod):
+    """The paper's base-case grid chain 1001 -> 252 -> 63 -> 16 -> 4 (Table 1)
+    from the geometric rule, solved on the GPU (log-normal K, ratio 1e6)."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = random_problem(2, (1001, 1001, 1), seed=33, contrast=1e6, ell=8.0, f_kind="zero")
+    sv = Solver(2, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=4, params={"dims_mode": 1})
+    assert [sv.level_dims(k)[:2] for k in range(sv.levels)] == [(1001, 1001), (252, 252), (63, 63), (16, 16), (4, 4)]
+    x, rep = sv.solve(cu(torch, w.f), rel_tol=1e-10)
+    print("table-1 chain iters", rep.iters)
+    assert rep.true_rel_res <= 1e-10 and not rep.not_converged
