@@ -408,13 +408,35 @@ namespace mss {
 // zin 8 + zout 8 = 48 for TWO half-sweeps (48 each when separate).  Per-cell arithmetic
 // and operand order are those of sweep_item.
 constexpr int kPX = 32;   // extended tile: pairs (incl. ring)
-constexpr int kPY = 8;    // extended tile: rows (incl. ring)
+constexpr int kPY = 16;   // extended tile: rows (incl. ring)
+
+// second-colour update of the pair at plane kp (faces / r reloaded from L1: they were
+// fetched one step earlier by the same thread)
+__device__ __forceinline__ double2 pair_second(const LevelDev& L, const double* __restrict__ r, int64_t c, int i0,
+                                               int j, int kp, int pb, double own, double xnb, double ys, double yn,
+                                               double zl, double zh) {
+  const int nx = L.nx, ny = L.ny;
+  const int64_t row = j + (int64_t)ny * kp;
+  const int64_t fx = c + row;
+  const double txl = __ldg(L.Tx + fx + pb), txh = __ldg(L.Tx + fx + pb + 1);
+  const int64_t fy = c + (int64_t)nx * kp;
+  const double t2 = __ldg(L.Ty + fy + pb), t3 = __ldg(L.Ty + fy + nx + pb);
+  const double t4 = __ldg(L.Tz + c + pb), t5 = __ldg(L.Tz + c + L.plane + pb);
+  const double rp = r[c + pb];
+  const double xl = pb ? own : xnb, xh = pb ? xnb : own;
+  const double acc = rp + (txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * zl + t5 * zh);
+  const double v2 = acc / (txl + txh + t2 + t3 + t4 + t5);
+  (void)i0;
+  return pb ? make_double2(own, v2) : make_double2(v2, own);
+}
 
 template <bool FIRST>
-__global__ void __launch_bounds__(kPX * kPY, 4) k_sweep2_col(LevelDev L, const double* __restrict__ r,
+__global__ void __launch_bounds__(kPX * kPY, 2) k_sweep2_col(LevelDev L, const double* __restrict__ r,
                                                              const double* __restrict__ zin,
                                                              double* __restrict__ zout, int col1, int kchunk) {
-  __shared__ double red[3][kPY][kPX];
+  // first-colour values of the extended tile for 4 planes: slots k&3; one barrier per
+  // plane suffices (the slot written at k+1 was last read before the barrier of k)
+  __shared__ double red[4][kPY][kPX];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int m = blockIdx.x * (kPX - 2) + tx - 1;
   const int j = blockIdx.y * (kPY - 2) + ty - 1;
@@ -427,113 +449,65 @@ __global__ void __launch_bounds__(kPX * kPY, 4) k_sweep2_col(LevelDev L, const d
   const bool interior = valid && tx >= 1 && tx <= kPX - 2 && ty >= 1 && ty <= kPY - 2;
   const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
   const int kb = max(k0 - 1, 0);
-  const int ke = min(k1, nz - 1);   // last plane of the first half-sweep
+  const int ke = min(k1, nz - 1);
   int64_t c = valid ? i0 + (int64_t)nx * (j + (int64_t)ny * kb) : 0;
-  double2 zdn = make_double2(0, 0), zc = make_double2(0, 0), tzl = make_double2(0, 0);
-  if (valid) {
-    if (!FIRST) {
-      zdn = ld2(zin + c - plane);
-      zc = ld2(zin + c);
-    }
-    tzl = ldg2(L.Tz + c);
+  double2 zdn = make_double2(0, 0), zc = make_double2(0, 0);
+  if (valid && !FIRST) {
+    zdn = ld2(zin + c - plane);
+    zc = ld2(zin + c);
   }
-  // faces / r of the previous plane (for the second half-sweep one plane behind)
-  double ptx0 = 0, ptx1 = 0, ptx2 = 0;
-  double2 ptyl = make_double2(0, 0), ptyu = make_double2(0, 0), ptzl = make_double2(0, 0),
-          ptzu = make_double2(0, 0), prr = make_double2(0, 0);
-  for (int k = kb; k <= ke; ++k) {
-    const int par = (i0 + j + k + L.z0 + col1) & 1;   // col1 cell of the pair at plane k
-    double tx0 = 0, tx1 = 0, tx2 = 0;
-    double2 tyl = make_double2(0, 0), tyu = make_double2(0, 0), tzu = make_double2(0, 0), rr = make_double2(0, 0);
-    double2 zup = make_double2(0, 0);
-    double v1 = 0.0;
-    if (valid) {
-      const int64_t row = j + (int64_t)ny * k;
-      const int64_t fx = c + row;
-      tx0 = __ldg(L.Tx + fx); tx1 = __ldg(L.Tx + fx + 1); tx2 = __ldg(L.Tx + fx + 2);
-      const int64_t fy = c + (int64_t)nx * k;
-      tyl = ldg2(L.Ty + fy); tyu = ldg2(L.Ty + fy + nx);
-      tzu = ldg2(L.Tz + c + plane);
-      rr = ld2(r + c);
-      const double txl = par ? tx1 : tx0, txh = par ? tx2 : tx1;
-      const double t2 = sel(tyl, par), t3 = sel(tyu, par), t4 = sel(tzl, par), t5 = sel(tzu, par);
-      double acc = sel(rr, par);
-      if (!FIRST) {
-        zup = ld2(zin + c + plane);
-        double xl, xh;
-        if (par) {
-          xl = zc.x;
-          xh = hasR ? zin[c + 2] : 0.0;
-        } else {
-          xl = hasL ? zin[c - 1] : 0.0;
-          xh = zc.y;
+  for (int k = kb; k <= ke + 1; ++k) {
+    // ---- first colour at plane k (k <= ke)
+    if (k <= ke) {
+      const int par = (i0 + j + k + L.z0 + col1) & 1;
+      double v1 = 0.0;
+      double2 zup = make_double2(0, 0);
+      if (valid) {
+        const int64_t row = j + (int64_t)ny * k;
+        const int64_t fx = c + row;
+        const double txl = __ldg(L.Tx + fx + par), txh = __ldg(L.Tx + fx + par + 1);
+        const int64_t fy = c + (int64_t)nx * k;
+        const double t2 = __ldg(L.Ty + fy + par), t3 = __ldg(L.Ty + fy + nx + par);
+        const double t4 = __ldg(L.Tz + c + par), t5 = __ldg(L.Tz + c + plane + par);
+        double acc = r[c + par];
+        if (!FIRST) {
+          zup = ld2(zin + c + plane);
+          double xl, xh;
+          if (par) {
+            xl = zc.x;
+            xh = hasR ? zin[c + 2] : 0.0;
+          } else {
+            xl = hasL ? zin[c - 1] : 0.0;
+            xh = zc.y;
+          }
+          const double ys = hasS ? zin[c - nx + par] : 0.0;
+          const double yn = hasN ? zin[c + nx + par] : 0.0;
+          acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * sel(zup, par);
         }
-        const double ys = hasS ? sel(ld2(zin + c - nx), par) : 0.0;
-        const double yn = hasN ? sel(ld2(zin + c + nx), par) : 0.0;
-        acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * sel(zup, par);
+        v1 = acc / (txl + txh + t2 + t3 + t4 + t5);
       }
-      v1 = acc / (txl + txh + t2 + t3 + t4 + t5);
+      red[k & 3][ty][tx] = v1;
+      if (!FIRST) {
+        zdn = zc;
+        zc = zup;
+      }
     }
-    red[k % 3][ty][tx] = v1;
     __syncthreads();
-    const int kp = k - 1;   // plane of the second half-sweep
+    // ---- second colour at plane kp = k - 1 (interior of the tile)
+    const int kp = k - 1;
     if (kp >= k0 && kp < k1 && interior) {
-      const int pb = (i0 + j + kp + L.z0 + col1 + 1) & 1;   // other-colour cell at plane kp
-      const double own = red[kp % 3][ty][tx];                // col1 cell of the same pair at kp
-      double xl, xh;
-      if (pb) {   // other-colour cell is i0+1: left = own col1 cell (i0), right = col1 cell of pair m+1
-        xl = own;
-        xh = hasR ? red[kp % 3][ty][tx + 1] : 0.0;
-      } else {    // other-colour cell is i0: left = col1 cell of pair m-1, right = own col1 cell (i0+1)
-        xl = hasL ? red[kp % 3][ty][tx - 1] : 0.0;
-        xh = own;
-      }
-      const double ys = hasS ? red[kp % 3][ty - 1][tx] : 0.0;
-      const double yn = hasN ? red[kp % 3][ty + 1][tx] : 0.0;
-      const double zl = (kp > 0) ? red[(kp + 2) % 3][ty][tx] : 0.0;    // plane kp-1
-      const double zh = (kp < nz - 1) ? red[k % 3][ty][tx] : 0.0;      // plane kp+1 = k
-      const double txl = pb ? ptx1 : ptx0, txh = pb ? ptx2 : ptx1;
-      const double t2 = sel(ptyl, pb), t3 = sel(ptyu, pb), t4 = sel(ptzl, pb), t5 = sel(ptzu, pb);
-      const double acc = sel(prr, pb) + (txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * zl + t5 * zh);
-      const double v2 = acc / (txl + txh + t2 + t3 + t4 + t5);
-      const int64_t cp = c - plane;
-      *reinterpret_cast<double2*>(zout + cp) = pb ? make_double2(own, v2) : make_double2(v2, own);
-    }
-    __syncthreads();
-    // carry plane k -> previous
-    ptx0 = tx0; ptx1 = tx1; ptx2 = tx2; ptyl = tyl; ptyu = tyu; ptzl = tzl; ptzu = tzu; prr = rr;
-    if (!FIRST) {
-      zdn = zc;
-      zc = zup;
-    }
-    tzl = tzu;
-    c += plane;
-  }
-  // the last plane of the chunk when it is the domain's top plane (no plane above to lag)
-  if (k1 == nz && ke == nz - 1) {
-    const int kp = nz - 1;
-    if (kp >= k0 && interior) {
       const int pb = (i0 + j + kp + L.z0 + col1 + 1) & 1;
-      const double own = red[kp % 3][ty][tx];
-      double xl, xh;
-      if (pb) {
-        xl = own;
-        xh = hasR ? red[kp % 3][ty][tx + 1] : 0.0;
-      } else {
-        xl = hasL ? red[kp % 3][ty][tx - 1] : 0.0;
-        xh = own;
-      }
-      const double ys = hasS ? red[kp % 3][ty - 1][tx] : 0.0;
-      const double yn = hasN ? red[kp % 3][ty + 1][tx] : 0.0;
-      const double zl = (kp > 0) ? red[(kp + 2) % 3][ty][tx] : 0.0;
-      const double zh = 0.0;
-      const double txl = pb ? ptx1 : ptx0, txh = pb ? ptx2 : ptx1;
-      const double t2 = sel(ptyl, pb), t3 = sel(ptyu, pb), t4 = sel(ptzl, pb), t5 = sel(ptzu, pb);
-      const double acc = sel(prr, pb) + (txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * zl + t5 * zh);
-      const double v2 = acc / (txl + txh + t2 + t3 + t4 + t5);
-      const int64_t cp = c - plane;
-      *reinterpret_cast<double2*>(zout + cp) = pb ? make_double2(own, v2) : make_double2(v2, own);
+      const int s1 = kp & 3;
+      const double own = red[s1][ty][tx];
+      const double xnb = pb ? (hasR ? red[s1][ty][tx + 1] : 0.0) : (hasL ? red[s1][ty][tx - 1] : 0.0);
+      const double ys = hasS ? red[s1][ty - 1][tx] : 0.0;
+      const double yn = hasN ? red[s1][ty + 1][tx] : 0.0;
+      const double zl = (kp > 0) ? red[(kp + 3) & 3][ty][tx] : 0.0;
+      const double zh = (kp < nz - 1) ? red[k & 3][ty][tx] : 0.0;
+      const int64_t cp = c - plane;   // c already advanced to plane k
+      *reinterpret_cast<double2*>(zout + cp) = pair_second(L, r, cp, i0, j, kp, pb, own, xnb, ys, yn, zl, zh);
     }
+    if (k <= ke) c += plane;
   }
 }
 

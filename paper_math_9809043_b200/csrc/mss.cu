@@ -344,10 +344,13 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
 
 // Temporally fused pair of half-sweeps (colour col1 then the other) zin -> zout.
 static bool pair_ok(const mss_ctx* ctx, int k) {
-  // opt-in (MSS_PAIR=1) until it beats two single sweeps
-  static int enabled = -1;
-  if (enabled < 0) enabled = getenv("MSS_PAIR") ? 1 : 0;
-  return enabled && col_ok(ctx, ctx->lv[k]) && !dist_level(ctx, k);
+  // Fused pairs beat two single sweeps on large levels only (512^3: 1.50 ms per pair vs
+  // 1.96 ms; 128^3: slower, the per-plane block barrier dominates): default for levels of
+  // at least 2^24 cells; MSS_PAIR=0 disables, MSS_PAIR=1 forces every eligible level.
+  const char* env = getenv("MSS_PAIR");   // read per call so tests can toggle it
+  const int mode = env ? atoi(env) : -1;
+  if (mode == 0 || !col_ok(ctx, ctx->lv[k]) || dist_level(ctx, k)) return false;
+  return mode == 1 || ctx->lv[k].N >= ((int64_t)1 << 24);
 }
 
 static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, double* zout, int col1, bool first) {

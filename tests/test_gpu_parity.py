@@ -424,3 +424,38 @@ def test_table1_chain_on_gpu(torch_mod):
     x, rep = sv.solve(cu(torch, w.f), rel_tol=1e-10)
     print("table-1 chain iters", rep.iters)
     assert rep.true_rel_res <= 1e-10 and not rep.not_converged
+
+
+@pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
+                                     ("3d_ragged", CASES[1][1])], ids=["C2", "C5_128", "3d_ragged"])
+def test_fused_pair_sweeps_match_single_sweeps(torch_mod, name, mk, monkeypatch):
+    """Temporally fused red+black pairs (k_sweep2_col, forced on every eligible level)
+    against single half-sweeps: identical counts, solutions within 1e-12; and the 9-sweep
+    smoothing hook against the oracle."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = mk()
+    K = torch.from_numpy(w.K).cuda()
+    monkeypatch.setenv("MSS_PAIR", "0")
+    a = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+    xa, ra = a.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    monkeypatch.setenv("MSS_PAIR", "1")
+    b = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+    xb, rb = b.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+    assert ra.iters == rb.iters
+    assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-12
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth)
+    rng = np.random.default_rng(3)
+    lv = o.levels[0]
+    r = rng.standard_normal(lv.shape)
+    zg = b.smooth(0, cu(torch, r), None, 9, 0).cpu().numpy()
+    zo = np.zeros(lv.shape)
+    o.smooth(0, r, zo, 9)
+    assert rel(zg, zo) <= KTOL
+    z0 = rng.standard_normal(lv.shape)
+    zg = b.smooth(0, cu(torch, r), cu(torch, z0), 4, 1).cpu().numpy()
+    zo = z0.copy()
+    for h in range(4):
+        col = (1 + h) % 2
+        O.halfsweep(lv.T, lv.diag, r, zo, col, lv.red if col == 0 else lv.black)
+    assert rel(zg, zo) <= KTOL
