@@ -207,7 +207,7 @@ static KFaces kfaces_of(const mss_ctx* ctx) {
   } while (0)
 
 // ============================================================================ live kernel timing
-enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_TAIL };
+enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_TAIL, KC_PAIR };
 
 static cudaEvent_t ev_get(mss_ctx* ctx) {
   if (!ctx->ev_free.empty()) {
@@ -361,8 +361,8 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
   if ((int64_t)nch * bx * by > kMaxPartials) nch = std::max(1, kMaxPartials / (bx * by));
   const int kch = (l.nz + nch - 1) / nch;
   nch = (l.nz + kch - 1) / kch;
-  // algorithmic bytes: T + r + zout (+ zin when not from zero), 2 half-sweeps per pass
-  ProfScope ps(ctx, first ? KC_SWEEP0 : KC_SWEEP, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
+  // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero)
+  ProfScope ps(ctx, KC_PAIR, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
   const dim3 grid(bx, by, nch), blk(kPX, kPY);
   if (first) k_sweep2_col<true><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
   else k_sweep2_col<false><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);

@@ -114,7 +114,7 @@ SIGNATURES = [
 ]
 
 KCLASS = ["halfsweep", "halfsweep_first", "residual", "restrict", "prolong_add", "pdir_spmv_dot",
-          "axpy_norm", "dot", "coarse_solve", "tail"]
+          "axpy_norm", "dot", "coarse_solve", "tail", "pair_sweep"]
 
 _lib = None
 
