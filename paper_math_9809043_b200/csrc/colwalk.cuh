@@ -410,93 +410,120 @@ namespace mss {
 constexpr int kPX = 32;   // extended tile: pairs (incl. ring)
 constexpr int kPY = 16;   // extended tile: rows (incl. ring)
 
-// second-colour update of the pair at plane kp (faces / r reloaded from L1: they were
-// fetched one step earlier by the same thread)
-__device__ __forceinline__ double2 pair_second(const LevelDev& L, const double* __restrict__ r, int64_t c, int i0,
-                                               int j, int kp, int pb, double own, double xnb, double ys, double yn,
-                                               double zl, double zh) {
-  const int nx = L.nx, ny = L.ny;
-  const int64_t row = j + (int64_t)ny * kp;
-  const int64_t fx = c + row;
-  const double txl = __ldg(L.Tx + fx + pb), txh = __ldg(L.Tx + fx + pb + 1);
-  const int64_t fy = c + (int64_t)nx * kp;
-  const double t2 = __ldg(L.Ty + fy + pb), t3 = __ldg(L.Ty + fy + nx + pb);
-  const double t4 = __ldg(L.Tz + c + pb), t5 = __ldg(L.Tz + c + L.plane + pb);
-  const double rp = r[c + pb];
-  const double xl = pb ? own : xnb, xh = pb ? xnb : own;
-  const double acc = rp + (txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * zl + t5 * zh);
-  const double v2 = acc / (txl + txh + t2 + t3 + t4 + t5);
-  (void)i0;
-  return pb ? make_double2(own, v2) : make_double2(v2, own);
-}
+// ---------------------------------------------------------------------------------------------
+// Fused red+black pair of half-sweeps (k_sweep2_col): a 32 x 16 tile of pairs (incl. a 1-cell
+// ring whose first-colour values feed the interior's second colour) walks z; the first colour
+// of plane k goes to a 4-slot shared ring (one barrier per plane), the second colour of plane
+// k-1 follows from it.  Software-pipelined: every input of plane k+1 (both cells of the pair: Tx[3], Ty/Ty_n/Tz_up/r as 128-bit pairs, and
+// the other-colour neighbours of z) is loaded while plane k is finished: the loads stay in
+// flight across the block barrier and the second-colour update, which now runs from registers
+// and shared memory only.  Tz's lower faces of plane k+1 are plane k's upper faces (carried).
+struct PairIn {
+  double tx0, tx1, tx2;   // x-faces of the pair: left of i0, between, right of i0+1
+  double2 ty, tyn, tzu;   // y-faces south/north and z-faces above, per cell of the pair
+  double2 rr;             // right-hand side per cell
+  double2 zup;            // z_in at plane k+1 (other-colour neighbours above)
+  double xn, ys, yn;      // other-colour x neighbour outside the pair, y neighbours
+};
+
+struct PairSec {          // second-colour cell of plane k: its six faces and rhs
+  double txl, txh, tys, tyn, tzl, tzh, r;
+};
 
 template <bool FIRST>
-__global__ void __launch_bounds__(kPX * kPY, 2) k_sweep2_col(LevelDev L, const double* __restrict__ r,
-                                                             const double* __restrict__ zin,
-                                                             double* __restrict__ zout, int col1, int kchunk) {
-  // first-colour values of the extended tile for 4 planes: slots k&3; one barrier per
-  // plane suffices (the slot written at k+1 was last read before the barrier of k)
-  __shared__ double red[4][kPY][kPX];
+__device__ __forceinline__ void pair_load(PairIn& in, const LevelDev& L, const double* __restrict__ r,
+                                          const double* __restrict__ zin, int64_t c, int j, int k, int par,
+                                          bool hasL, bool hasR, bool hasS, bool hasN) {
+  const int nx = L.nx, ny = L.ny;
+  const int64_t plane = L.plane;
+  const int64_t fx = c + j + (int64_t)ny * k;
+  in.tx0 = __ldg(L.Tx + fx);
+  in.tx1 = __ldg(L.Tx + fx + 1);
+  in.tx2 = __ldg(L.Tx + fx + 2);
+  const int64_t fy = c + (int64_t)nx * k;
+  in.ty = ldg2(L.Ty + fy);
+  in.tyn = ldg2(L.Ty + fy + nx);
+  in.tzu = ldg2(L.Tz + c + plane);
+  in.rr = ldg2(r + c);
+  if (!FIRST) {
+    in.zup = (k + 1 < L.nz) ? ld2(zin + c + plane) : make_double2(0, 0);
+    const bool hx = par ? hasR : hasL;
+    in.xn = hx ? zin[c + (par ? 2 : -1)] : 0.0;
+    in.ys = hasS ? zin[c - nx + par] : 0.0;
+    in.yn = hasN ? zin[c + nx + par] : 0.0;
+  }
+}
+
+template <bool FIRST, int TY>
+__global__ void __launch_bounds__(kPX * TY, 1)
+    k_sweep2_col(LevelDev L, const double* __restrict__ r, const double* __restrict__ zin,
+                  double* __restrict__ zout, int col1, int kchunk) {
+  __shared__ double red[4][TY][kPX];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int m = blockIdx.x * (kPX - 2) + tx - 1;
-  const int j = blockIdx.y * (kPY - 2) + ty - 1;
+  const int j = blockIdx.y * (TY - 2) + ty - 1;
   const int nx = L.nx, ny = L.ny, nz = L.nz;
   const int64_t plane = L.plane;
   const int k0 = blockIdx.z * kchunk;
   const int k1 = min(nz, k0 + kchunk);
   const int i0 = 2 * m;
   const bool valid = m >= 0 && i0 < nx && j >= 0 && j < ny;
-  const bool interior = valid && tx >= 1 && tx <= kPX - 2 && ty >= 1 && ty <= kPY - 2;
+  const bool interior = valid && tx >= 1 && tx <= kPX - 2 && ty >= 1 && ty <= TY - 2;
   const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
   const int kb = max(k0 - 1, 0);
   const int ke = min(k1, nz - 1);
+  const int par0 = (i0 + j + L.z0 + col1) & 1;   // first-colour cell of the pair at even k
   int64_t c = valid ? i0 + (int64_t)nx * (j + (int64_t)ny * kb) : 0;
-  double2 zdn = make_double2(0, 0), zc = make_double2(0, 0);
-  if (valid && !FIRST) {
-    zdn = ld2(zin + c - plane);
-    zc = ld2(zin + c);
+  double2 zdn = make_double2(0, 0), zc = make_double2(0, 0), tzl = make_double2(0, 0);
+  PairIn in;
+  PairSec sec = {0, 0, 0, 0, 0, 0, 0};
+  if (valid) {
+    if (!FIRST) {
+      zdn = kb > 0 ? ld2(zin + c - plane) : make_double2(0, 0);
+      zc = ld2(zin + c);
+    }
+    tzl = ldg2(L.Tz + c);
+    pair_load<FIRST>(in, L, r, zin, c, j, kb, par0 ^ (kb & 1), hasL, hasR, hasS, hasN);
   }
   for (int k = kb; k <= ke + 1; ++k) {
-    // ---- first colour at plane k (k <= ke)
+    PairSec nsec = sec;
     if (k <= ke) {
-      const int par = (i0 + j + k + L.z0 + col1) & 1;
+      // ---- first colour at plane k from the prefetched inputs
+      const int par = par0 ^ (k & 1);
       double v1 = 0.0;
-      double2 zup = make_double2(0, 0);
       if (valid) {
-        const int64_t row = j + (int64_t)ny * k;
-        const int64_t fx = c + row;
-        const double txl = __ldg(L.Tx + fx + par), txh = __ldg(L.Tx + fx + par + 1);
-        const int64_t fy = c + (int64_t)nx * k;
-        const double t2 = __ldg(L.Ty + fy + par), t3 = __ldg(L.Ty + fy + nx + par);
-        const double t4 = __ldg(L.Tz + c + par), t5 = __ldg(L.Tz + c + plane + par);
-        double acc = r[c + par];
+        const double txl = par ? in.tx1 : in.tx0, txh = par ? in.tx2 : in.tx1;
+        const double t2 = sel(in.ty, par), t3 = sel(in.tyn, par);
+        const double t4 = sel(tzl, par), t5 = sel(in.tzu, par);
+        double acc = sel(in.rr, par);
         if (!FIRST) {
-          zup = ld2(zin + c + plane);
-          double xl, xh;
-          if (par) {
-            xl = zc.x;
-            xh = hasR ? zin[c + 2] : 0.0;
-          } else {
-            xl = hasL ? zin[c - 1] : 0.0;
-            xh = zc.y;
-          }
-          const double ys = hasS ? zin[c - nx + par] : 0.0;
-          const double yn = hasN ? zin[c + nx + par] : 0.0;
-          acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * sel(zup, par);
+          const double xl = par ? zc.x : in.xn, xh = par ? in.xn : zc.y;
+          acc += txl * xl + txh * xh + t2 * in.ys + t3 * in.yn + t4 * sel(zdn, par) + t5 * sel(in.zup, par);
         }
         v1 = acc / (txl + txh + t2 + t3 + t4 + t5);
+        const int pb = par ^ 1;
+        nsec.txl = pb ? in.tx1 : in.tx0;
+        nsec.txh = pb ? in.tx2 : in.tx1;
+        nsec.tys = sel(in.ty, pb);
+        nsec.tyn = sel(in.tyn, pb);
+        nsec.tzl = sel(tzl, pb);
+        nsec.tzh = sel(in.tzu, pb);
+        nsec.r = sel(in.rr, pb);
+        tzl = in.tzu;
+        if (!FIRST) {
+          zdn = zc;
+          zc = in.zup;
+        }
       }
       red[k & 3][ty][tx] = v1;
-      if (!FIRST) {
-        zdn = zc;
-        zc = zup;
-      }
+      // ---- issue plane k+1's loads: in flight across the barrier and the second colour
+      if (valid && k + 1 <= ke) pair_load<FIRST>(in, L, r, zin, c + plane, j, k + 1, par ^ 1, hasL, hasR, hasS, hasN);
     }
     __syncthreads();
-    // ---- second colour at plane kp = k - 1 (interior of the tile)
+    // ---- second colour at plane kp = k - 1 (interior of the tile), registers + smem only
     const int kp = k - 1;
     if (kp >= k0 && kp < k1 && interior) {
-      const int pb = (i0 + j + kp + L.z0 + col1 + 1) & 1;
+      const int pb = par0 ^ (kp & 1) ^ 1;
       const int s1 = kp & 3;
       const double own = red[s1][ty][tx];
       const double xnb = pb ? (hasR ? red[s1][ty][tx + 1] : 0.0) : (hasL ? red[s1][ty][tx - 1] : 0.0);
@@ -504,10 +531,14 @@ __global__ void __launch_bounds__(kPX * kPY, 2) k_sweep2_col(LevelDev L, const d
       const double yn = hasN ? red[s1][ty + 1][tx] : 0.0;
       const double zl = (kp > 0) ? red[(kp + 3) & 3][ty][tx] : 0.0;
       const double zh = (kp < nz - 1) ? red[k & 3][ty][tx] : 0.0;
-      const int64_t cp = c - plane;   // c already advanced to plane k
-      *reinterpret_cast<double2*>(zout + cp) = pair_second(L, r, cp, i0, j, kp, pb, own, xnb, ys, yn, zl, zh);
+      const double xl = pb ? own : xnb, xh = pb ? xnb : own;
+      const double acc = sec.r + (sec.txl * xl + sec.txh * xh + sec.tys * ys + sec.tyn * yn + sec.tzl * zl +
+                                  sec.tzh * zh);
+      const double v2 = acc / (sec.txl + sec.txh + sec.tys + sec.tyn + sec.tzl + sec.tzh);
+      *reinterpret_cast<double2*>(zout + c - plane) = pb ? make_double2(own, v2) : make_double2(v2, own);
     }
     if (k <= ke) c += plane;
+    sec = nsec;
   }
 }
 

@@ -344,7 +344,7 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
 
 // Temporally fused pair of half-sweeps (colour col1 then the other) zin -> zout.
 static bool pair_ok(const mss_ctx* ctx, int k) {
-  // Fused pairs beat two single sweeps on large levels only (512^3: 1.50 ms per pair vs
+  // Fused pairs beat two single sweeps on large levels only (512^3: 1.43 ms per pair vs
   // 1.96 ms; 128^3: slower, the per-plane block barrier dominates): default for levels of
   // at least 2^24 cells; MSS_PAIR=0 disables, MSS_PAIR=1 forces every eligible level.
   const char* env = getenv("MSS_PAIR");   // read per call so tests can toggle it
@@ -364,8 +364,8 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
   // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero)
   ProfScope ps(ctx, KC_PAIR, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
   const dim3 grid(bx, by, nch), blk(kPX, kPY);
-  if (first) k_sweep2_col<true><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
-  else k_sweep2_col<false><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
+  if (first) k_sweep2_col<true, kPY><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
+  else k_sweep2_col<false, kPY><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
   ctx->launches++;
   return MSS_OK;
 }
