@@ -57,6 +57,7 @@ struct Level {
   int64_t N = 0, plane = 0;
   double h[3] = {1, 1, 1};
   double *Tx = nullptr, *Ty = nullptr, *Tz = nullptr;
+  double* txp = nullptr;                 // Tx with row pitch nx+2 for the TMA pair kernel (pairtma.cuh)
   // ghosted cell vectors (interior pointers)
   double *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *b = nullptr, *s = nullptr;
   double *p[2] = {nullptr, nullptr};
@@ -135,6 +136,13 @@ struct mss_ctx {
   std::vector<char> tsm_h;
   bool tsm_dirty = true;
   long long* tsm_phase = nullptr;
+  // TMA tensor maps (pairtma.cuh), cached by base pointer and kind (opaque 128-byte images)
+  struct TmapEnt {
+    const void* ptr;
+    int kind;
+    alignas(64) unsigned char img[128];
+  };
+  std::vector<TmapEnt> tmaps;
   // matrix-free level-0 faces from scalar K (colwalk.cuh KFaces)
   bool kfaces = false;
   double* kf_K = nullptr;                  // ghosted copy of K on level 0

@@ -21,6 +21,7 @@
 #include "internal.cuh"
 #include "kernels.cuh"
 #include "colwalk.cuh"
+#include "pairtma.cuh"
 #include "comm.cuh"
 
 using namespace mss;
@@ -342,6 +343,52 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   return MSS_OK;
 }
 
+// ---- TMA tensor maps (driver entry point fetched through the runtime: no -lcuda)
+static bool pair_tma_on() {
+  const char* e = getenv("MSS_PAIR_TMA");   // read per call so tests can toggle it
+  return !e || atoi(e) != 0;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D fp64 tensor (d0 fastest, dense) with box (b0, b1, 1); out-of-bounds elements read 0.
+static bool tmap_get(mss_ctx* ctx, CUtensorMap* out, const void* base, int kind, int64_t d0, int64_t d1, int64_t d2,
+                     int b0, int b1) {
+  for (const auto& e : ctx->tmaps)
+    if (e.ptr == base && e.kind == kind) {
+      memcpy(out, e.img, sizeof(CUtensorMap));
+      return true;
+    }
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)d0 * 8, (cuuint64_t)(d0 * d1) * 8};
+  cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  mss_ctx::TmapEnt e;
+  e.ptr = base;
+  e.kind = kind;
+  memcpy(e.img, out, sizeof(CUtensorMap));
+  ctx->tmaps.push_back(e);
+  return true;
+}
+
 // Temporally fused pair of half-sweeps (colour col1 then the other) zin -> zout.
 static bool pair_ok(const mss_ctx* ctx, int k) {
   // Fused pairs beat two single sweeps on large levels only (512^3: 1.43 ms per pair vs
@@ -363,6 +410,40 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
   nch = (l.nz + kch - 1) / kch;
   // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero)
   ProfScope ps(ctx, KC_PAIR, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
+  if (l.txp && pair_tma_on()) {
+    PairMaps M;
+    if (!tmap_get(ctx, &M.z, zin, 0, l.nx, l.ny, l.nz, kTZW, kTZH) ||
+        !tmap_get(ctx, &M.tx, l.txp, 1, l.nx + 2, l.ny, l.nz, kTXW, kPY) ||
+        !tmap_get(ctx, &M.ty, l.Ty, 2, l.nx, l.ny + 1, l.nz, kTW, kPY + 1) ||
+        !tmap_get(ctx, &M.tz, l.Tz, 3, l.nx, l.ny, l.nz + 1, kTW, kPY) ||
+        !tmap_get(ctx, &M.r, r, 4, l.nx, l.ny, l.nz, kTW, kPY))
+      return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
+    // z chunks per tile column: one CTA per SM, so minimise waves x (planes + 2 halo planes
+    // + ~4 planes of pipeline fill); 512^3 -> 4 chunks of 128 planes, 1332 CTAs = 9 waves
+    const char* nce = getenv("MSS_PAIR_NCH");
+    int tnch = 1;
+    if (nce) {
+      tnch = std::max(1, atoi(nce));
+    } else {
+      const int64_t tiles = (int64_t)bx * by;
+      int64_t best = -1;
+      for (int c = 1; c <= std::min(32, l.nz); ++c) {
+        const int64_t kc = (l.nz + c - 1) / c;
+        const int64_t cost = ((tiles * c + kSMs - 1) / kSMs) * (kc + 6);
+        if (best < 0 || cost < best) {
+          best = cost;
+          tnch = c;
+        }
+      }
+    }
+    const int tkch = (l.nz + tnch - 1) / tnch;
+    tnch = (l.nz + tkch - 1) / tkch;
+    const dim3 tgrid(bx, by, tnch), tblk(kPX, kPY);
+    if (first) k_sweep2t_col<true><<<tgrid, tblk, kPairTmaSmem, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+    else k_sweep2t_col<false><<<tgrid, tblk, kPairTmaSmem, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+    ctx->launches++;
+    return MSS_OK;
+  }
   const dim3 grid(bx, by, nch), blk(kPX, kPY);
   if (first) k_sweep2_col<true, kPY><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
   else k_sweep2_col<false, kPY><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
@@ -1163,6 +1244,22 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(X);
   compute_lift(ctx);
+  // padded Tx copies for the TMA pair kernel on every single-GPU column-walk level
+  if (ndim == 3 && pair_tma_on() && tma_encoder()) {
+    bool any = false;
+    for (int k = 0; k <= ctx->L; ++k) {
+      Level& l = ctx->lv[k];
+      if (!col_ok(ctx, l) || l.dist) continue;
+      const int64_t rows = (int64_t)l.ny * l.nz;
+      TRY(dalloc(ctx, (void**)&l.txp, sizeof(double) * (size_t)(rows * (l.nx + 2))));
+      LAUNCH(k_pad_tx, grid_for(rows * (l.nx + 2)), l.Tx, l.txp, l.nx, rows);
+      any = true;
+    }
+    if (any) {
+      CK(cudaFuncSetAttribute(k_sweep2t_col<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairTmaSmem));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairTmaSmem));
+    }
+  }
   TRY(tail_setup(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
