@@ -66,129 +66,163 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* m, int c
       : "memory");
 }
 
+struct PairCtx {
+  double* smd;
+  double* red;
+  uint64_t* bar;
+  const PairMaps* M;
+  double* zout;
+  int64_t plane;
+  int tx, ty, tid, lx, x0, j0, kb, ke, k0, k1, nz;
+  bool valid, interior;
+};
+
+// plane p -> slot s; its fill number (p - kb) >> 2 gives the mbarrier parity
+template <bool FIRST>
+__device__ __forceinline__ void pair_issue(const PairCtx& C, int p, int s) {
+  double* st = C.smd + s * kStageD;
+  uint64_t* b = &C.bar[s];
+  if (p >= C.nz) {   // only the top z faces exist above the last plane
+    mbar_expect(b, kBytesTz);
+    tma_load3(st + kOffTz, &C.M->tz, C.x0, C.j0, p, b);
+    return;
+  }
+  mbar_expect(b, FIRST ? kBytesT : kBytesT + kBytesZ);
+  if (!FIRST) tma_load3(st + kOffZ, &C.M->z, C.x0 - 2, C.j0 - 1, p, b);
+  tma_load3(st + kOffTx, &C.M->tx, C.x0, C.j0, p, b);
+  tma_load3(st + kOffTy, &C.M->ty, C.x0, C.j0, p, b);
+  tma_load3(st + kOffTz, &C.M->tz, C.x0, C.j0, p, b);
+  tma_load3(st + kOffR, &C.M->r, C.x0, C.j0, p, b);
+}
+
+// One plane step: first colour at k (parity P, slot U), barrier, refill, second colour at
+// k-1 (its colour is then P as well).  U and P are compile-time so slot offsets and the
+// cell-of-pair selects fold away; sin holds plane k-1's second-colour cell, sout gets k's.
+template <bool FIRST, int U, int P>
+__device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, double2& zdn, const PairSec& sin,
+                                          PairSec& sout) {
+  if (k > C.ke + 1) return;   // block-uniform
+  constexpr int U1 = (U + 1) & 3, Um1 = (U + 3) & 3, Um2 = (U + 2) & 3;
+  const int ty = C.ty, tx = C.tx, lx = C.lx;
+  if (k <= C.ke) {
+    mbar_wait(&C.bar[U1], ((k + 1 - C.kb) >> 2) & 1);   // plane k's own slot was awaited a step ago
+    const double* S0 = C.smd + U * kStageD;
+    const double* S1 = C.smd + U1 * kStageD;
+    double v1 = 0.0;
+    if (C.valid) {
+      const double* txr = S0 + kOffTx + ty * kTXW + lx;
+      const double2 t01 = *reinterpret_cast<const double2*>(txr);
+      const double t2x = txr[2];
+      const double2 tys = *reinterpret_cast<const double2*>(S0 + kOffTy + ty * kTW + lx);
+      const double2 tyn = *reinterpret_cast<const double2*>(S0 + kOffTy + (ty + 1) * kTW + lx);
+      const double2 tzl = *reinterpret_cast<const double2*>(S0 + kOffTz + ty * kTW + lx);
+      const double2 tzu = *reinterpret_cast<const double2*>(S1 + kOffTz + ty * kTW + lx);
+      const double2 rr = *reinterpret_cast<const double2*>(S0 + kOffR + ty * kTW + lx);
+      const double txl = P ? t01.y : t01.x, txh = P ? t2x : t01.y;
+      const double t2 = P ? tys.y : tys.x, t3 = P ? tyn.y : tyn.x;
+      const double t4 = P ? tzl.y : tzl.x, t5 = P ? tzu.y : tzu.x;
+      double acc = P ? rr.y : rr.x;
+      if (!FIRST) {
+        const double* Z = S0 + kOffZ + (ty + 1) * kTZW + lx + 2;   // own pair: Z[0], Z[1]
+        const double2 zc = *reinterpret_cast<const double2*>(Z);
+        const double xn = P ? Z[2] : Z[-1];
+        const double ys = Z[-kTZW + P], yn = Z[kTZW + P];
+        const double zu = (k + 1 < C.nz) ? S1[kOffZ + (ty + 1) * kTZW + lx + 2 + P] : 0.0;
+        const double xl = P ? zc.x : xn, xh = P ? xn : zc.y;
+        acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * (P ? zdn.y : zdn.x) + t5 * zu;
+        zdn = zc;
+      }
+      v1 = acc / (txl + txh + t2 + t3 + t4 + t5);
+      sout.txl = P ? t01.x : t01.y;   // the other cell of the pair
+      sout.txh = P ? t01.y : t2x;
+      sout.tys = P ? tys.x : tys.y;
+      sout.tyn = P ? tyn.x : tyn.y;
+      sout.tzl = P ? tzl.x : tzl.y;
+      sout.tzh = P ? tzu.x : tzu.y;
+      sout.r = P ? rr.x : rr.y;
+    }
+    C.red[(U * kPY + ty) * kPX + tx] = v1;
+  }
+  __syncthreads();
+  // plane k's slot is no longer read (its successor and the carried registers hold what
+  // the rest of the walk needs): refill it with plane k+4
+  if (C.tid == 0 && k <= C.ke && k + kTmaStages <= C.ke + 1) pair_issue<FIRST>(C, k + kTmaStages, U);
+  // ---- second colour at plane kp = k - 1 (interior; its cell is P of the pair), from
+  // registers + the shared ring.  Out-of-domain ring pairs stored 0 = no neighbour.
+  const int kp = k - 1;
+  if (kp >= C.k0 && kp < C.k1 && C.interior) {
+    const double* R1 = C.red + (Um1 * kPY + ty) * kPX + tx;
+    const double own = R1[0];
+    const double xnb = P ? R1[1] : R1[-1];
+    const double ys = R1[-kPX], yn = R1[kPX];
+    const double zl = (kp > 0) ? C.red[(Um2 * kPY + ty) * kPX + tx] : 0.0;
+    const double zh = (kp < C.nz - 1) ? C.red[(U * kPY + ty) * kPX + tx] : 0.0;
+    const double xl = P ? own : xnb, xh = P ? xnb : own;
+    const double acc =
+        sin.r + (sin.txl * xl + sin.txh * xh + sin.tys * ys + sin.tyn * yn + sin.tzl * zl + sin.tzh * zh);
+    const double v2 = acc / (sin.txl + sin.txh + sin.tys + sin.tyn + sin.tzl + sin.tzh);
+    *reinterpret_cast<double2*>(C.zout + c - C.plane) = P ? make_double2(own, v2) : make_double2(v2, own);
+  }
+  if (k <= C.ke) c += C.plane;
+}
+
 template <bool FIRST>
 __global__ void __launch_bounds__(kPX * kPY, 1)
     k_sweep2t_col(const __grid_constant__ PairMaps M, LevelDev L, const double* __restrict__ zin,
                   double* __restrict__ zout, int col1, int kchunk) {
   extern __shared__ __align__(128) double smd[];
-  double* red = smd + kTmaStages * kStageD;   // [4][kPY][kPX] first-colour ring
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 4 * kPY * kPX);
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int tid = ty * kPX + tx;
+  PairCtx C;
+  C.smd = smd;
+  C.red = smd + kTmaStages * kStageD;   // [4][kPY][kPX] first-colour ring, slot = (k - kb) & 3
+  C.bar = reinterpret_cast<uint64_t*>(C.red + 4 * kPY * kPX);
+  C.M = &M;
+  C.zout = zout;
+  C.tx = threadIdx.x;
+  C.ty = threadIdx.y;
+  C.tid = C.ty * kPX + C.tx;
+  C.lx = 2 * C.tx;
   const int mb = blockIdx.x * (kPX - 2) - 1;   // first pair of the tile (ring)
-  const int x0 = 2 * mb;                       // first cell of the tile
-  const int j0 = blockIdx.y * (kPY - 2) - 1;   // first row of the tile
-  const int m = mb + tx, j = j0 + ty;
-  const int nx = L.nx, ny = L.ny, nz = L.nz;
-  const int64_t plane = L.plane;
-  const int k0 = blockIdx.z * kchunk;
-  const int k1 = min(nz, k0 + kchunk);
+  C.x0 = 2 * mb;                               // first cell of the tile
+  C.j0 = blockIdx.y * (kPY - 2) - 1;           // first row of the tile
+  const int m = mb + C.tx, j = C.j0 + C.ty;
+  const int nx = L.nx, ny = L.ny;
+  C.nz = L.nz;
+  C.plane = L.plane;
+  C.k0 = blockIdx.z * kchunk;
+  C.k1 = min(C.nz, C.k0 + kchunk);
   const int i0 = 2 * m;
-  const bool valid = m >= 0 && i0 < nx && j >= 0 && j < ny;
-  const bool interior = valid && tx >= 1 && tx <= kPX - 2 && ty >= 1 && ty <= kPY - 2;
-  const int kb = max(k0 - 1, 0);
-  const int ke = min(k1, nz - 1);
-  const int par0 = (i0 + j + L.z0 + col1) & 1;   // first-colour cell of the pair at even k
-
-  // plane p -> slot (p - kb) & 3; its fill number (p - kb) >> 2 gives the mbarrier parity
-  auto issue = [&](int p) {
-    const int s = (p - kb) & (kTmaStages - 1);
-    double* st = smd + s * kStageD;
-    if (p >= nz) {   // only the top z faces exist above the last plane
-      mbar_expect(&bar[s], kBytesTz);
-      tma_load3(st + kOffTz, &M.tz, x0, j0, p, &bar[s]);
-      return;
-    }
-    mbar_expect(&bar[s], FIRST ? kBytesT : kBytesT + kBytesZ);
-    if (!FIRST) tma_load3(st + kOffZ, &M.z, x0 - 2, j0 - 1, p, &bar[s]);
-    tma_load3(st + kOffTx, &M.tx, x0, j0, p, &bar[s]);
-    tma_load3(st + kOffTy, &M.ty, x0, j0, p, &bar[s]);
-    tma_load3(st + kOffTz, &M.tz, x0, j0, p, &bar[s]);
-    tma_load3(st + kOffR, &M.r, x0, j0, p, &bar[s]);
-  };
-  const int np = ke + 2 - kb;   // planes kb .. ke+1 are staged
-  if (tid == 0) {
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(&bar[s], 1);
+  C.valid = m >= 0 && i0 < nx && j >= 0 && j < ny;
+  C.interior = C.valid && C.tx >= 1 && C.tx <= kPX - 2 && C.ty >= 1 && C.ty <= kPY - 2;
+  C.kb = max(C.k0 - 1, 0);
+  C.ke = min(C.k1, C.nz - 1);
+  const int np = C.ke + 2 - C.kb;   // planes kb .. ke+1 are staged
+  if (C.tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&C.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0)
-    for (int q = 0; q < min(np, kTmaStages); ++q) issue(kb + q);
+  if (C.tid == 0)
+    for (int q = 0; q < min(np, kTmaStages); ++q) pair_issue<FIRST>(C, C.kb + q, q);
 
-  const int lx = 2 * tx;
-  int64_t c = valid ? i0 + (int64_t)nx * (j + (int64_t)ny * kb) : 0;
+  int64_t c = C.valid ? i0 + (int64_t)nx * (j + (int64_t)ny * C.kb) : 0;
   double2 zdn = make_double2(0, 0);
-  if (!FIRST && valid && kb > 0) zdn = ld2(zin + c - plane);
-  PairSec sec = {0, 0, 0, 0, 0, 0, 0};
-  mbar_wait(&bar[0], 0);
-  for (int k = kb; k <= ke + 1; ++k) {
-    PairSec nsec = sec;
-    if (k <= ke) {
-      const int s0 = (k - kb) & (kTmaStages - 1), s1 = (k + 1 - kb) & (kTmaStages - 1);
-      mbar_wait(&bar[s1], ((k + 1 - kb) >> 2) & 1);   // plane k's own slot was awaited one plane ago
-      const double* S0 = smd + s0 * kStageD;
-      const double* S1 = smd + s1 * kStageD;
-      double v1 = 0.0;
-      if (valid) {
-        const int par = par0 ^ (k & 1);
-        const double* txr = S0 + kOffTx + ty * kTXW + lx;
-        const double2 t01 = *reinterpret_cast<const double2*>(txr);
-        const double t2x = txr[2];
-        const double2 tys = *reinterpret_cast<const double2*>(S0 + kOffTy + ty * kTW + lx);
-        const double2 tyn = *reinterpret_cast<const double2*>(S0 + kOffTy + (ty + 1) * kTW + lx);
-        const double2 tzl = *reinterpret_cast<const double2*>(S0 + kOffTz + ty * kTW + lx);
-        const double2 tzu = *reinterpret_cast<const double2*>(S1 + kOffTz + ty * kTW + lx);
-        const double2 rr = *reinterpret_cast<const double2*>(S0 + kOffR + ty * kTW + lx);
-        const double txl = par ? t01.y : t01.x, txh = par ? t2x : t01.y;
-        const double t2 = sel(tys, par), t3 = sel(tyn, par), t4 = sel(tzl, par), t5 = sel(tzu, par);
-        double acc = sel(rr, par);
-        if (!FIRST) {
-          const double* Z = S0 + kOffZ + (ty + 1) * kTZW + lx + 2;   // own pair: Z[0], Z[1]
-          const double2 zc = *reinterpret_cast<const double2*>(Z);
-          const double xn = par ? Z[2] : Z[-1];
-          const double ys = Z[-kTZW + par], yn = Z[kTZW + par];
-          const double2 zup = (k + 1 < nz)
-                                  ? *reinterpret_cast<const double2*>(S1 + kOffZ + (ty + 1) * kTZW + lx + 2)
-                                  : make_double2(0, 0);
-          const double xl = par ? zc.x : xn, xh = par ? xn : zc.y;
-          acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * sel(zup, par);
-          zdn = zc;
-        }
-        v1 = acc / (txl + txh + t2 + t3 + t4 + t5);
-        const int pb = par ^ 1;
-        nsec.txl = pb ? t01.y : t01.x;
-        nsec.txh = pb ? t2x : t01.y;
-        nsec.tys = sel(tys, pb);
-        nsec.tyn = sel(tyn, pb);
-        nsec.tzl = sel(tzl, pb);
-        nsec.tzh = sel(tzu, pb);
-        nsec.r = sel(rr, pb);
-      }
-      red[((k & 3) * kPY + ty) * kPX + tx] = v1;
+  if (!FIRST && C.valid && C.kb > 0) zdn = ld2(zin + c - C.plane);
+  // first-colour parity at the start of every 4-plane group (warp-uniform: a warp is a row)
+  const int pA = (i0 + j + L.z0 + col1 + C.kb) & 1;
+  PairSec sa = {0, 0, 0, 0, 0, 0, 0}, sb = sa;
+  mbar_wait(&C.bar[0], 0);
+  for (int k = C.kb; k <= C.ke + 1; k += 4) {
+    if (pA) {
+      pair_step<FIRST, 0, 1>(C, k, c, zdn, sa, sb);
+      pair_step<FIRST, 1, 0>(C, k + 1, c, zdn, sb, sa);
+      pair_step<FIRST, 2, 1>(C, k + 2, c, zdn, sa, sb);
+      pair_step<FIRST, 3, 0>(C, k + 3, c, zdn, sb, sa);
+    } else {
+      pair_step<FIRST, 0, 0>(C, k, c, zdn, sa, sb);
+      pair_step<FIRST, 1, 1>(C, k + 1, c, zdn, sb, sa);
+      pair_step<FIRST, 2, 0>(C, k + 2, c, zdn, sa, sb);
+      pair_step<FIRST, 3, 1>(C, k + 3, c, zdn, sb, sa);
     }
-    __syncthreads();
-    // plane k's slot is no longer read (its successor and the carried registers hold what
-    // the rest of the walk needs): refill it with plane k+4
-    if (tid == 0 && k <= ke && k + kTmaStages <= ke + 1) issue(k + kTmaStages);
-    // ---- second colour at plane kp = k - 1 (interior), registers + shared ring only.
-    // Out-of-domain ring pairs stored 0, which is the missing neighbour's contribution.
-    const int kp = k - 1;
-    if (kp >= k0 && kp < k1 && interior) {
-      const int pb = par0 ^ (kp & 1) ^ 1;
-      const double* R1 = red + ((kp & 3) * kPY + ty) * kPX + tx;
-      const double own = R1[0];
-      const double xnb = pb ? R1[1] : R1[-1];
-      const double ys = R1[-kPX], yn = R1[kPX];
-      const double zl = (kp > 0) ? red[(((kp + 3) & 3) * kPY + ty) * kPX + tx] : 0.0;
-      const double zh = (kp < nz - 1) ? red[((k & 3) * kPY + ty) * kPX + tx] : 0.0;
-      const double xl = pb ? own : xnb, xh = pb ? xnb : own;
-      const double acc = sec.r + (sec.txl * xl + sec.txh * xh + sec.tys * ys + sec.tyn * yn + sec.tzl * zl +
-                                  sec.tzh * zh);
-      const double v2 = acc / (sec.txl + sec.txh + sec.tys + sec.tyn + sec.tzl + sec.tzh);
-      *reinterpret_cast<double2*>(zout + c - plane) = pb ? make_double2(own, v2) : make_double2(v2, own);
-    }
-    if (k <= ke) c += plane;
-    sec = nsec;
   }
 }
 
