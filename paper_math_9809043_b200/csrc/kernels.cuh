@@ -675,6 +675,40 @@ __global__ void k_prolong_black(LevelDev L, int ncx, int ncy, int ncz, int s, in
     prolong_black_item<NDIM>(L, hx, ncx, ncy, ncz, s, kind, y, z, (uint32_t)t, zc0);
 }
 
+// one 1-D extension weight: fine index -> (I0, w0) + (I1, w1), w1 = 0 when I1 == I0
+// (host-built tables, same rule as interp_w; uploaded once per level and axis)
+struct W1 {
+  int I0, I1;
+  double w0, w1;
+};
+
+// Restriction along axis 1 or 2 of a single-GPU level from the weight table of that axis:
+// one CTA per output row (q1, q2), threads along the contiguous axis 0, no index division.
+// Same taps, weights and summation order as restrict_item.
+__global__ void __launch_bounds__(128) k_restrict_axis_w(const double* __restrict__ in, double* __restrict__ out,
+                                                         int n0, int n1, int axis, int nf, int nc,
+                                                         const W1* __restrict__ wt) {
+  const int q1 = blockIdx.x, q2 = blockIdx.y;
+  const int o1 = (axis == 1) ? nc : n1;
+  const int I = (axis == 1) ? q1 : q2;
+  int lo, hi;
+  fine_window(I, (double)nf / (double)nc, nf, lo, hi);
+  const int64_t sax = (axis == 1) ? (int64_t)n0 : (int64_t)n0 * n1;
+  const int64_t ibase = (axis == 1) ? (int64_t)n0 * n1 * q2 : (int64_t)n0 * q1;
+  const int64_t obase = (int64_t)n0 * (q1 + (int64_t)o1 * q2);
+  for (int q0 = threadIdx.x; q0 < n0; q0 += blockDim.x) {
+    double acc = 0.0;
+    for (int i = lo; i < hi; ++i) {
+      const W1 e = wt[i];
+      double w = 0.0;
+      if (e.I0 == I) w += e.w0;
+      if (e.I1 == I && e.I1 != e.I0) w += e.w1;
+      if (w != 0.0) acc += w * in[ibase + (int64_t)i * sax + q0];
+    }
+    out[obase + q0] = acc;
+  }
+}
+
 __global__ void k_restrict_axis(const double* __restrict__ in, double* __restrict__ out,
                                 int n0, int n1, int n2, int axis, int nc, int s, int kind,
                                 int in_off, int nf_g, int out_off, int nc_g) {

@@ -528,7 +528,14 @@ static int op_restrict_yz(mss_ctx* ctx, int k, double* coarse) {
     const double rb = (ctx->ndim == 3) ? 8.0 * (2.0 * c.nx * f.ny * f.nz + 2.0 * c.nx * c.ny * f.nz + c.N)
                                        : 8.0 * ((double)c.nx * f.ny + c.N);
     ProfScope ps(ctx, KC_RESTRICT, k, rb);
-    if (ctx->ndim == 3) {
+    if (!fd && ctx->ndim == 3 && f.w[1] && f.w[2] && f.nz <= 65535 && c.nz <= 65535) {
+      // y then z from the level's weight tables (one CTA per output row)
+      k_restrict_axis_w<<<dim3(c.ny, f.nz), 128, 0, ctx->stream>>>(f.t1, f.t2, c.nx, f.ny, 1, f.ny, c.ny,
+                                                                    reinterpret_cast<const W1*>(f.w[1]));
+      k_restrict_axis_w<<<dim3(c.ny, c.nz), 128, 0, ctx->stream>>>(f.t2, coarse, c.nx, c.ny, 2, f.nz, c.nz,
+                                                                    reinterpret_cast<const W1*>(f.w[2]));
+      ctx->launches += 2;
+    } else if (ctx->ndim == 3) {
       LAUNCH(k_restrict_axis, grid_for((int64_t)c.nx * c.ny * f.nz), f.t1, f.t2, c.nx, f.ny, f.nz, 1, c.ny, S, kind,
              0, 0, 0, 0);
       if (fd) TRY(ctx->comm->halo(ctx->stream, f.t2, cplane, f.nz, 2));

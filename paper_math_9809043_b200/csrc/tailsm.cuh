@@ -41,12 +41,6 @@ struct FDiv {
   __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
 };
 
-// one 1-D extension weight: fine index -> (I0, w0) + (I1, w1), w1 = 0 when I1 == I0
-struct W1 {
-  int I0, I1;
-  double w0, w1;
-};
-
 struct TsLevel {
   int nx, ny, nz;      // dims of the level
   int P;               // cells per outer slice: nx*ny (3-D) | nx (2-D)

@@ -21,10 +21,13 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tail", type=int, default=65536)
 ap.add_argument("--prof-level", type=int, default=8)
 ap.add_argument("--params", default="{}")
+ap.add_argument("--stream", action="store_true", help="run on a non-default stream")
 args = ap.parse_args()
 build.build()
 from paper_math_9809043_b200.mss import Solver  # noqa: E402
 
+if args.stream:
+    torch.cuda.set_stream(torch.cuda.Stream())
 w = make_workload(args.config, n=args.n)
 K = torch.from_numpy(w.K).cuda()
 f = torch.from_numpy(w.f.ravel()).cuda()
