@@ -459,3 +459,48 @@ def test_fused_pair_sweeps_match_single_sweeps(torch_mod, name, mk, monkeypatch)
         col = (1 + h) % 2
         O.halfsweep(lv.T, lv.diag, r, zo, col, lv.red if col == 0 else lv.black)
     assert rel(zg, zo) <= KTOL
+
+
+def _all_dirichlet(ndim):
+    from workloads.configs import bc_table, DIRICHLET
+    return bc_table(ndim, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0), "y-": (DIRICHLET, 0.5),
+                           "y+": (DIRICHLET, 0.25), "z-": (DIRICHLET, 2.0), "z+": (DIRICHLET, -1.0)})
+
+
+PAIR_EDGE = [
+    # (n, bc): partial last tiles in x (hx % 30) and y (ny % 14), short z walks (fewer
+    # planes than the 4-stage ring), Dirichlet faces on every side incl. the z-top faces
+    ("x72_y32_z16", (72, 32, 16), None),
+    ("x256_y20_z8", (256, 20, 8), "dirichlet"),
+    ("x64_y60_z12", (64, 60, 12), "dirichlet"),
+    ("x64_y16_z40", (64, 16, 40), None),
+]
+
+
+@pytest.mark.parametrize("name,n,bc", PAIR_EDGE, ids=[c[0] for c in PAIR_EDGE])
+@pytest.mark.parametrize("tma", ["1", "0"])
+def test_pair_sweep_edges(torch_mod, name, n, bc, tma, monkeypatch):
+    """Forced fused pairs (TMA-fed or register-pipelined) on ragged level-0 shapes against
+    the oracle's half-sweep sequence: 9 from zero and 4 from a nonzero z."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    monkeypatch.setenv("MSS_PAIR", "1")
+    monkeypatch.setenv("MSS_PAIR_TMA", tma)
+    w = random_problem(3, n, seed=11, bc=_all_dirichlet(3) if bc else None)
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=1)
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=1)
+    lv = o.levels[0]
+    rng = np.random.default_rng(5)
+    r = rng.standard_normal(lv.shape)
+    zg = s.smooth(0, cu(torch, r), None, 9, 0).cpu().numpy()
+    zo = np.zeros(lv.shape)
+    o.smooth(0, r, zo, 9)
+    assert rel(zg, zo) <= KTOL
+    for first in (0, 1):
+        z0 = rng.standard_normal(lv.shape)
+        zg = s.smooth(0, cu(torch, r), cu(torch, z0), 4, first).cpu().numpy()
+        zo = z0.copy()
+        for h in range(4):
+            col = (first + h) % 2
+            O.halfsweep(lv.T, lv.diag, r, zo, col, lv.red if col == 0 else lv.black)
+        assert rel(zg, zo) <= KTOL
