@@ -411,25 +411,31 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
   // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero)
   ProfScope ps(ctx, KC_PAIR, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
   if (l.txp && pair_tma_on()) {
+    // tile rows: 16 (one 190 KB CTA per SM) on big levels, 8 (two 80 KB CTAs per SM) below
+    const char* tye = getenv("MSS_PAIR_TY");
+    const bool big = tye ? atoi(tye) >= 16 : l.N >= ((int64_t)1 << 24);
+    const int TY = big ? PairBig::TY : PairSmall::TY;
+    const int occ = big ? PairBig::MINB : PairSmall::MINB;
     PairMaps M;
-    if (!tmap_get(ctx, &M.z, zin, 0, l.nx, l.ny, l.nz, kTZW, kTZH) ||
-        !tmap_get(ctx, &M.tx, l.txp, 1, l.nx + 2, l.ny, l.nz, kTXW, kPY) ||
-        !tmap_get(ctx, &M.ty, l.Ty, 2, l.nx, l.ny + 1, l.nz, kTW, kPY + 1) ||
-        !tmap_get(ctx, &M.tz, l.Tz, 3, l.nx, l.ny, l.nz + 1, kTW, kPY) ||
-        !tmap_get(ctx, &M.r, r, 4, l.nx, l.ny, l.nz, kTW, kPY))
+    if (!tmap_get(ctx, &M.z, zin, 0 + 8 * big, l.nx, l.ny, l.nz, 2 * kPX + 4, TY + 2) ||
+        !tmap_get(ctx, &M.tx, l.txp, 1 + 8 * big, l.nx + 2, l.ny, l.nz, 2 * kPX + 2, TY) ||
+        !tmap_get(ctx, &M.ty, l.Ty, 2 + 8 * big, l.nx, l.ny + 1, l.nz, 2 * kPX, TY + 1) ||
+        !tmap_get(ctx, &M.tz, l.Tz, 3 + 8 * big, l.nx, l.ny, l.nz + 1, 2 * kPX, TY) ||
+        !tmap_get(ctx, &M.r, r, 4 + 8 * big, l.nx, l.ny, l.nz, 2 * kPX, TY))
       return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
-    // z chunks per tile column: one CTA per SM, so minimise waves x (planes + 2 halo planes
-    // + ~4 planes of pipeline fill); 512^3 -> 4 chunks of 128 planes, 1332 CTAs = 9 waves
+    const int tby = (l.ny + TY - 3) / (TY - 2);
+    // z chunks per tile column: minimise waves x (planes + 2 halo planes + ~4 planes of
+    // pipeline fill); 512^3 -> 4 chunks of 128 planes, 1332 CTAs = 9 waves of 148
     const char* nce = getenv("MSS_PAIR_NCH");
     int tnch = 1;
     if (nce) {
       tnch = std::max(1, atoi(nce));
     } else {
-      const int64_t tiles = (int64_t)bx * by;
+      const int64_t tiles = (int64_t)bx * tby, slots = (int64_t)kSMs * occ;
       int64_t best = -1;
       for (int c = 1; c <= std::min(32, l.nz); ++c) {
         const int64_t kc = (l.nz + c - 1) / c;
-        const int64_t cost = ((tiles * c + kSMs - 1) / kSMs) * (kc + 6);
+        const int64_t cost = ((tiles * c + slots - 1) / slots) * (kc + 6);
         if (best < 0 || cost < best) {
           best = cost;
           tnch = c;
@@ -438,9 +444,14 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     }
     const int tkch = (l.nz + tnch - 1) / tnch;
     tnch = (l.nz + tkch - 1) / tkch;
-    const dim3 tgrid(bx, by, tnch), tblk(kPX, kPY);
-    if (first) k_sweep2t_col<true><<<tgrid, tblk, kPairTmaSmem, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
-    else k_sweep2t_col<false><<<tgrid, tblk, kPairTmaSmem, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+    const dim3 tgrid(bx, tby, tnch), tblk(kPX, TY);
+    if (big) {
+      if (first) k_sweep2t_col<true, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+      else k_sweep2t_col<false, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+    } else {
+      if (first) k_sweep2t_col<true, PairSmall><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+      else k_sweep2t_col<false, PairSmall><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+    }
     ctx->launches++;
     return MSS_OK;
   }
@@ -1263,8 +1274,10 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       any = true;
     }
     if (any) {
-      CK(cudaFuncSetAttribute(k_sweep2t_col<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairTmaSmem));
-      CK(cudaFuncSetAttribute(k_sweep2t_col<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairTmaSmem));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<true, PairBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairBig::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairBig::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<true, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
     }
   }
   TRY(tail_setup(ctx));

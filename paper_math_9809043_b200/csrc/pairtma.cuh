@@ -21,22 +21,33 @@
 
 namespace mss {
 
-constexpr int kTmaStages = 4;
-constexpr int kTZW = 2 * kPX + 4;    // z tile width: cells x0-2 .. x0+2kPX+1       (68)
-constexpr int kTZH = kPY + 2;        // z tile rows: j0-1 .. j0+kPY                   (18)
-constexpr int kTXW = 2 * kPX + 2;    // Tx tile width: faces x0 .. x0+2kPX+1         (66)
-constexpr int kTW = 2 * kPX;         // Ty / Tz / r tile width: cells x0 .. x0+2kPX-1 (64)
-__host__ __device__ constexpr int rnd16(int v) { return (v + 15) & ~15; }   // 128-byte parts
-constexpr int kOffZ = 0;
-constexpr int kOffTx = kOffZ + rnd16(kTZW * kTZH);
-constexpr int kOffTy = kOffTx + rnd16(kTXW * kPY);
-constexpr int kOffTz = kOffTy + rnd16(kTW * (kPY + 1));
-constexpr int kOffR = kOffTz + rnd16(kTW * kPY);
-constexpr int kStageD = kOffR + rnd16(kTW * kPY);
-constexpr uint32_t kBytesZ = 8u * kTZW * kTZH;
-constexpr uint32_t kBytesTz = 8u * kTW * kPY;
-constexpr uint32_t kBytesT = 8u * (kTXW * kPY + kTW * (kPY + 1) + kTW * kPY + kTW * kPY);
-constexpr size_t kPairTmaSmem = sizeof(double) * ((size_t)kTmaStages * kStageD + 4 * kPY * kPX) + 64;
+// Tile geometry: TY rows of threads (incl. the ring), NS TMA stages.  The z-walk is unrolled
+// by UN planes (a multiple of NS and of 2) so ring slots and the colour are compile-time; the
+// first-colour ring has UN >= 4 slots (the second colour reads three planes while the next
+// plane's first colour is written).
+template <int TY_, int NS_>
+struct PairGeo {
+  static constexpr int TY = TY_, NS = NS_;
+  static constexpr int UN = (NS == 4) ? 4 : 6;
+  static constexpr int RN = UN;
+  static constexpr int ZW = 2 * kPX + 4;   // z tile width: cells x0-2 .. x0+2kPX+1       (68)
+  static constexpr int ZH = TY + 2;        // z tile rows: j0-1 .. j0+TY
+  static constexpr int XW = 2 * kPX + 2;   // Tx tile width: faces x0 .. x0+2kPX+1         (66)
+  static constexpr int W = 2 * kPX;        // Ty / Tz / r tile width: cells x0 .. x0+2kPX-1 (64)
+  static constexpr int oZ = 0;
+  static constexpr int oTx = oZ + ((ZW * ZH + 15) & ~15);   // 128-byte aligned parts
+  static constexpr int oTy = oTx + ((XW * TY + 15) & ~15);
+  static constexpr int oTz = oTy + ((W * (TY + 1) + 15) & ~15);
+  static constexpr int oR = oTz + ((W * TY + 15) & ~15);
+  static constexpr int SD = oR + ((W * TY + 15) & ~15);     // doubles per stage
+  static constexpr uint32_t BZ = 8u * ZW * ZH;
+  static constexpr uint32_t BTz = 8u * W * TY;
+  static constexpr uint32_t BT = 8u * (XW * TY + W * (TY + 1) + W * TY + W * TY);
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)NS * SD + (size_t)RN * TY * kPX) + 64;
+  static constexpr int MINB = (TY >= 16) ? 1 : 2;   // CTAs per SM the shared memory allows
+};
+using PairBig = PairGeo<16, 4>;     // 512 threads, 190 KB: 1 CTA / SM (level 0 of C5)
+using PairSmall = PairGeo<8, 3>;    // 256 threads, 80 KB: 2 CTAs / SM (smaller levels)
 
 struct PairMaps {
   CUtensorMap z, tx, ty, tz, r;
@@ -78,56 +89,58 @@ struct PairCtx {
 };
 
 // plane p -> slot s; its fill number (p - kb) >> 2 gives the mbarrier parity
-template <bool FIRST>
+template <bool FIRST, class G>
 __device__ __forceinline__ void pair_issue(const PairCtx& C, int p, int s) {
-  double* st = C.smd + s * kStageD;
+  double* st = C.smd + s * G::SD;
   uint64_t* b = &C.bar[s];
   if (p >= C.nz) {   // only the top z faces exist above the last plane
-    mbar_expect(b, kBytesTz);
-    tma_load3(st + kOffTz, &C.M->tz, C.x0, C.j0, p, b);
+    mbar_expect(b, G::BTz);
+    tma_load3(st + G::oTz, &C.M->tz, C.x0, C.j0, p, b);
     return;
   }
-  mbar_expect(b, FIRST ? kBytesT : kBytesT + kBytesZ);
-  if (!FIRST) tma_load3(st + kOffZ, &C.M->z, C.x0 - 2, C.j0 - 1, p, b);
-  tma_load3(st + kOffTx, &C.M->tx, C.x0, C.j0, p, b);
-  tma_load3(st + kOffTy, &C.M->ty, C.x0, C.j0, p, b);
-  tma_load3(st + kOffTz, &C.M->tz, C.x0, C.j0, p, b);
-  tma_load3(st + kOffR, &C.M->r, C.x0, C.j0, p, b);
+  mbar_expect(b, FIRST ? G::BT : G::BT + G::BZ);
+  if (!FIRST) tma_load3(st + G::oZ, &C.M->z, C.x0 - 2, C.j0 - 1, p, b);
+  tma_load3(st + G::oTx, &C.M->tx, C.x0, C.j0, p, b);
+  tma_load3(st + G::oTy, &C.M->ty, C.x0, C.j0, p, b);
+  tma_load3(st + G::oTz, &C.M->tz, C.x0, C.j0, p, b);
+  tma_load3(st + G::oR, &C.M->r, C.x0, C.j0, p, b);
 }
 
-// One plane step: first colour at k (parity P, slot U), barrier, refill, second colour at
-// k-1 (its colour is then P as well).  U and P are compile-time so slot offsets and the
-// cell-of-pair selects fold away; sin holds plane k-1's second-colour cell, sout gets k's.
-template <bool FIRST, int U, int P>
+// One plane step u of the unrolled walk: first colour at k (parity P), barrier, refill,
+// second colour at k-1 (its colour is then P as well).  Stage slot u % NS and ring slot u are
+// compile-time; sin holds plane k-1's second-colour cell, sout gets plane k's.
+template <bool FIRST, class G, int U, int P>
 __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, double2& zdn, const PairSec& sin,
                                           PairSec& sout) {
   if (k > C.ke + 1) return;   // block-uniform
-  constexpr int U1 = (U + 1) & 3, Um1 = (U + 3) & 3, Um2 = (U + 2) & 3;
+  constexpr int S0i = U % G::NS, S1i = (U + 1) % G::NS;
+  constexpr int R0 = U, Rm1 = (U + G::RN - 1) % G::RN, Rm2 = (U + G::RN - 2) % G::RN;
+  constexpr int ZW = G::ZW, W = G::W, XW = G::XW;
   const int ty = C.ty, tx = C.tx, lx = C.lx;
   if (k <= C.ke) {
-    mbar_wait(&C.bar[U1], ((k + 1 - C.kb) >> 2) & 1);   // plane k's own slot was awaited a step ago
-    const double* S0 = C.smd + U * kStageD;
-    const double* S1 = C.smd + U1 * kStageD;
+    mbar_wait(&C.bar[S1i], ((k + 1 - C.kb) / G::NS) & 1);   // plane k's own stage was awaited a step ago
+    const double* S0 = C.smd + S0i * G::SD;
+    const double* S1 = C.smd + S1i * G::SD;
     double v1 = 0.0;
     if (C.valid) {
-      const double* txr = S0 + kOffTx + ty * kTXW + lx;
+      const double* txr = S0 + G::oTx + ty * XW + lx;
       const double2 t01 = *reinterpret_cast<const double2*>(txr);
       const double t2x = txr[2];
-      const double2 tys = *reinterpret_cast<const double2*>(S0 + kOffTy + ty * kTW + lx);
-      const double2 tyn = *reinterpret_cast<const double2*>(S0 + kOffTy + (ty + 1) * kTW + lx);
-      const double2 tzl = *reinterpret_cast<const double2*>(S0 + kOffTz + ty * kTW + lx);
-      const double2 tzu = *reinterpret_cast<const double2*>(S1 + kOffTz + ty * kTW + lx);
-      const double2 rr = *reinterpret_cast<const double2*>(S0 + kOffR + ty * kTW + lx);
+      const double2 tys = *reinterpret_cast<const double2*>(S0 + G::oTy + ty * W + lx);
+      const double2 tyn = *reinterpret_cast<const double2*>(S0 + G::oTy + (ty + 1) * W + lx);
+      const double2 tzl = *reinterpret_cast<const double2*>(S0 + G::oTz + ty * W + lx);
+      const double2 tzu = *reinterpret_cast<const double2*>(S1 + G::oTz + ty * W + lx);
+      const double2 rr = *reinterpret_cast<const double2*>(S0 + G::oR + ty * W + lx);
       const double txl = P ? t01.y : t01.x, txh = P ? t2x : t01.y;
       const double t2 = P ? tys.y : tys.x, t3 = P ? tyn.y : tyn.x;
       const double t4 = P ? tzl.y : tzl.x, t5 = P ? tzu.y : tzu.x;
       double acc = P ? rr.y : rr.x;
       if (!FIRST) {
-        const double* Z = S0 + kOffZ + (ty + 1) * kTZW + lx + 2;   // own pair: Z[0], Z[1]
+        const double* Z = S0 + G::oZ + (ty + 1) * ZW + lx + 2;   // own pair: Z[0], Z[1]
         const double2 zc = *reinterpret_cast<const double2*>(Z);
         const double xn = P ? Z[2] : Z[-1];
-        const double ys = Z[-kTZW + P], yn = Z[kTZW + P];
-        const double zu = (k + 1 < C.nz) ? S1[kOffZ + (ty + 1) * kTZW + lx + 2 + P] : 0.0;
+        const double ys = Z[-ZW + P], yn = Z[ZW + P];
+        const double zu = (k + 1 < C.nz) ? S1[G::oZ + (ty + 1) * ZW + lx + 2 + P] : 0.0;
         const double xl = P ? zc.x : xn, xh = P ? xn : zc.y;
         acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * (P ? zdn.y : zdn.x) + t5 * zu;
         zdn = zc;
@@ -141,22 +154,22 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
       sout.tzh = P ? tzu.x : tzu.y;
       sout.r = P ? rr.x : rr.y;
     }
-    C.red[(U * kPY + ty) * kPX + tx] = v1;
+    C.red[(R0 * G::TY + ty) * kPX + tx] = v1;
   }
   __syncthreads();
-  // plane k's slot is no longer read (its successor and the carried registers hold what
-  // the rest of the walk needs): refill it with plane k+4
-  if (C.tid == 0 && k <= C.ke && k + kTmaStages <= C.ke + 1) pair_issue<FIRST>(C, k + kTmaStages, U);
+  // plane k's stage is no longer read (its successor and the carried registers hold what
+  // the rest of the walk needs): refill it with plane k+NS
+  if (C.tid == 0 && k <= C.ke && k + G::NS <= C.ke + 1) pair_issue<FIRST, G>(C, k + G::NS, S0i);
   // ---- second colour at plane kp = k - 1 (interior; its cell is P of the pair), from
   // registers + the shared ring.  Out-of-domain ring pairs stored 0 = no neighbour.
   const int kp = k - 1;
   if (kp >= C.k0 && kp < C.k1 && C.interior) {
-    const double* R1 = C.red + (Um1 * kPY + ty) * kPX + tx;
+    const double* R1 = C.red + (Rm1 * G::TY + ty) * kPX + tx;
     const double own = R1[0];
     const double xnb = P ? R1[1] : R1[-1];
     const double ys = R1[-kPX], yn = R1[kPX];
-    const double zl = (kp > 0) ? C.red[(Um2 * kPY + ty) * kPX + tx] : 0.0;
-    const double zh = (kp < C.nz - 1) ? C.red[(U * kPY + ty) * kPX + tx] : 0.0;
+    const double zl = (kp > 0) ? C.red[(Rm2 * G::TY + ty) * kPX + tx] : 0.0;
+    const double zh = (kp < C.nz - 1) ? C.red[(R0 * G::TY + ty) * kPX + tx] : 0.0;
     const double xl = P ? own : xnb, xh = P ? xnb : own;
     const double acc =
         sin.r + (sin.txl * xl + sin.txh * xh + sin.tys * ys + sin.tyn * yn + sin.tzl * zl + sin.tzh * zh);
@@ -166,15 +179,26 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
   if (k <= C.ke) c += C.plane;
 }
 
-template <bool FIRST>
-__global__ void __launch_bounds__(kPX * kPY, 1)
+// UN consecutive plane steps starting at parity p0 (sa / sb ping-pong the second-colour state)
+template <bool FIRST, class G, int P0, int U = 0>
+__device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, double2& zdn, PairSec& sa,
+                                           PairSec& sb) {
+  if constexpr (U < G::UN) {
+    if constexpr ((U & 1) == 0) pair_step<FIRST, G, U, P0 ^ (U & 1)>(C, k + U, c, zdn, sa, sb);
+    else pair_step<FIRST, G, U, P0 ^ (U & 1)>(C, k + U, c, zdn, sb, sa);
+    pair_group<FIRST, G, P0, U + 1>(C, k, c, zdn, sa, sb);
+  }
+}
+
+template <bool FIRST, class G>
+__global__ void __launch_bounds__(kPX * G::TY, G::MINB)
     k_sweep2t_col(const __grid_constant__ PairMaps M, LevelDev L, const double* __restrict__ zin,
                   double* __restrict__ zout, int col1, int kchunk) {
   extern __shared__ __align__(128) double smd[];
   PairCtx C;
   C.smd = smd;
-  C.red = smd + kTmaStages * kStageD;   // [4][kPY][kPX] first-colour ring, slot = (k - kb) & 3
-  C.bar = reinterpret_cast<uint64_t*>(C.red + 4 * kPY * kPX);
+  C.red = smd + G::NS * G::SD;   // [RN][TY][kPX] first-colour ring, slot = (k - kb) % RN
+  C.bar = reinterpret_cast<uint64_t*>(C.red + G::RN * G::TY * kPX);
   C.M = &M;
   C.zout = zout;
   C.tx = threadIdx.x;
@@ -183,7 +207,7 @@ __global__ void __launch_bounds__(kPX * kPY, 1)
   C.lx = 2 * C.tx;
   const int mb = blockIdx.x * (kPX - 2) - 1;   // first pair of the tile (ring)
   C.x0 = 2 * mb;                               // first cell of the tile
-  C.j0 = blockIdx.y * (kPY - 2) - 1;           // first row of the tile
+  C.j0 = blockIdx.y * (G::TY - 2) - 1;         // first row of the tile
   const int m = mb + C.tx, j = C.j0 + C.ty;
   const int nx = L.nx, ny = L.ny;
   C.nz = L.nz;
@@ -192,37 +216,28 @@ __global__ void __launch_bounds__(kPX * kPY, 1)
   C.k1 = min(C.nz, C.k0 + kchunk);
   const int i0 = 2 * m;
   C.valid = m >= 0 && i0 < nx && j >= 0 && j < ny;
-  C.interior = C.valid && C.tx >= 1 && C.tx <= kPX - 2 && C.ty >= 1 && C.ty <= kPY - 2;
+  C.interior = C.valid && C.tx >= 1 && C.tx <= kPX - 2 && C.ty >= 1 && C.ty <= G::TY - 2;
   C.kb = max(C.k0 - 1, 0);
   C.ke = min(C.k1, C.nz - 1);
   const int np = C.ke + 2 - C.kb;   // planes kb .. ke+1 are staged
   if (C.tid == 0) {
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(&C.bar[s], 1);
+    for (int s = 0; s < G::NS; ++s) mbar_init(&C.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (C.tid == 0)
-    for (int q = 0; q < min(np, kTmaStages); ++q) pair_issue<FIRST>(C, C.kb + q, q);
+    for (int q = 0; q < min(np, G::NS); ++q) pair_issue<FIRST, G>(C, C.kb + q, q);
 
   int64_t c = C.valid ? i0 + (int64_t)nx * (j + (int64_t)ny * C.kb) : 0;
   double2 zdn = make_double2(0, 0);
   if (!FIRST && C.valid && C.kb > 0) zdn = ld2(zin + c - C.plane);
-  // first-colour parity at the start of every 4-plane group (warp-uniform: a warp is a row)
+  // first-colour parity at the start of every group (warp-uniform: a warp is a row)
   const int pA = (i0 + j + L.z0 + col1 + C.kb) & 1;
   PairSec sa = {0, 0, 0, 0, 0, 0, 0}, sb = sa;
   mbar_wait(&C.bar[0], 0);
-  for (int k = C.kb; k <= C.ke + 1; k += 4) {
-    if (pA) {
-      pair_step<FIRST, 0, 1>(C, k, c, zdn, sa, sb);
-      pair_step<FIRST, 1, 0>(C, k + 1, c, zdn, sb, sa);
-      pair_step<FIRST, 2, 1>(C, k + 2, c, zdn, sa, sb);
-      pair_step<FIRST, 3, 0>(C, k + 3, c, zdn, sb, sa);
-    } else {
-      pair_step<FIRST, 0, 0>(C, k, c, zdn, sa, sb);
-      pair_step<FIRST, 1, 1>(C, k + 1, c, zdn, sb, sa);
-      pair_step<FIRST, 2, 0>(C, k + 2, c, zdn, sa, sb);
-      pair_step<FIRST, 3, 1>(C, k + 3, c, zdn, sb, sa);
-    }
+  for (int k = C.kb; k <= C.ke + 1; k += G::UN) {
+    if (pA) pair_group<FIRST, G, 1>(C, k, c, zdn, sa, sb);
+    else pair_group<FIRST, G, 0>(C, k, c, zdn, sa, sb);
   }
 }
 

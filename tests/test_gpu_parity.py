@@ -478,14 +478,17 @@ PAIR_EDGE = [
 
 
 @pytest.mark.parametrize("name,n,bc", PAIR_EDGE, ids=[c[0] for c in PAIR_EDGE])
-@pytest.mark.parametrize("tma", ["1", "0"])
-def test_pair_sweep_edges(torch_mod, name, n, bc, tma, monkeypatch):
-    """Forced fused pairs (TMA-fed or register-pipelined) on ragged level-0 shapes against
-    the oracle's half-sweep sequence: 9 from zero and 4 from a nonzero z."""
+@pytest.mark.parametrize("variant", ["tma16", "tma8", "regs"])
+def test_pair_sweep_edges(torch_mod, name, n, bc, variant, monkeypatch):
+    """Forced fused pairs (TMA-fed with 16- or 8-row tiles, or register-pipelined) on ragged
+    level-0 shapes against the oracle's half-sweep sequence: 9 from zero and 4
+    from a nonzero z."""
     torch = torch_mod
     from paper_math_9809043_b200.mss import Solver
     monkeypatch.setenv("MSS_PAIR", "1")
-    monkeypatch.setenv("MSS_PAIR_TMA", tma)
+    monkeypatch.setenv("MSS_PAIR_TMA", "0" if variant == "regs" else "1")
+    if variant != "regs":
+        monkeypatch.setenv("MSS_PAIR_TY", variant[3:])
     w = random_problem(3, n, seed=11, bc=_all_dirichlet(3) if bc else None)
     s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=1)
     o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=1)
