@@ -233,7 +233,7 @@ struct TailSm {
   // ---------------------------------------------------------------- passes
   // half-sweep of colour col; dot: returns r.z over all local cells (cluster-summed)
   __device__ double sweep(int q, int col, bool first, bool dot) {
-    const TsLevel& l = lvl(q);
+    const TsLevel l = lvl(q);   // by value: smem stores below cannot alias it
     const int o0 = olo(l), o1 = ohi(l);
     const int hx = l.hx;
     const int rows = (o1 - o0) * (NDIM == 3 ? l.ny : 1);
@@ -290,8 +290,8 @@ struct TailSm {
 
   // r_{q+1} = R (r - A z) on level q (black residual only)
   __device__ void resid_restrict(int q) {
-    const TsLevel& f = lvl(q);
-    const TsLevel& c = lvl(q + 1);
+    const TsLevel f = lvl(q);
+    const TsLevel c = lvl(q + 1);
     const int S = A->s;
     const int o0 = olo(f), o1 = ohi(f);
     const W1* wx = wt(f.o_wx);
@@ -374,8 +374,8 @@ struct TailSm {
 
   // z_black += (E x_{q+1})_black on level q
   __device__ void prolong(int q) {
-    const TsLevel& f = lvl(q);
-    const TsLevel& c = lvl(q + 1);
+    const TsLevel f = lvl(q);
+    const TsLevel c = lvl(q + 1);
     const int o0 = olo(f), o1 = ohi(f);
     const int hx = f.hx;
     const int rows = (o1 - o0) * (NDIM == 3 ? f.ny : 1);
@@ -544,7 +544,9 @@ template <>
 template <>
 __device__ bool TailSm<3>::precond<0>(int, double&) { return false; }
 
-template <int NDIM>
+// D = L - L0: recursion depth of the tail, a template parameter so that each launch carries
+// only the PCG frames it needs (register pressure; a deeper instantiation spills).
+template <int NDIM, int D>
 __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restrict__ Ag) {
   extern __shared__ double sm_dyn[];
   // The level descriptors are read in every pass; cluster barriers invalidate L1, so a
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
     for (int t = threadIdx.x; t < n; t += blockDim.x) sm_dyn[l.o_r + t] = A->r_in[(int64_t)o0 * l.P + t];
   }
   T.sync();
-  const bool ok = T.template pcg<7>(A->L0);
+  const bool ok = T.template pcg<D>(A->L0);
   (void)ok;
   {
     const TsLevel& l = T.lvl(A->L0);
@@ -582,6 +584,22 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
 }  // namespace mss
 
 // ============================================================================ host side
+// the k_tailsm instantiation for a tail of depth D = L - L0 (1 .. kTsMaxLv - 1)
+static const void* tailsm_kernel(int ndim, int D) {
+#define TSK(N)                                                                           \
+  switch (D) {                                                                           \
+    case 1: return (const void*)mss::k_tailsm<N, 1>;                                     \
+    case 2: return (const void*)mss::k_tailsm<N, 2>;                                     \
+    case 3: return (const void*)mss::k_tailsm<N, 3>;                                     \
+    case 4: return (const void*)mss::k_tailsm<N, 4>;                                     \
+    case 5: return (const void*)mss::k_tailsm<N, 5>;                                     \
+    case 6: return (const void*)mss::k_tailsm<N, 6>;                                     \
+    default: return (const void*)mss::k_tailsm<N, 7>;                                    \
+  }
+  if (ndim == 3) { TSK(3) }
+  TSK(2)
+#undef TSK
+}
 // Lay out levels L0..L in shared memory; returns false if they do not fit.
 static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
   using namespace mss;
@@ -659,7 +677,7 @@ static void tailsm_setup(mss_ctx* ctx) {
     if (dbg) fprintf(stderr, "[mss] tailsm: level %d does not fit (%d doubles)\n", L0, a.smem_doubles);
     return;
   }
-  auto kern = (ctx->ndim == 3) ? (void*)mss::k_tailsm<3> : (void*)mss::k_tailsm<2>;
+  auto kern = tailsm_kernel(ctx->ndim, ctx->L - L0);
   const size_t shm = (size_t)a.smem_doubles * sizeof(double);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
@@ -743,8 +761,8 @@ static int tailsm_launch(mss_ctx* ctx, int k) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   const mss::TsArgs* dp = reinterpret_cast<const mss::TsArgs*>(ctx->tsm_d);
-  cudaError_t e = (ctx->ndim == 3) ? cudaLaunchKernelEx(&cfg, mss::k_tailsm<3>, dp)
-                                   : cudaLaunchKernelEx(&cfg, mss::k_tailsm<2>, dp);
+  void* args[] = {(void*)&dp};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, tailsm_kernel(ctx->ndim, a.L - a.L0), args);
   ctx->launches++;
   return e == cudaSuccess ? MSS_OK : MSS_ECUDA;
 }
