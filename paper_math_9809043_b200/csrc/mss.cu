@@ -389,6 +389,14 @@ static bool tmap_get(mss_ctx* ctx, CUtensorMap* out, const void* base, int kind,
   return true;
 }
 
+// TMA SpMV: big levels by default (measured: the one-CTA-per-SM walk is latency-bound on
+// small ones); MSS_SPMV_TMA=1 forces every padded level (tests), 0 disables.
+static bool spmv_tma_ok(const Level& l) {
+  const char* e = getenv("MSS_SPMV_TMA");
+  if (e) return atoi(e) != 0;
+  return pair_tma_on() && l.N >= ((int64_t)1 << 24);
+}
+
 // Temporally fused pair of half-sweeps (colour col1 then the other) zin -> zout.
 static bool pair_ok(const mss_ctx* ctx, int k) {
   // Fused pairs beat two single sweeps on large levels only (512^3: 1.43 ms per pair vs
@@ -742,6 +750,40 @@ static int pcg_level(mss_ctx* ctx, int k) {
       k_spmv_col<4, true><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds,
                                                                        it == 0 ? 1 : 0, kch,
                                                                        red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
+      ctx->launches++;
+    } else if (l.txp && spmv_tma_ok(l)) {
+      // TMA-fed SpMV (pairtma.cuh): faces from the padded Tx copy of this level
+      SpmvMaps M;
+      if (!tmap_get(ctx, &M.z, l.z, 16, l.nx, l.ny, l.nz, SpmvGeo::ZW, SpmvGeo::ZH) ||
+          !tmap_get(ctx, &M.p, pin, 16, l.nx, l.ny, l.nz, SpmvGeo::ZW, SpmvGeo::ZH) ||
+          !tmap_get(ctx, &M.tx, l.txp, 17, l.nx + 2, l.ny, l.nz, SpmvGeo::XW, SpmvGeo::TY) ||
+          !tmap_get(ctx, &M.ty, l.Ty, 18, l.nx, l.ny + 1, l.nz, SpmvGeo::W, SpmvGeo::TY + 1) ||
+          !tmap_get(ctx, &M.tz, l.Tz, 19, l.nx, l.ny, l.nz + 1, SpmvGeo::W, SpmvGeo::TY))
+        return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
+      const int sbx = (l.nx / 2 + kPX - 1) / kPX, sby = (l.ny + SpmvGeo::TY - 1) / SpmvGeo::TY;
+      const char* nce = getenv("MSS_SPMV_NCH");
+      int snch = 1;
+      if (nce) {
+        snch = std::max(1, atoi(nce));
+      } else {
+        const int64_t tiles = (int64_t)sbx * sby;
+        int64_t best = -1;
+        for (int cc = 1; cc <= std::min(32, l.nz); ++cc) {
+          const int64_t kc = (l.nz + cc - 1) / cc;
+          const int64_t cost = ((tiles * cc + kSMs - 1) / kSMs) * (kc + 5);
+          if (best < 0 || cost < best) {
+            best = cost;
+            snch = cc;
+          }
+        }
+      }
+      int skch = (l.nz + snch - 1) / snch;
+      snch = (l.nz + skch - 1) / skch;
+      if ((int64_t)sbx * sby * snch > kMaxPartials) return set_err(MSS_EINVAL, "spmv grid too large");
+      const dim3 sgrid(sbx, sby, snch), sblk(kPX, SpmvGeo::TY);
+      const RedOut ro = red_to(ctx, &ds->pq, k, 0);
+      if (it == 0) k_spmv_tma<true><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro);
+      else k_spmv_tma<false><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro);
       ctx->launches++;
     } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
       k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
@@ -1278,6 +1320,8 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairBig::SMEM));
       CK(cudaFuncSetAttribute(k_sweep2t_col<true, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
+      CK(cudaFuncSetAttribute(k_spmv_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
+      CK(cudaFuncSetAttribute(k_spmv_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
     }
   }
   TRY(tail_setup(ctx));

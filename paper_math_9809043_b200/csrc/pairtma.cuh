@@ -241,6 +241,124 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// a10 on TMA: p_out = z + beta p_in, q = A p_out, p_out . q (same per-cell expressions as
+// k_spmv_col; neighbour p values are formed from z and p_in, never from p_out).  Tile: 32 pairs
+// x 16 rows, all interior (no in-kernel dependency, so no ring); per plane the z and p_in tiles
+// (1-cell apron) and the faces arrive by TMA in a 4-stage ring; one barrier per plane releases
+// the slot that is refilled.
+struct SpmvGeo {
+  static constexpr int TY = 16, NS = 4;
+  static constexpr int ZW = 2 * kPX + 4, ZH = TY + 2, XW = 2 * kPX + 2, W = 2 * kPX;
+  static constexpr int oZ = 0;
+  static constexpr int oP = oZ + ((ZW * ZH + 15) & ~15);
+  static constexpr int oTx = oP + ((ZW * ZH + 15) & ~15);
+  static constexpr int oTy = oTx + ((XW * TY + 15) & ~15);
+  static constexpr int oTz = oTy + ((W * (TY + 1) + 15) & ~15);
+  static constexpr int SD = oTz + ((W * TY + 15) & ~15);
+  static constexpr uint32_t BZ = 8u * ZW * ZH;
+  static constexpr uint32_t BTz = 8u * W * TY;
+  static constexpr uint32_t BT = 8u * (XW * TY + W * (TY + 1) + W * TY);
+  static constexpr size_t SMEM = sizeof(double) * (size_t)NS * SD + 64;
+};
+
+struct SpmvMaps {
+  CUtensorMap z, p, tx, ty, tz;
+};
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
+    k_spmv_tma(const __grid_constant__ SpmvMaps M, LevelDev L, const double* __restrict__ z,
+               const double* __restrict__ pin, double* __restrict__ pout, double* __restrict__ q, const Scal* sc,
+               int kchunk, RedOut ro) {
+  using G = SpmvGeo;
+  extern __shared__ __align__(128) double smd[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smd + G::NS * G::SD);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kPX + tx;
+  const int x0 = 2 * kPX * blockIdx.x, j0 = G::TY * blockIdx.y;
+  const int m = blockIdx.x * kPX + tx, j = j0 + ty;
+  const int nx = L.nx, ny = L.ny, nz = L.nz;
+  const int64_t plane = L.plane;
+  const int k0 = blockIdx.z * kchunk, k1 = min(nz, k0 + kchunk);
+  const int i0 = 2 * m, lx = 2 * tx;
+  const bool valid = i0 < nx && j < ny;
+  const double beta = FIRST ? 0.0 : sc->rho / sc->rho_prev;
+  // planes k0 .. k1 are staged (plane k1 for the upper neighbours / faces)
+  auto issue = [&](int p) {
+    const int s = (p - k0) & (G::NS - 1);
+    double* st = smd + s * G::SD;
+    if (p >= nz) {
+      mbar_expect(&bar[s], G::BTz);
+      tma_load3(st + G::oTz, &M.tz, x0, j0, p, &bar[s]);
+      return;
+    }
+    mbar_expect(&bar[s], G::BT + (FIRST ? 1u : 2u) * G::BZ);
+    tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p, &bar[s]);
+    if (!FIRST) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p, &bar[s]);
+    tma_load3(st + G::oTx, &M.tx, x0, j0, p, &bar[s]);
+    tma_load3(st + G::oTy, &M.ty, x0, j0, p, &bar[s]);
+    tma_load3(st + G::oTz, &M.tz, x0, j0, p, &bar[s]);
+  };
+  const int np = k1 - k0 + 1;
+  if (tid == 0) {
+    for (int s = 0; s < G::NS; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < min(np, G::NS); ++s) issue(k0 + s);
+  double acc = 0.0;
+  int64_t c = valid ? i0 + (int64_t)nx * (j + (int64_t)ny * k0) : 0;
+  double2 pdn = make_double2(0.0, 0.0);
+  if (valid) {
+    const double2 zz = ld2(z + c - plane);   // ghost plane below the domain is zero
+    if (FIRST) {
+      pdn = zz;
+    } else {
+      const double2 pp = ld2(pin + c - plane);
+      pdn = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
+    }
+  }
+  auto PV = [&](const double* S, int off) {   // p value at smem offset of the z / p tiles
+    return FIRST ? S[G::oZ + off] : S[G::oZ + off] + beta * S[G::oP + off];
+  };
+  mbar_wait(&bar[0], 0);
+  for (int k = k0; k < k1; ++k) {
+    const int s0 = (k - k0) & (G::NS - 1), s1 = (k + 1 - k0) & (G::NS - 1);
+    mbar_wait(&bar[s1], ((k + 1 - k0) >> 2) & 1);
+    const double* S0 = smd + s0 * G::SD;
+    const double* S1 = smd + s1 * G::SD;
+    if (valid) {
+      const int zo = (ty + 1) * G::ZW + lx + 2;   // own pair in the z / p tiles
+      const double2 pc = make_double2(PV(S0, zo), PV(S0, zo + 1));
+      const double2 pup = (k + 1 < nz) ? make_double2(PV(S1, zo), PV(S1, zo + 1)) : make_double2(0.0, 0.0);
+      const double2 ps = make_double2(PV(S0, zo - G::ZW), PV(S0, zo - G::ZW + 1));
+      const double2 pn = make_double2(PV(S0, zo + G::ZW), PV(S0, zo + G::ZW + 1));
+      const double pl = PV(S0, zo - 1), pr = PV(S0, zo + 2);
+      const double* txr = S0 + G::oTx + ty * G::XW + lx;
+      const double2 t01 = *reinterpret_cast<const double2*>(txr);
+      const double tx0 = t01.x, tx1 = t01.y, tx2 = txr[2];
+      const double2 tyl = *reinterpret_cast<const double2*>(S0 + G::oTy + ty * G::W + lx);
+      const double2 tyu = *reinterpret_cast<const double2*>(S0 + G::oTy + (ty + 1) * G::W + lx);
+      const double2 tzl = *reinterpret_cast<const double2*>(S0 + G::oTz + ty * G::W + lx);
+      const double2 tzu = *reinterpret_cast<const double2*>(S1 + G::oTz + ty * G::W + lx);
+      const double d0 = tx0 + tx1 + tyl.x + tyu.x + tzl.x + tzu.x;
+      const double d1 = tx1 + tx2 + tyl.y + tyu.y + tzl.y + tzu.y;
+      const double s0v = tx0 * pl + tx1 * pc.y + tyl.x * ps.x + tyu.x * pn.x + tzl.x * pdn.x + tzu.x * pup.x;
+      const double s1v = tx1 * pc.x + tx2 * pr + tyl.y * ps.y + tyu.y * pn.y + tzl.y * pdn.y + tzu.y * pup.y;
+      const double q0 = d0 * pc.x - s0v, q1 = d1 * pc.y - s1v;
+      *reinterpret_cast<double2*>(pout + c) = pc;
+      *reinterpret_cast<double2*>(q + c) = make_double2(q0, q1);
+      acc += pc.x * q0 + pc.y * q1;
+      pdn = pc;
+      c += plane;
+    }
+    __syncthreads();   // plane k's slot is free: refill it with plane k+4
+    if (tid == 0 && k + G::NS <= k1) issue(k + G::NS);
+  }
+  grid_sum_finish(acc, ro);
+}
+
 // Txp: Tx with row pitch n_x + 2 (faces 0..n_x, one zero pad) so TMA can describe it.
 __global__ void k_pad_tx(const double* __restrict__ Tx, double* __restrict__ Txp, int nx, int64_t rows) {
   const int64_t n = rows * (nx + 2);

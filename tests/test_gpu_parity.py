@@ -507,3 +507,28 @@ def test_pair_sweep_edges(torch_mod, name, n, bc, variant, monkeypatch):
             col = (first + h) % 2
             O.halfsweep(lv.T, lv.diag, r, zo, col, lv.red if col == 0 else lv.black)
         assert rel(zg, zo) <= KTOL
+
+
+@pytest.mark.parametrize("name,n,bc", PAIR_EDGE, ids=[c[0] for c in PAIR_EDGE])
+def test_spmv_tma_solves(torch_mod, name, n, bc, monkeypatch):
+    """TMA-fed direction + SpMV + p.q (forced on every padded level) inside full solves on
+    ragged shapes: identical per-level counts, and solutions within the solve gate of the
+    oracle.  The per-cell arithmetic is that of the column-walk SpMV, but p.q is
+    summed in a different block order, so the two CG trajectories differ by rounding and the
+    converged solutions by O(rel_tol): 1e-9 between them, not the bitwise-kernel 1e-12."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = random_problem(3, n, seed=13, bc=_all_dirichlet(3) if bc else None)
+    K = torch.from_numpy(w.K).cuda()
+    monkeypatch.setenv("MSS_SPMV_TMA", "0")
+    a = Solver(w.ndim, w.n, K, w.bc, depth=1)
+    xa, ra = a.solve(cu(torch, w.f), rel_tol=1e-10)
+    monkeypatch.setenv("MSS_SPMV_TMA", "1")
+    b = Solver(w.ndim, w.n, K, w.bc, depth=1)
+    xb, rb = b.solve(cu(torch, w.f), rel_tol=1e-10)
+    assert ra.iters == rb.iters
+    assert rel(xb.cpu().numpy(), xa.cpu().numpy()) <= 1e-9
+    assert rb.true_rel_res <= 1e-10
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=1)
+    xo, _ = o.solve(w.f, rel_tol=1e-10)
+    assert rel(xb.cpu().numpy(), xo.ravel()) <= 1e-8
