@@ -208,6 +208,32 @@ int mss_profile_read(const mss_ctx* ctx, int kclass, int level, int64_t* count,
 /* Number of library kernels launched since the context was created. */
 int mss_kernel_launches(const mss_ctx* ctx, int64_t* count);
 
+/* ---- NEXT-4: log-normal permeability fields and the manufactured problem -------------
+ * "random log-normal permeability field with either a Gaussian auto-correlation
+ * function or a power law auto-correlation function (1 / (1 + r^T Lambda r))^(1/4), where
+ * Lambda is a positive definite matrix which defines cutoff lengths ... The variance of the
+ * permeability field is adjusted by scaling the log of the field."  The sampler is the
+ * reading of DESIGN.md §2 (F1-F5): counter-based white noise (splitmix64 + Box-Muller,
+ * cell c uses counters 2c, 2c+1 of splitmix64(seed)), circulant embedding of the
+ * covariance at signed minimum-image lags of the periodic grid (negative spectrum
+ * clipped), standardisation, log K = log_mean + sqrt(log_var) g, K = exp(log K). */
+typedef struct {
+  int model;            /* 0 Gaussian exp(-r^T Lambda r) (F1), 1 power law (1 + r^T Lambda r)^(-1/4) */
+  double ell[3];        /* principal correlation / cutoff lengths, in cells (> 0; unused axes ignored) */
+  double theta;         /* rotation of the principal axes in the x-y plane, radians (F2) */
+  double log_mean;      /* mean of log K */
+  double log_var;       /* variance of log K (>= 0) */
+  uint64_t seed;        /* white-noise stream (F4) */
+} mss_field_params;
+/* K: device, N = nx*ny*nz fp64 (caller-owned, x fastest; nz = 1 in 2-D).  Synchronous on
+ * `stream` (temporaries ~3.5 N doubles are freed before returning).  Errors: MSS_EINVAL
+ * (ndim, sizes, lengths, variance, model), MSS_ENOMEM, MSS_ECUDA (incl. cuFFT failures). */
+int mss_field_generate(int ndim, const int64_t n[3], const mss_field_params* p, double* K, void* stream);
+/* P:707-713 (accuracy study): f_out = (A_0 x_exact - b_0) / V, b_0 the boundary terms of the
+ * right-hand side (O5 with f = 0), so mss_solve(f_out) has the discrete solution x_exact
+ * (reading F6).  x_exact, f_out: device, local N (z-slab in distributed contexts). */
+int mss_manufacture_rhs(mss_ctx* ctx, const double* x_exact, double* f_out);
+
 #ifdef __cplusplus
 }
 #endif

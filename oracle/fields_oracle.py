@@ -21,7 +21,10 @@ Readings ("NEXT-4 readings"):
       plane; lengths in cells.
   F3  Sampler (the paper gives none): circulant embedding on the periodic grid —
       the covariance is evaluated at signed minimum-image lags, its DFT S (real) is
-      clipped at 0, and G = IDFT(sqrt(S) DFT(w)) for white noise w.
+      clipped: values below 1e-8 S_0 (S_0 = S(0) = sum C >= |S| since C > 0) — the negative
+      ones, and those where the square root would amplify the DFT's rounding noise
+      (|d sqrt S| <= eps S_0 / (2 sqrt S)) — are set to 0 by both implementations alike;
+      the dropped power is <= 1e-8 S_0 per mode.  G = IDFT(sqrt(S) DFT(w)), w white noise.
   F4  White noise from a counter-based generator both sides implement: splitmix64 of
       (splitmix64(seed) + 2c + s), s = 0, 1, turned into u = (top 53 bits + 1/2) 2^-53 and
       a standard normal by Box-Muller, w_c = sqrt(-2 ln u_0) cos(2 pi u_1).
@@ -101,13 +104,22 @@ def periodic_covariance(ndim, n, model, ell, theta) -> np.ndarray:
     return np.ascontiguousarray(np.transpose(C))   # -> (z, y, x) / (y, x)
 
 
+SPECTRUM_FLOOR = 1e-8
+
+
+def clip_spectrum(S):
+    """F3: S where S >= 1e-8 S_0 (S_0 = S at zero frequency, the largest value), else 0."""
+    S0 = S.flat[0]
+    return np.where(S >= SPECTRUM_FLOOR * S0, S, 0.0)
+
+
 def gaussian_field(ndim, n, model, ell, theta, seed, noise=None) -> np.ndarray:
-    """F3: G = IDFT(sqrt(max(S, 0)) DFT(w)), S = DFT(C) (real: C is even)."""
+    """F3: G = IDFT(sqrt(clip(S)) DFT(w)), S = DFT(C) (real: C is even)."""
     shape = O.shape_of(ndim, n)
     N = int(np.prod(shape))
     w = white_noise(seed, N).reshape(shape) if noise is None else np.asarray(noise, dtype=np.float64)
     S = np.fft.fftn(periodic_covariance(ndim, n, model, ell, theta)).real
-    A = np.sqrt(np.maximum(S, 0.0))
+    A = np.sqrt(clip_spectrum(S))
     return np.fft.ifftn(A * np.fft.fftn(w)).real
 
 

@@ -51,6 +51,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd += [os.path.join(CSRC, "mss.cu"), "-o", LIB + ".tmp"]
     if inc:
         cmd += ["-l:libnccl.so.2"]
+    # cuFFT (NEXT-4 field sampler: a library FFT as a step of the method)
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+    cmd += ["-L", cudalib, "-lcufft", "-Xlinker", f"-rpath={cudalib}"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

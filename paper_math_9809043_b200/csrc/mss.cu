@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "colwalk.cuh"
 #include "pairtma.cuh"
+#include "fields.cuh"
 #include "comm.cuh"
 
 using namespace mss;
@@ -1719,3 +1720,129 @@ int mss_setup_loopback(mss_ctx** out, void* group, int rank, int ndim, const int
   return setup_common(out, c, ndim, n_global, extent, K_local, k_comp, bc, depth, p, stream);
 }
 }
+
+// ============================================================================ NEXT-4 fields
+int mss_field_generate(int ndim, const int64_t n[3], const mss_field_params* p, double* K, void* stream) {
+  if ((ndim != 2 && ndim != 3) || !n || !p || !K) return set_err(MSS_EINVAL, "field: bad arguments");
+  const int64_t nz = (ndim == 3) ? n[2] : 1;
+  if (n[0] < 1 || n[1] < 1 || nz < 1 || n[0] > (1 << 20) || n[1] > (1 << 20) || nz > (1 << 20))
+    return set_err(MSS_EINVAL, "field: bad sizes");
+  if (p->model != 0 && p->model != 1) return set_err(MSS_EINVAL, "field: model must be 0 (Gaussian) or 1 (power law)");
+  for (int d = 0; d < ndim; ++d)
+    if (!(p->ell[d] > 0.0) || !std::isfinite(p->ell[d])) return set_err(MSS_EINVAL, "field: lengths must be > 0");
+  if (!(p->log_var >= 0.0) || !std::isfinite(p->log_var) || !std::isfinite(p->log_mean) || !std::isfinite(p->theta))
+    return set_err(MSS_EINVAL, "field: bad variance / mean / angle");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t N = n[0] * n[1] * nz;
+  const int64_t nh = n[0] / 2 + 1, M = nh * n[1] * nz;
+  // F2: Lambda = R^T diag(1/l^2) R
+  FieldGeo g;
+  g.nx = (int)n[0];
+  g.ny = (int)n[1];
+  g.nz = (int)nz;
+  g.ndim = ndim;
+  g.model = p->model;
+  double L[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, R[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int d = 0; d < ndim; ++d) L[d][d] = 1.0 / (p->ell[d] * p->ell[d]);
+  const double c = std::cos(p->theta), s = std::sin(p->theta);
+  R[0][0] = c; R[0][1] = s; R[1][0] = -s; R[1][1] = c;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double acc = 0.0;
+      for (int e = 0; e < 3; ++e) acc += R[e][a] * L[e][e] * R[e][b];
+      g.lam[a][b] = acc;
+    }
+  double *C = nullptr, *part = nullptr, *stat = nullptr;
+  cufftDoubleComplex *Sx = nullptr, *Wx = nullptr;
+  cufftHandle fwd = 0, inv = 0;
+  bool pf = false, pi = false;
+  int rc = MSS_OK;
+  auto fail = [&](int code, const char* msg) {
+    rc = set_err(code, msg);
+    return rc;
+  };
+  const int nb = 1184;
+  do {
+    if (cudaMalloc(&C, sizeof(double) * N) != cudaSuccess || cudaMalloc(&Sx, sizeof(cufftDoubleComplex) * M) != cudaSuccess ||
+        cudaMalloc(&Wx, sizeof(cufftDoubleComplex) * M) != cudaSuccess ||
+        cudaMalloc(&part, sizeof(double) * nb) != cudaSuccess || cudaMalloc(&stat, sizeof(double) * 2) != cudaSuccess) {
+      cudaGetLastError();
+      fail(MSS_ENOMEM, "field: cudaMalloc failed");
+      break;
+    }
+    const bool d3 = (ndim == 3);
+    if ((d3 ? cufftPlan3d(&fwd, (int)nz, (int)n[1], (int)n[0], CUFFT_D2Z) : cufftPlan2d(&fwd, (int)n[1], (int)n[0], CUFFT_D2Z)) !=
+        CUFFT_SUCCESS) {
+      fail(MSS_ECUDA, "field: cuFFT D2Z plan failed");
+      break;
+    }
+    pf = true;
+    if ((d3 ? cufftPlan3d(&inv, (int)nz, (int)n[1], (int)n[0], CUFFT_Z2D) : cufftPlan2d(&inv, (int)n[1], (int)n[0], CUFFT_Z2D)) !=
+        CUFFT_SUCCESS) {
+      fail(MSS_ECUDA, "field: cuFFT Z2D plan failed");
+      break;
+    }
+    pi = true;
+    cufftSetStream(fwd, st);
+    cufftSetStream(inv, st);
+    const int gb = (int)std::min<int64_t>((N + 255) / 256, 4736);
+    // S = DFT(C)
+    k_periodic_cov<<<gb, 256, 0, st>>>(g, C);
+    if (cufftExecD2Z(fwd, C, Sx) != CUFFT_SUCCESS) {
+      fail(MSS_ECUDA, "field: cuFFT D2Z (covariance) failed");
+      break;
+    }
+    // W = DFT(w), w the F4 white noise (C reused as the noise / field buffer)
+    const uint64_t base = [](uint64_t x) {
+      uint64_t z = x + 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return z ^ (z >> 31);
+    }(p->seed);
+    k_white_noise<<<gb, 256, 0, st>>>(N, base, C);
+    if (cufftExecD2Z(fwd, C, Wx) != CUFFT_SUCCESS) {
+      fail(MSS_ECUDA, "field: cuFFT D2Z (noise) failed");
+      break;
+    }
+    const int gm = (int)std::min<int64_t>((M + 255) / 256, 4736);
+    k_spectral_filter<<<gm, 256, 0, st>>>(M, Sx, Wx, 1.0 / (double)N);
+    if (cufftExecZ2D(inv, Wx, C) != CUFFT_SUCCESS) {
+      fail(MSS_ECUDA, "field: cuFFT Z2D failed");
+      break;
+    }
+    // F5: mean, population variance, rescaled exponential
+    k_field_partial<1><<<nb, 256, 0, st>>>(N, C, nullptr, part);
+    k_field_final<<<1, 256, 0, st>>>(nb, part, 1.0 / (double)N, stat);
+    k_field_partial<2><<<nb, 256, 0, st>>>(N, C, stat, part);
+    k_field_final<<<1, 256, 0, st>>>(nb, part, 1.0 / (double)N, stat + 1);
+    k_lognormal<<<gb, 256, 0, st>>>(N, C, stat, stat + 1, p->log_mean, std::sqrt(p->log_var), K);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+      fail(MSS_ECUDA, "field: kernel failure");
+      break;
+    }
+  } while (0);
+  if (pf) cufftDestroy(fwd);
+  if (pi) cufftDestroy(inv);
+  cudaFree(C);
+  cudaFree(Sx);
+  cudaFree(Wx);
+  cudaFree(part);
+  cudaFree(stat);
+  return rc;
+}
+
+int mss_manufacture_rhs(mss_ctx* ctx, const double* x_exact, double* f_out) {
+  if (!ctx || !x_exact || !f_out) return set_err(MSS_EINVAL, "manufacture: null argument");
+  Level& l = ctx->lv[0];
+  // b_0: the boundary terms (O5 with f = 0) into l.b; x~ (with halos) into l.x; r = b_0 - A x~
+  CK(cudaMemsetAsync(l.q, 0, sizeof(double) * l.N, ctx->stream));
+  BCDev bc = bc_dev(ctx);
+  DISPATCH(ctx->ndim, k_rhs_lift, grid_for(l.N), l.dev(), l.q, l.b, nullptr, cell_volume(ctx), bc);
+  CK(cudaMemcpyAsync(l.x, x_exact, sizeof(double) * l.N, cudaMemcpyDeviceToDevice, ctx->stream));
+  TRY(do_halo(ctx, 0, l.x));
+  TRY(op_residual(ctx, 0, l.b, l.x, l.r, nullptr));
+  LAUNCH(k_neg_scale, grid_for(l.N), l.N, l.r, 1.0 / cell_volume(ctx), f_out);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+

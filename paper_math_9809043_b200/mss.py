@@ -71,12 +71,20 @@ class Info(ctypes.Structure):
     ]
 
 
+class FieldParams(ctypes.Structure):
+    """mss_field_params (include/mss.h, NEXT-4)."""
+    _fields_ = [("model", ctypes.c_int), ("ell", ctypes.c_double * 3), ("theta", ctypes.c_double),
+                ("log_mean", ctypes.c_double), ("log_var", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
 P = ctypes.c_void_p
 I64P = ctypes.POINTER(ctypes.c_int64)
 DP = ctypes.POINTER(ctypes.c_double)
 
 # (name, restype, argtypes) for every symbol include/mss.h declares.
 SIGNATURES = [
+    ("mss_field_generate", ctypes.c_int, [ctypes.c_int, I64P, ctypes.POINTER(FieldParams), P, P]),
+    ("mss_manufacture_rhs", ctypes.c_int, [P, P, P]),
     ("mss_default_params", ctypes.c_int, [ctypes.POINTER(Params)]),
     ("mss_strerror", ctypes.c_char_p, [ctypes.c_int]),
     ("mss_last_error", ctypes.c_char_p, []),
@@ -179,6 +187,30 @@ def slab_range(n_global, rank: int, nranks: int, params: Optional[dict] = None, 
     _check(lib.mss_slab_range(nn, 3, ctypes.byref(prm), -1 if depth is None else int(depth), int(rank), int(nranks),
                               ctypes.byref(zb), ctypes.byref(ze)), "mss_slab_range", allow_nc=False)
     return zb.value, ze.value
+
+
+def generate_field(ndim: int, n, model: int = 1, ell=(8.0, 1.0, 1.0), theta: float = 0.0, log_mean: float = 0.0,
+                   log_var: float = 1.0, seed: int = 0, device=None, stream=None) -> torch.Tensor:
+    """Log-normal permeability field on the device (mss_field_generate, NEXT-4):
+    model 0 Gaussian, 1 power law (1 + r^T Lambda r)^(-1/4); lengths in cells; shape
+    (nz, ny, nx) / (ny, nx)."""
+    lib = load_library()
+    nx, ny = int(n[0]), int(n[1])
+    nz = int(n[2]) if ndim == 3 else 1
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    shape = (nz, ny, nx) if ndim == 3 else (ny, nx)
+    K = torch.empty(shape, dtype=torch.float64, device=dev)
+    fp = FieldParams()
+    fp.model = int(model)
+    ell = list(ell) + [1.0] * (3 - len(ell))
+    for d in range(3):
+        fp.ell[d] = float(ell[d])
+    fp.theta, fp.log_mean, fp.log_var, fp.seed = float(theta), float(log_mean), float(log_var), int(seed) & (2 ** 64 - 1)
+    st = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+    nn = (ctypes.c_int64 * 3)(nx, ny, nz)
+    _check(lib.mss_field_generate(int(ndim), nn, ctypes.byref(fp), ctypes.c_void_p(K.data_ptr()), ctypes.c_void_p(st)),
+           "mss_field_generate")
+    return K
 
 
 def nccl_unique_id() -> bytes:
@@ -303,6 +335,13 @@ class Solver:
         return SolveReport(0, list(inf.iters[:L1]), list(inf.calls[:L1]),
                            [tuple(inf.dims[k]) for k in range(L1)], bool(inf.not_converged),
                            inf.true_rel_res, inf.kernel_launches, inf.tail_level, inf.tail_kind)
+
+    def manufacture_rhs(self, x_exact: torch.Tensor) -> torch.Tensor:
+        """f' with discrete solution x_exact (mss_manufacture_rhs)."""
+        n = self.level_N(0)
+        f = torch.empty(n, dtype=torch.float64, device=x_exact.device)
+        _check(self.lib.mss_manufacture_rhs(self.ctx, _dev_ptr(x_exact, n), f.data_ptr()), "mss_manufacture_rhs")
+        return f
 
     def profile(self, enable: bool, max_level: int = 0):
         _check(self.lib.mss_profile(self.ctx, 1 if enable else 0, int(max_level)), "mss_profile")

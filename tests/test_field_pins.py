@@ -62,18 +62,25 @@ def _circular_autocorr(h, lag):
 @pytest.mark.parametrize("ndim,n,ell,theta", [(2, (48, 40, 1), (5.0, 2.0), 0.4),
                                                (3, (32, 24, 18), (2.5, 2.0, 1.5), 0.2)])
 def test_P13_circulant_embedding_reproduces_gaussian_covariance(ndim, n, ell, theta):
-    """Impulse noise: G = IDFT(sqrt S) and its circular autocorrelation is IDFT(S) = C
-    exactly when S >= 0 (Gaussian model, lengths well inside the torus)."""
+    """Impulse noise: G = IDFT(sqrt clip(S)); its circular autocorrelation (explicit shifts)
+    is IDFT(clip(S)) to rounding, and C of the formula to within the dropped spectral mass
+    (F3 floor), since IDFT(S) = C exactly (Gaussian model, lengths well inside the torus)."""
     shape = O.shape_of(ndim, n)
     delta = np.zeros(shape)
     delta[(0,) * ndim] = 1.0
     h = F.gaussian_field(ndim, n, 0, ell, theta, seed=0, noise=delta)
     S = np.fft.fftn(F.periodic_covariance(ndim, n, 0, ell, theta)).real
     assert S.min() > -1e-12 * S.max()
+    Sc = F.clip_spectrum(S)
+    Cr = np.fft.ifftn(Sc).real
+    dropped = float(np.sum(np.abs(S - Sc))) / S.size
+    assert dropped < 1e-7
     Lam = F.lambda_matrix(ndim, ell, theta).tolist()
     for lag in [(0,) * ndim, (1,) + (0,) * (ndim - 1), (0, 1) + (0,) * (ndim - 2), (2, -1) + (0,) * (ndim - 2),
                 (-3, 2) + ((1,) if ndim == 3 else ())]:
-        assert abs(_circular_autocorr(h, lag) - _cov_formula(0, lag, Lam)) < 1e-12
+        ac = _circular_autocorr(h, lag)
+        assert abs(ac - Cr[tuple(l % m for l, m in zip(reversed(lag), h.shape))]) < 1e-12
+        assert abs(ac - _cov_formula(0, lag, Lam)) < dropped + 1e-12
 
 
 def test_P13_power_law_embedding():
@@ -89,10 +96,11 @@ def test_P13_power_law_embedding():
     delta[0, 0] = 1.0
     h = F.gaussian_field(2, n, 1, ell, theta, seed=0, noise=delta)
     S = np.fft.fftn(F.periodic_covariance(2, n, 1, ell, theta)).real
-    Cr = np.fft.ifftn(np.maximum(S, 0.0)).real
+    assert S.flat[0] >= np.abs(S).max()
+    Cr = np.fft.ifftn(F.clip_spectrum(S)).real
     for lag in [(0, 0), (1, 0), (0, 1), (3, 1), (8, 2), (-5, 7)]:
         assert abs(_circular_autocorr(h, lag) - Cr[lag[1] % 64, lag[0] % 64]) < 1e-12
-    clipped = float(np.sum(np.maximum(-S, 0.0))) / S.size
+    clipped = float(np.sum(F.clip_spectrum(S) - S)) / S.size
     assert abs(_circular_autocorr(h, (0, 0)) - (1.0 + clipped)) < 1e-12
     Lam = F.lambda_matrix(2, ell, theta).tolist()
     for lag in [(8, 2), (12, 3), (20, 5)]:
