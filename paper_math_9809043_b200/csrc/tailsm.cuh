@@ -297,6 +297,18 @@ struct TailSm {
     const W1* wx = wt(f.o_wx);
     const W1* wy = wt(f.o_wy);
     {
+      // pass A0: the black residual of every local cell, once, into the level's q array
+      // (dead during the preconditioner); the x-windows below overlap 3-fold
+      const int nl = (o1 - o0) * f.P;
+      for (int t = threadIdx.x; t < nl; t += blockDim.x) {
+        int i, j, k;
+        decode(f, t, o0, i, j, k);
+        if (((i + j + k) & 1) == 0) continue;
+        sm[f.o_q + t] = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nbr(f, f.o_z, t, i, j, k, o0, o1));
+      }
+      __syncthreads();
+    }
+    {
       // pass A: t1[I, j, (k)] on local outer slices
       const int per_slice = f.t1_slice;
       const int n = (o1 - o0) * per_slice;
@@ -320,13 +332,13 @@ struct TailSm {
           const W1 w1 = wx[i];
           const double w = (w1.I0 == I ? w1.w0 : 0.0) + (w1.I1 == I ? w1.w1 : 0.0);
           if (w == 0.0) continue;
-          const int t = base + i;
-          const double res = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nbr(f, f.o_z, t, i, j, k, o0, o1));
-          acc += w * res;
+          acc += w * sm[f.o_q + base + i];
         }
         sm[f.o_t1 + u] = acc;
       }
-      sync();
+      // 3-D: pass B reads only this CTA's planes of t1; 2-D: pass C gathers across CTAs
+      if (NDIM == 3) __syncthreads();
+      else sync();
       mark(1);
     }
     if (NDIM == 3) {
