@@ -71,10 +71,23 @@ static int dalloc(mss_ctx* ctx, void** p, size_t bytes) {
 
 // ghosted cell vector: (nz + 2) planes, zeroed; returns the interior pointer.
 static int valloc(mss_ctx* ctx, const Level& l, double** out) {
+  // ghost planes each side: 1, or 2 on distributed levels (the fused pairs' z halos)
+  const int64_t g = l.dist ? 2 : 1;
   void* p = nullptr;
-  TRY(dalloc(ctx, &p, sizeof(double) * (size_t)(l.N + 2 * l.plane)));
-  CK(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)(l.N + 2 * l.plane), ctx->stream));
-  *out = reinterpret_cast<double*>(p) + l.plane;
+  TRY(dalloc(ctx, &p, sizeof(double) * (size_t)(l.N + 2 * g * l.plane)));
+  CK(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)(l.N + 2 * g * l.plane), ctx->stream));
+  *out = reinterpret_cast<double*>(p) + g * l.plane;
+  return MSS_OK;
+}
+
+// face array with one zeroed ghost face plane each side on distributed levels (filled by a
+// halo exchange at the end of setup; read by the fused pairs' redundant ghost-plane colour)
+static int falloc(mss_ctx* ctx, const Level& l, int64_t fplane, int64_t nplanes, double** out) {
+  const int64_t g = l.dist ? 1 : 0;
+  void* p = nullptr;
+  TRY(dalloc(ctx, &p, sizeof(double) * (size_t)(fplane * (nplanes + 2 * g))));
+  if (g) CK(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)(fplane * (nplanes + 2 * g)), ctx->stream));
+  *out = reinterpret_cast<double*>(p) + g * fplane;
   return MSS_OK;
 }
 
@@ -405,8 +418,12 @@ static bool pair_ok(const mss_ctx* ctx, int k) {
   // at least 2^24 cells; MSS_PAIR=0 disables, MSS_PAIR=1 forces every eligible level.
   const char* env = getenv("MSS_PAIR");   // read per call so tests can toggle it
   const int mode = env ? atoi(env) : -1;
-  if (mode == 0 || !col_ok(ctx, ctx->lv[k]) || dist_level(ctx, k)) return false;
-  return mode == 1 || ctx->lv[k].N >= ((int64_t)1 << 24);
+  const Level& l = ctx->lv[k];
+  if (mode == 0 || !col_ok(ctx, l)) return false;
+  // z-slab levels: only the TMA kernel computes the ghost planes' first colour
+  if (dist_level(ctx, k) && !(l.txp && pair_tma_on())) return false;
+  // per-rank slab size decides (a z-slab of 512^2 x 64 is 2^24 cells)
+  return mode == 1 || l.N >= ((int64_t)1 << 24);
 }
 
 static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, double* zout, int col1, bool first) {
@@ -425,12 +442,16 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     const bool big = tye ? atoi(tye) >= 16 : l.N >= ((int64_t)1 << 24);
     const int TY = big ? PairBig::TY : PairSmall::TY;
     const int occ = big ? PairBig::MINB : PairSmall::MINB;
+    // z-slab levels: the z map starts 2 ghost planes below the slab, the face / r maps 1
+    const int gz = l.dist ? 2 : 0, gf = l.dist ? 1 : 0;
     PairMaps M;
-    if (!tmap_get(ctx, &M.z, zin, 0 + 8 * big, l.nx, l.ny, l.nz, 2 * kPX + 4, TY + 2) ||
-        !tmap_get(ctx, &M.tx, l.txp, 1 + 8 * big, l.nx + 2, l.ny, l.nz, 2 * kPX + 2, TY) ||
-        !tmap_get(ctx, &M.ty, l.Ty, 2 + 8 * big, l.nx, l.ny + 1, l.nz, 2 * kPX, TY + 1) ||
-        !tmap_get(ctx, &M.tz, l.Tz, 3 + 8 * big, l.nx, l.ny, l.nz + 1, 2 * kPX, TY) ||
-        !tmap_get(ctx, &M.r, r, 4 + 8 * big, l.nx, l.ny, l.nz, 2 * kPX, TY))
+    if (!tmap_get(ctx, &M.z, zin - gz * l.plane, 0 + 8 * big, l.nx, l.ny, l.nz + 2 * gz, 2 * kPX + 4, TY + 2) ||
+        !tmap_get(ctx, &M.tx, l.txp - gf * (int64_t)(l.nx + 2) * l.ny, 1 + 8 * big, l.nx + 2, l.ny, l.nz + 2 * gf,
+                  2 * kPX + 2, TY) ||
+        !tmap_get(ctx, &M.ty, l.Ty - gf * (int64_t)l.nx * (l.ny + 1), 2 + 8 * big, l.nx, l.ny + 1, l.nz + 2 * gf,
+                  2 * kPX, TY + 1) ||
+        !tmap_get(ctx, &M.tz, l.Tz - gf * l.plane, 3 + 8 * big, l.nx, l.ny, l.nz + 1 + 2 * gf, 2 * kPX, TY) ||
+        !tmap_get(ctx, &M.r, r - gf * l.plane, 4 + 8 * big, l.nx, l.ny, l.nz + 2 * gf, 2 * kPX, TY))
       return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
     const int tby = (l.ny + TY - 3) / (TY - 2);
     // z chunks per tile column: minimise waves x (planes + 2 halo planes + ~4 planes of
@@ -455,11 +476,17 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     tnch = (l.nz + tkch - 1) / tkch;
     const dim3 tgrid(bx, tby, tnch), tblk(kPX, TY);
     if (big) {
-      if (first) k_sweep2t_col<true, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
-      else k_sweep2t_col<false, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+      if (first)
+        k_sweep2t_col<true, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch, gz, gf);
+      else
+        k_sweep2t_col<false, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch, gz, gf);
     } else {
-      if (first) k_sweep2t_col<true, PairSmall><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
-      else k_sweep2t_col<false, PairSmall><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch);
+      if (first)
+        k_sweep2t_col<true, PairSmall><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch, gz,
+                                                                                       gf);
+      else
+        k_sweep2t_col<false, PairSmall><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch, gz,
+                                                                                        gf);
     }
     ctx->launches++;
     return MSS_OK;
@@ -501,10 +528,15 @@ static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half
     const int npairs = (n_half - (dot_last ? 1 : 0)) / 2;
     double* cur = l.z;
     double* oth = l.s;
+    // z-slab levels: the pairs read 1 ghost plane of r and 2 of z (SURVEY §8(e) C-H1 with
+    // the halo of two half-sweeps exchanged at once)
+    TRY(do_halo(ctx, k, const_cast<double*>(r), 1));
+    if (!z_zero) TRY(do_halo(ctx, k, cur, 2));
     for (int pi = 0; pi < npairs; ++pi) {
       const int col1 = (first_colour + 2 * pi) & 1;
       TRY(op_pair(ctx, k, r, cur, oth, col1, z_zero && pi == 0));
       std::swap(cur, oth);
+      TRY(do_halo(ctx, k, cur, 2));
     }
     if (cur != l.z) {
       l.s = l.z;
@@ -516,6 +548,7 @@ static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half
       const bool first = z_zero && h == 0;
       double* dot = (h == n_half - 1 && !first) ? dot_last : nullptr;
       TRY(op_halfsweep(ctx, k, r, l.z, col, first, dot));
+      TRY(do_halo(ctx, k, l.z));
       if (dot) TRY(do_allred(ctx, k, dot));
     }
     return MSS_OK;
@@ -754,12 +787,16 @@ static int pcg_level(mss_ctx* ctx, int k) {
       ctx->launches++;
     } else if (l.txp && spmv_tma_ok(l)) {
       // TMA-fed SpMV (pairtma.cuh): faces from the padded Tx copy of this level
+      // z-slab levels: every map starts one (ghost) plane below the slab
+      const int g = l.dist ? 1 : 0;
       SpmvMaps M;
-      if (!tmap_get(ctx, &M.z, l.z, 16, l.nx, l.ny, l.nz, SpmvGeo::ZW, SpmvGeo::ZH) ||
-          !tmap_get(ctx, &M.p, pin, 16, l.nx, l.ny, l.nz, SpmvGeo::ZW, SpmvGeo::ZH) ||
-          !tmap_get(ctx, &M.tx, l.txp, 17, l.nx + 2, l.ny, l.nz, SpmvGeo::XW, SpmvGeo::TY) ||
-          !tmap_get(ctx, &M.ty, l.Ty, 18, l.nx, l.ny + 1, l.nz, SpmvGeo::W, SpmvGeo::TY + 1) ||
-          !tmap_get(ctx, &M.tz, l.Tz, 19, l.nx, l.ny, l.nz + 1, SpmvGeo::W, SpmvGeo::TY))
+      if (!tmap_get(ctx, &M.z, l.z - g * l.plane, 16, l.nx, l.ny, l.nz + 2 * g, SpmvGeo::ZW, SpmvGeo::ZH) ||
+          !tmap_get(ctx, &M.p, pin - g * l.plane, 16, l.nx, l.ny, l.nz + 2 * g, SpmvGeo::ZW, SpmvGeo::ZH) ||
+          !tmap_get(ctx, &M.tx, l.txp - g * (int64_t)(l.nx + 2) * l.ny, 17, l.nx + 2, l.ny, l.nz + 2 * g, SpmvGeo::XW,
+                    SpmvGeo::TY) ||
+          !tmap_get(ctx, &M.ty, l.Ty - g * (int64_t)l.nx * (l.ny + 1), 18, l.nx, l.ny + 1, l.nz + 2 * g, SpmvGeo::W,
+                    SpmvGeo::TY + 1) ||
+          !tmap_get(ctx, &M.tz, l.Tz - g * l.plane, 19, l.nx, l.ny, l.nz + 1 + 2 * g, SpmvGeo::W, SpmvGeo::TY))
         return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
       const int sbx = (l.nx / 2 + kPX - 1) / kPX, sby = (l.ny + SpmvGeo::TY - 1) / SpmvGeo::TY;
       const char* nce = getenv("MSS_SPMV_NCH");
@@ -783,8 +820,10 @@ static int pcg_level(mss_ctx* ctx, int k) {
       if ((int64_t)sbx * sby * snch > kMaxPartials) return set_err(MSS_EINVAL, "spmv grid too large");
       const dim3 sgrid(sbx, sby, snch), sblk(kPX, SpmvGeo::TY);
       const RedOut ro = red_to(ctx, &ds->pq, k, 0);
-      if (it == 0) k_spmv_tma<true><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro);
-      else k_spmv_tma<false><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro);
+      if (it == 0)
+        k_spmv_tma<true><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro, g);
+      else
+        k_spmv_tma<false><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro, g);
       ctx->launches++;
     } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
       k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
@@ -1116,9 +1155,11 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     l.N = l.plane * l.nz;
     for (int d = 0; d < 3; ++d) l.h[d] = ctx->extent[d] / (double)dims[k][d];
     const int64_t nfx = (int64_t)(l.nx + 1) * l.ny * l.nz, nfy = (int64_t)l.nx * (l.ny + 1) * l.nz;
-    TRY(dalloc(ctx, (void**)&l.Tx, sizeof(double) * nfx));
-    TRY(dalloc(ctx, (void**)&l.Ty, sizeof(double) * nfy));
-    if (ndim == 3) TRY(dalloc(ctx, (void**)&l.Tz, sizeof(double) * (size_t)(l.N + l.plane)));
+    (void)nfx;
+    (void)nfy;
+    TRY(falloc(ctx, l, (int64_t)(l.nx + 1) * l.ny, l.nz, &l.Tx));
+    TRY(falloc(ctx, l, (int64_t)l.nx * (l.ny + 1), l.nz, &l.Ty));
+    if (ndim == 3) TRY(falloc(ctx, l, l.plane, l.nz + 1, &l.Tz));
     TRY(valloc(ctx, l, &l.x));
     TRY(valloc(ctx, l, &l.r));
     TRY(valloc(ctx, l, &l.z));
@@ -1278,6 +1319,16 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       cudaFree(Tzext);
     }
   }
+  // ghost face planes of the distributed levels (fused pairs on z-slabs): Tx / Ty planes
+  // -1 and nz, Tz face planes -1 and nz + 1 from the neighbours
+  for (int k = 0; k < ctx->ndist; ++k) {
+    Level& l = ctx->lv[k];
+    TRY(ctx->comm->halo(ctx->stream, l.Tx, (int64_t)(l.nx + 1) * l.ny, l.nz, 1));
+    TRY(ctx->comm->halo(ctx->stream, l.Ty, (int64_t)l.nx * (l.ny + 1), l.nz, 1));
+    if (ndim == 3)
+      TRY(ctx->comm->exch(ctx->stream, l.Tz + l.plane, l.Tz - l.plane, l.Tz + (int64_t)(l.nz - 1) * l.plane,
+                          l.Tz + (int64_t)(l.nz + 1) * l.plane, (size_t)l.plane));
+  }
   // a3: dense coarsest matrix, Cholesky, inverse
   Level& lc = ctx->lv[ctx->L];
   if (lc.N > 8192) return set_err(MSS_EINVAL, "coarsest level too large for the dense solve");
@@ -1310,10 +1361,13 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     bool any = false;
     for (int k = 0; k <= ctx->L; ++k) {
       Level& l = ctx->lv[k];
-      if (!col_ok(ctx, l) || l.dist) continue;
-      const int64_t rows = (int64_t)l.ny * l.nz;
-      TRY(dalloc(ctx, (void**)&l.txp, sizeof(double) * (size_t)(rows * (l.nx + 2))));
-      LAUNCH(k_pad_tx, grid_for(rows * (l.nx + 2)), l.Tx, l.txp, l.nx, rows);
+      if (!col_ok(ctx, l)) continue;
+      const int64_t g = l.dist ? 1 : 0;   // ghost face planes (distributed levels)
+      const int64_t rows = (int64_t)l.ny * (l.nz + 2 * g);
+      double* base = nullptr;
+      TRY(dalloc(ctx, (void**)&base, sizeof(double) * (size_t)(rows * (l.nx + 2))));
+      LAUNCH(k_pad_tx, grid_for(rows * (l.nx + 2)), l.Tx - g * (int64_t)(l.nx + 1) * l.ny, base, l.nx, rows);
+      l.txp = base + g * (int64_t)(l.nx + 2) * l.ny;
       any = true;
     }
     if (any) {

@@ -85,6 +85,8 @@ struct PairCtx {
   double* zout;
   int64_t plane;
   int tx, ty, tid, lx, x0, j0, kb, ke, k0, k1, nz;
+  int gz, gf;      // TMA plane offsets of the z map and of the face / r maps (ghost planes)
+  bool bot, top;   // the slab touches the global bottom / top of the domain
   bool valid, interior;
 };
 
@@ -93,17 +95,21 @@ template <bool FIRST, class G>
 __device__ __forceinline__ void pair_issue(const PairCtx& C, int p, int s) {
   double* st = C.smd + s * G::SD;
   uint64_t* b = &C.bar[s];
-  if (p >= C.nz) {   // only the top z faces exist above the last plane
-    mbar_expect(b, G::BTz);
-    tma_load3(st + G::oTz, &C.M->tz, C.x0, C.j0, p, b);
+  if (p > C.ke) {
+    // the plane above the walk: only its z (upper neighbours; none above the global top)
+    // and its z faces (the walk's last upper faces) are read
+    const bool zx = !FIRST && !(C.top && p >= C.nz);
+    mbar_expect(b, G::BTz + (zx ? G::BZ : 0u));
+    if (zx) tma_load3(st + G::oZ, &C.M->z, C.x0 - 2, C.j0 - 1, p + C.gz, b);
+    tma_load3(st + G::oTz, &C.M->tz, C.x0, C.j0, p + C.gf, b);
     return;
   }
   mbar_expect(b, FIRST ? G::BT : G::BT + G::BZ);
-  if (!FIRST) tma_load3(st + G::oZ, &C.M->z, C.x0 - 2, C.j0 - 1, p, b);
-  tma_load3(st + G::oTx, &C.M->tx, C.x0, C.j0, p, b);
-  tma_load3(st + G::oTy, &C.M->ty, C.x0, C.j0, p, b);
-  tma_load3(st + G::oTz, &C.M->tz, C.x0, C.j0, p, b);
-  tma_load3(st + G::oR, &C.M->r, C.x0, C.j0, p, b);
+  if (!FIRST) tma_load3(st + G::oZ, &C.M->z, C.x0 - 2, C.j0 - 1, p + C.gz, b);
+  tma_load3(st + G::oTx, &C.M->tx, C.x0, C.j0, p + C.gf, b);
+  tma_load3(st + G::oTy, &C.M->ty, C.x0, C.j0, p + C.gf, b);
+  tma_load3(st + G::oTz, &C.M->tz, C.x0, C.j0, p + C.gf, b);
+  tma_load3(st + G::oR, &C.M->r, C.x0, C.j0, p + C.gf, b);
 }
 
 // One plane step u of the unrolled walk: first colour at k (parity P), barrier, refill,
@@ -140,7 +146,7 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
         const double2 zc = *reinterpret_cast<const double2*>(Z);
         const double xn = P ? Z[2] : Z[-1];
         const double ys = Z[-ZW + P], yn = Z[ZW + P];
-        const double zu = (k + 1 < C.nz) ? S1[G::oZ + (ty + 1) * ZW + lx + 2 + P] : 0.0;
+        const double zu = (!C.top || k + 1 < C.nz) ? S1[G::oZ + (ty + 1) * ZW + lx + 2 + P] : 0.0;
         const double xl = P ? zc.x : xn, xh = P ? xn : zc.y;
         acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * (P ? zdn.y : zdn.x) + t5 * zu;
         zdn = zc;
@@ -168,8 +174,8 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
     const double own = R1[0];
     const double xnb = P ? R1[1] : R1[-1];
     const double ys = R1[-kPX], yn = R1[kPX];
-    const double zl = (kp > 0) ? C.red[(Rm2 * G::TY + ty) * kPX + tx] : 0.0;
-    const double zh = (kp < C.nz - 1) ? C.red[(R0 * G::TY + ty) * kPX + tx] : 0.0;
+    const double zl = (kp > 0 || !C.bot) ? C.red[(Rm2 * G::TY + ty) * kPX + tx] : 0.0;
+    const double zh = (kp < C.nz - 1 || !C.top) ? C.red[(R0 * G::TY + ty) * kPX + tx] : 0.0;
     const double xl = P ? own : xnb, xh = P ? xnb : own;
     const double acc =
         sin.r + (sin.txl * xl + sin.txh * xh + sin.tys * ys + sin.tyn * yn + sin.tzl * zl + sin.tzh * zh);
@@ -190,10 +196,14 @@ __device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, 
   }
 }
 
+// gz / gf: plane offsets of the z map and of the face / r maps: 0 on a whole level, 2 and 1
+// on a z-slab level, whose maps start at its ghost planes; there the first colour is also
+// computed on the ghost planes -1 and nz (redundantly, from the halo-exchanged z, r and
+// faces) so the second colour of the slab's end planes needs no exchange in between.
 template <bool FIRST, class G>
 __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
     k_sweep2t_col(const __grid_constant__ PairMaps M, LevelDev L, const double* __restrict__ zin,
-                  double* __restrict__ zout, int col1, int kchunk) {
+                  double* __restrict__ zout, int col1, int kchunk, int gz, int gf) {
   extern __shared__ __align__(128) double smd[];
   PairCtx C;
   C.smd = smd;
@@ -217,8 +227,12 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
   const int i0 = 2 * m;
   C.valid = m >= 0 && i0 < nx && j >= 0 && j < ny;
   C.interior = C.valid && C.tx >= 1 && C.tx <= kPX - 2 && C.ty >= 1 && C.ty <= G::TY - 2;
-  C.kb = max(C.k0 - 1, 0);
-  C.ke = min(C.k1, C.nz - 1);
+  C.gz = gz;
+  C.gf = gf;
+  C.bot = (L.z0 == 0);
+  C.top = (L.z0 + C.nz >= L.nzg);
+  C.kb = max(C.k0 - 1, C.bot ? 0 : -1);
+  C.ke = min(C.k1, C.top ? C.nz - 1 : C.nz);
   const int np = C.ke + 2 - C.kb;   // planes kb .. ke+1 are staged
   if (C.tid == 0) {
     for (int s = 0; s < G::NS; ++s) mbar_init(&C.bar[s], 1);
@@ -230,7 +244,7 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
 
   int64_t c = C.valid ? i0 + (int64_t)nx * (j + (int64_t)ny * C.kb) : 0;
   double2 zdn = make_double2(0, 0);
-  if (!FIRST && C.valid && C.kb > 0) zdn = ld2(zin + c - C.plane);
+  if (!FIRST && C.valid && (C.kb > 0 || !C.bot)) zdn = ld2(zin + c - C.plane);
   // first-colour parity at the start of every group (warp-uniform: a warp is a row)
   const int pA = (i0 + j + L.z0 + col1 + C.kb) & 1;
   PairSec sa = {0, 0, 0, 0, 0, 0, 0}, sb = sa;
@@ -270,7 +284,7 @@ template <bool FIRST>
 __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
     k_spmv_tma(const __grid_constant__ SpmvMaps M, LevelDev L, const double* __restrict__ z,
                const double* __restrict__ pin, double* __restrict__ pout, double* __restrict__ q, const Scal* sc,
-               int kchunk, RedOut ro) {
+               int kchunk, RedOut ro, int gz) {
   using G = SpmvGeo;
   extern __shared__ __align__(128) double smd[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smd + G::NS * G::SD);
@@ -283,21 +297,28 @@ __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
   const int i0 = 2 * m, lx = 2 * tx;
   const bool valid = i0 < nx && j < ny;
   const double beta = FIRST ? 0.0 : sc->rho / sc->rho_prev;
-  // planes k0 .. k1 are staged (plane k1 for the upper neighbours / faces)
+  const bool top = (L.z0 + nz >= L.nzg);   // z-slab levels: ghost plane nz holds the neighbour's
+  // planes k0 .. k1 are staged (plane k1: only the upper neighbours' z, p and the z faces);
+  // gz: plane offset of every map (1 on a z-slab level, whose maps start at the ghost plane)
   auto issue = [&](int p) {
     const int s = (p - k0) & (G::NS - 1);
     double* st = smd + s * G::SD;
-    if (p >= nz) {
-      mbar_expect(&bar[s], G::BTz);
-      tma_load3(st + G::oTz, &M.tz, x0, j0, p, &bar[s]);
+    if (p >= k1) {
+      const bool zx = !(top && p >= nz);
+      mbar_expect(&bar[s], G::BTz + (zx ? (FIRST ? 1u : 2u) * G::BZ : 0u));
+      if (zx) {
+        tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p + gz, &bar[s]);
+        if (!FIRST) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p + gz, &bar[s]);
+      }
+      tma_load3(st + G::oTz, &M.tz, x0, j0, p + gz, &bar[s]);
       return;
     }
     mbar_expect(&bar[s], G::BT + (FIRST ? 1u : 2u) * G::BZ);
-    tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p, &bar[s]);
-    if (!FIRST) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p, &bar[s]);
-    tma_load3(st + G::oTx, &M.tx, x0, j0, p, &bar[s]);
-    tma_load3(st + G::oTy, &M.ty, x0, j0, p, &bar[s]);
-    tma_load3(st + G::oTz, &M.tz, x0, j0, p, &bar[s]);
+    tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p + gz, &bar[s]);
+    if (!FIRST) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p + gz, &bar[s]);
+    tma_load3(st + G::oTx, &M.tx, x0, j0, p + gz, &bar[s]);
+    tma_load3(st + G::oTy, &M.ty, x0, j0, p + gz, &bar[s]);
+    tma_load3(st + G::oTz, &M.tz, x0, j0, p + gz, &bar[s]);
   };
   const int np = k1 - k0 + 1;
   if (tid == 0) {
@@ -331,7 +352,7 @@ __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
     if (valid) {
       const int zo = (ty + 1) * G::ZW + lx + 2;   // own pair in the z / p tiles
       const double2 pc = make_double2(PV(S0, zo), PV(S0, zo + 1));
-      const double2 pup = (k + 1 < nz) ? make_double2(PV(S1, zo), PV(S1, zo + 1)) : make_double2(0.0, 0.0);
+      const double2 pup = (!top || k + 1 < nz) ? make_double2(PV(S1, zo), PV(S1, zo + 1)) : make_double2(0.0, 0.0);
       const double2 ps = make_double2(PV(S0, zo - G::ZW), PV(S0, zo - G::ZW + 1));
       const double2 pn = make_double2(PV(S0, zo + G::ZW), PV(S0, zo + G::ZW + 1));
       const double pl = PV(S0, zo - 1), pr = PV(S0, zo + 2);
