@@ -52,6 +52,7 @@ struct TsLevel {
   // shared-memory offsets (doubles)
   int o_tx, o_ty, o_tz, o_dg, o_x, o_r, o_z, o_p0, o_p1, o_q, o_t1, o_t2;
   int o_wx, o_wy, o_wz;     // W1 tables (3 doubles per entry) for the transfer to level+1
+  int o_tup;                // upper outer-axis faces of the top local slice (static: no DSMEM read)
   int t1_slice, t2_slice;   // elements per outer slice of t1 / t2
   int ncx, ncy, ncz;   // dims of the next level
   double thr;
@@ -175,6 +176,10 @@ struct TailSm {
       sm[l.o_tx + t] = t0;
       sm[l.o_ty + t] = t2;
       sm[l.o_tz + t] = t4;
+      // the top local slice's upper faces along the outer axis (z in 3-D, y in 2-D): read
+      // from HBM once here instead of from the next CTA's shared memory in every pass
+      const int o = (NDIM == 3) ? k : j;
+      if (o == o1 - 1) sm[l.o_tup + t - (o1 - 1 - o0) * l.P] = (NDIM == 3) ? t5 : t3;
       double d = t0 + t1 + t2 + t3;
       if (NDIM == 3) d += t4 + t5;
       sm[l.o_dg + t] = d;
@@ -218,13 +223,13 @@ struct TailSm {
     } else {
       yl = (j > 0) ? below(l, off, t, j, o0) : 0.0;
       yh = (j < l.ny - 1) ? above(l, off, t, j, o1, o0) : 0.0;
-      tyh = (j < l.ny - 1) ? above(l, l.o_ty, t, j, o1, o0) : 0.0;
+      tyh = (j < l.ny - 1) ? ((j < o1 - 1) ? sm[l.o_ty + t + l.P] : sm[l.o_tup + t - (j - o0) * l.P]) : 0.0;
     }
     double s = tx[t] * xl + txh * xh + ty[t] * yl + tyh * yh;
     if (NDIM == 3) {
       const double zl = (k > 0) ? below(l, off, t, k, o0) : 0.0;
       const double zh = (k < l.nz - 1) ? above(l, off, t, k, o1, o0) : 0.0;
-      const double tzh = (k < l.nz - 1) ? above(l, l.o_tz, t, k, o1, o0) : 0.0;
+      const double tzh = (k < l.nz - 1) ? ((k < o1 - 1) ? sm[l.o_tz + t + l.P] : sm[l.o_tup + t - (k - o0) * l.P]) : 0.0;
       s += sm[l.o_tz + t] * zl + tzh * zh;
     }
     return s;
@@ -653,6 +658,7 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
       t.o_wx = off; off += 3 * L.nx;
       t.o_wy = off; off += 3 * L.ny;
       t.o_wz = off; off += (nd == 3) ? 3 * L.nz : 0;
+      t.o_tup = off; off += t.P;
       t.gwx = reinterpret_cast<const W1*>(L.w[0]);
       t.gwy = reinterpret_cast<const W1*>(L.w[1]);
       t.gwz = reinterpret_cast<const W1*>(L.w[2]);
@@ -660,7 +666,7 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
       t.ncx = t.ncy = t.ncz = 0;
       t.o_x = off; off += t.cap;
       t.o_r = off; off += t.cap;
-      t.o_tx = t.o_ty = t.o_tz = t.o_dg = t.o_z = t.o_p0 = t.o_p1 = t.o_q = t.o_t1 = t.o_t2 = -1;
+      t.o_tx = t.o_ty = t.o_tz = t.o_dg = t.o_z = t.o_p0 = t.o_p1 = t.o_q = t.o_t1 = t.o_t2 = t.o_tup = -1;
       t.o_wx = t.o_wy = t.o_wz = -1;
       t.gwx = t.gwy = t.gwz = nullptr;
       t.t1_slice = t.t2_slice = 0;
