@@ -1155,9 +1155,6 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     l.plane = (int64_t)l.nx * l.ny;
     l.N = l.plane * l.nz;
     for (int d = 0; d < 3; ++d) l.h[d] = ctx->extent[d] / (double)dims[k][d];
-    const int64_t nfx = (int64_t)(l.nx + 1) * l.ny * l.nz, nfy = (int64_t)l.nx * (l.ny + 1) * l.nz;
-    (void)nfx;
-    (void)nfy;
     TRY(falloc(ctx, l, (int64_t)(l.nx + 1) * l.ny, l.nz, &l.Tx));
     TRY(falloc(ctx, l, (int64_t)l.nx * (l.ny + 1), l.nz, &l.Ty));
     if (ndim == 3) TRY(falloc(ctx, l, l.plane, l.nz + 1, &l.Tz));
