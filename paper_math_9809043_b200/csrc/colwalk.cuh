@@ -349,11 +349,47 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
   }
 }
 
-// a8 column-walk: z_black += (E y)_black, thread per pair walking z.
+// a8, one thread per cell pair (grid-stride, many loads in flight): z_black += (E y)_black
+// with the level's per-axis weight tables (single-GPU uniform levels), 128-bit pair access.
+// Same expression and operand order as prolong_item.
+__global__ void __launch_bounds__(256) k_prolong_pairs(LevelDev L, int ncx, int ncy, const double* __restrict__ y,
+                                                       double* __restrict__ z, const W1* __restrict__ wx,
+                                                       const W1* __restrict__ wy, const W1* __restrict__ wz) {
+  const uint32_t hx = (uint32_t)L.nx >> 1;
+  const uint32_t npair = hx * (uint32_t)L.ny * (uint32_t)L.nz;
+  const int64_t cp = (int64_t)ncx * ncy;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < npair; u += gridDim.x * blockDim.x) {
+    const uint32_t row = u / hx;
+    const uint32_t m = u - row * hx;
+    const uint32_t k = row / (uint32_t)L.ny;
+    const uint32_t j = row - k * (uint32_t)L.ny;
+    const int i0 = 2 * (int)m;
+    const int par = (i0 + (int)j + (int)k + L.z0 + 1) & 1;   // black cell: i0 + par
+    const int64_t c = i0 + (int64_t)L.nx * row;
+    double2 zc = ld2(z + c);
+    const W1 ax = wx[i0 + par], ay = wy[j], az = wz[k];
+    auto Yv = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * cc); };
+    double acc = ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0, az.I0) + ax.w1 * Yv(ax.I1, ay.I0, az.I0)) +
+                 ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1, az.I0) + ax.w1 * Yv(ax.I1, ay.I1, az.I0));
+    acc *= az.w0;
+    acc += az.w1 * (ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0, az.I1) + ax.w1 * Yv(ax.I1, ay.I0, az.I1)) +
+                    ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1, az.I1) + ax.w1 * Yv(ax.I1, ay.I1, az.I1)));
+    if (par) zc.y += acc;
+    else zc.x += acc;
+    *reinterpret_cast<double2*>(z + c) = zc;
+  }
+}
+
+// a8 column-walk: z_black += (E y)_black, thread per pair walking z.  Per coarse plane Z the
+// x-y interpolated values of both cells of the pair, P_a(Z) and P_b(Z), are formed once and
+// carried (the fine walk revisits each coarse plane ~s times); the black cell then gets
+// w_z0 P(Z0) + w_z1 P(Z1) — the same expressions, in the same order, as prolong_item.  The
+// pair is read / written with one 128-bit access and the next plane's pair is loaded ahead.
 template <int MINB>
 __global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L, int ncx, int ncy, int ncz, int s,
                                                                       int kind, const double* __restrict__ y,
-                                                                      double* __restrict__ z, int kchunk, int zc0) {
+                                                                      double* __restrict__ z, int kchunk, int zc0,
+                                                                      const W1* __restrict__ wz = nullptr) {
   const int m = blockIdx.x * kColX + threadIdx.x;
   const int j = blockIdx.y * kColY + threadIdx.y;
   const int k0 = blockIdx.z * kchunk;
@@ -369,21 +405,52 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_prolong_col(LevelDev L,
   interp_w(i0 + 1, ncx, rx, kind, Xb0, wxb0, Xb1, wxb1);
   interp_w(j, ncy, ry, kind, Y0, wy0, Y1, wy1);
   const int64_t cp = (int64_t)ncx * ncy;
+  const double* yr0 = y + (int64_t)ncx * Y0;
+  const double* yr1 = y + (int64_t)ncx * Y1;
+  // x-y interpolated coarse value of cell a / b on coarse plane Zc (same operand order as
+  // the bracket of prolong_item)
+  auto Pxy = [&](int Zc, double& pa, double& pb) {
+    const int64_t zo = cp * (Zc - zc0);
+    const double a00 = __ldg(yr0 + zo + Xa0), a10 = __ldg(yr0 + zo + Xa1);
+    const double a01 = __ldg(yr1 + zo + Xa0), a11 = __ldg(yr1 + zo + Xa1);
+    const double b00 = __ldg(yr0 + zo + Xb0), b10 = __ldg(yr0 + zo + Xb1);
+    const double b01 = __ldg(yr1 + zo + Xb0), b11 = __ldg(yr1 + zo + Xb1);
+    pa = wy0 * (wxa0 * a00 + wxa1 * a10) + wy1 * (wxa0 * a01 + wxa1 * a11);
+    pb = wy0 * (wxb0 * b00 + wxb1 * b10) + wy1 * (wxb0 * b01 + wxb1 * b11);
+  };
   int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
+  int Zc0 = -1, Zc1 = -1;             // cached coarse planes
+  double pa0 = 0, pb0 = 0, pa1 = 0, pb1 = 0;
+  double2 zc = ld2(z + c);
   for (int k = k0; k < k1; ++k) {
-    const int par = (i0 + j + k + L.z0 + 1) & 1;
-    const int X0 = par ? Xb0 : Xa0, X1 = par ? Xb1 : Xa1;
-    const double wx0 = par ? wxb0 : wxa0, wx1 = par ? wxb1 : wxa1;
+    const double2 znext = (k + 1 < k1) ? ld2(z + c + L.plane) : make_double2(0, 0);
+    const int par = (i0 + j + k + L.z0 + 1) & 1;   // black cell of the pair: i0 + par
     int Z0, Z1;
     double wz0, wz1;
-    interp_w(k + L.z0, ncz, rz, kind, Z0, wz0, Z1, wz1);
-    auto Yv = [&](int a, int bb, int cc) { return __ldg(y + a + (int64_t)ncx * bb + cp * (cc - zc0)); };
-    double acc = wy0 * (wx0 * Yv(X0, Y0, Z0) + wx1 * Yv(X1, Y0, Z0)) +
-                 wy1 * (wx0 * Yv(X0, Y1, Z0) + wx1 * Yv(X1, Y1, Z0));
+    if (wz) {   // the level's z weight table (single-GPU levels): one broadcast load
+      const W1 e = wz[k];
+      Z0 = e.I0; Z1 = e.I1; wz0 = e.w0; wz1 = e.w1;
+      if (Z1 == Z0) Z1 = Z0, wz1 = 0.0;
+    } else {
+      interp_w(k + L.z0, ncz, rz, kind, Z0, wz0, Z1, wz1);
+    }
+    double qa0, qb0, qa1, qb1;
+    if (Z0 == Zc0) { qa0 = pa0; qb0 = pb0; }
+    else if (Z0 == Zc1) { qa0 = pa1; qb0 = pb1; }
+    else Pxy(Z0, qa0, qb0);
+    if (Z1 == Z0) { qa1 = qa0; qb1 = qb0; }
+    else if (Z1 == Zc1) { qa1 = pa1; qb1 = pb1; }
+    else if (Z1 == Zc0) { qa1 = pa0; qb1 = pb0; }
+    else Pxy(Z1, qa1, qb1);
+    Zc0 = Z0; pa0 = qa0; pb0 = qb0;
+    Zc1 = Z1; pa1 = qa1; pb1 = qb1;
+    double acc = par ? qb0 : qa0;
     acc *= wz0;
-    acc += wz1 * (wy0 * (wx0 * Yv(X0, Y0, Z1) + wx1 * Yv(X1, Y0, Z1)) +
-                  wy1 * (wx0 * Yv(X0, Y1, Z1) + wx1 * Yv(X1, Y1, Z1)));
-    z[c + par] += acc;
+    acc += wz1 * (par ? qb1 : qa1);
+    if (par) zc.y += acc;
+    else zc.x += acc;
+    *reinterpret_cast<double2*>(z + c) = zc;
+    zc = znext;
     c += L.plane;
   }
 }

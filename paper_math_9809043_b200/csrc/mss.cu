@@ -668,9 +668,17 @@ static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int c
     ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
     dim3 cgrid;
     int kch = 0;
-    if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && col_grid((const void*)k_prolong_col<4>, f, &cgrid, &kch)) {
-      k_prolong_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(f.dev(), c.nx, c.ny, nczg, ctx->prm.scale,
-                                                                       ctx->prm.interp, y, z, kch, zc0);
+    const char* pve = getenv("MSS_PROLONG_PAIRS");
+    if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && !dist_level(ctx, k) && f.w[0] && f.w[1] && f.w[2] &&
+        (pve ? atoi(pve) != 0 : true) && (int64_t)(f.nx / 2) * f.ny * f.nz < ((int64_t)1 << 32)) {
+      const int64_t np = (int64_t)(f.nx / 2) * f.ny * f.nz;
+      LAUNCH(k_prolong_pairs, grid_for(np), f.dev(), c.nx, c.ny, y, z, reinterpret_cast<const W1*>(f.w[0]),
+             reinterpret_cast<const W1*>(f.w[1]), reinterpret_cast<const W1*>(f.w[2]));
+    } else if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && col_grid((const void*)k_prolong_col<3>, f, &cgrid, &kch)) {
+      // single-GPU levels read the z weights from the level's table (same rule as interp_w)
+      const W1* wzt = (!dist_level(ctx, k) && f.w[2]) ? reinterpret_cast<const W1*>(f.w[2]) : nullptr;
+      k_prolong_col<3><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(f.dev(), c.nx, c.ny, nczg, ctx->prm.scale,
+                                                                       ctx->prm.interp, y, z, kch, zc0, wzt);
       ctx->launches++;
     } else if (colour == 1) {
       const int64_t work = (int64_t)((f.nx + 1) / 2) * f.ny * f.nz;
