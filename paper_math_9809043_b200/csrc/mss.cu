@@ -299,12 +299,21 @@ static int op_dot(mss_ctx* ctx, int level, int64_t n, const double* a, const dou
   return do_allred(ctx, level, out);
 }
 
+static int spmv_tma_launch(mss_ctx* ctx, int k, bool residual, bool first, const double* zx, const double* pb,
+                           double* pout, double* qr, RedOut ro);
+static bool spmv_tma_ok(const Level& l);
+
 static int op_residual(mss_ctx* ctx, int k, const double* b, const double* x, double* r, double* rr_out) {
   Level& l = ctx->lv[k];
   RedOut ro = red_to(ctx, rr_out, k, 0);
   {
     ProfScope ps(ctx, KC_RESID, k, cell_bytes(ctx, KC_RESID) * l.N);
-    DISPATCH(ctx->ndim, k_residual, grid_for(l.N), l.dev(), b, x, r, ro);
+    // the SpMV's TMA kernel in residual mode where it runs (x's ghost planes are current)
+    if (b && l.txp && spmv_tma_ok(l)) {
+      TRY(spmv_tma_launch(ctx, k, true, true, x, b, nullptr, r, ro));
+    } else {
+      DISPATCH(ctx->ndim, k_residual, grid_for(l.N), l.dev(), b, x, r, ro);
+    }
   }
   return rr_out ? do_allred(ctx, k, rr_out) : MSS_OK;
 }
@@ -410,6 +419,54 @@ static bool spmv_tma_ok(const Level& l) {
   const char* e = getenv("MSS_SPMV_TMA");
   if (e) return atoi(e) != 0;
   return pair_tma_on();
+}
+
+// TMA direction + SpMV + p.q (pairtma.cuh), or in residual mode r = b - A x (+ ||r||^2):
+// zx = z (x), pb = p_in (b), pout (unused for the residual), qr = q (r).
+static int spmv_tma_launch(mss_ctx* ctx, int k, bool residual, bool first, const double* zx, const double* pb,
+                           double* pout, double* qr, RedOut ro) {
+  Level& l = ctx->lv[k];
+  // z-slab levels: every map starts one (ghost) plane below the slab
+  const int g = l.dist ? 1 : 0;
+  SpmvMaps M;
+  if (!tmap_get(ctx, &M.z, zx - g * l.plane, 16, l.nx, l.ny, l.nz + 2 * g, SpmvGeo::ZW, SpmvGeo::ZH) ||
+      !tmap_get(ctx, &M.p, pb - g * l.plane, 16, l.nx, l.ny, l.nz + 2 * g, SpmvGeo::ZW, SpmvGeo::ZH) ||
+      !tmap_get(ctx, &M.tx, l.txp - g * (int64_t)(l.nx + 2) * l.ny, 17, l.nx + 2, l.ny, l.nz + 2 * g, SpmvGeo::XW,
+                SpmvGeo::TY) ||
+      !tmap_get(ctx, &M.ty, l.Ty - g * (int64_t)l.nx * (l.ny + 1), 18, l.nx, l.ny + 1, l.nz + 2 * g, SpmvGeo::W,
+                SpmvGeo::TY + 1) ||
+      !tmap_get(ctx, &M.tz, l.Tz - g * l.plane, 19, l.nx, l.ny, l.nz + 1 + 2 * g, SpmvGeo::W, SpmvGeo::TY))
+    return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
+  const int sbx = (l.nx / 2 + kPX - 1) / kPX, sby = (l.ny + SpmvGeo::TY - 1) / SpmvGeo::TY;
+  const char* nce = getenv("MSS_SPMV_NCH");
+  int snch = 1;
+  if (nce) {
+    snch = std::max(1, atoi(nce));
+  } else {
+    const int64_t tiles = (int64_t)sbx * sby;
+    int64_t best = -1;
+    for (int cc = 1; cc <= std::min(32, l.nz); ++cc) {
+      const int64_t kc = (l.nz + cc - 1) / cc;
+      const int64_t cost = ((tiles * cc + kSMs - 1) / kSMs) * (kc + 5);
+      if (best < 0 || cost < best) {
+        best = cost;
+        snch = cc;
+      }
+    }
+  }
+  int skch = (l.nz + snch - 1) / snch;
+  snch = (l.nz + skch - 1) / skch;
+  if ((int64_t)sbx * sby * snch > kMaxPartials) return set_err(MSS_EINVAL, "spmv grid too large");
+  const dim3 sgrid(sbx, sby, snch), sblk(kPX, SpmvGeo::TY);
+  Scal* ds = ctx->dscal + k;
+  if (residual)
+    k_spmv_tma<true, true><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), zx, pb, pout, qr, ds, skch, ro, g);
+  else if (first)
+    k_spmv_tma<true><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), zx, pb, pout, qr, ds, skch, ro, g);
+  else
+    k_spmv_tma<false><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), zx, pb, pout, qr, ds, skch, ro, g);
+  ctx->launches++;
+  return MSS_OK;
 }
 
 // Temporally fused pair of half-sweeps (colour col1 then the other) zin -> zout.
@@ -795,45 +852,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
                                                                        red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
       ctx->launches++;
     } else if (l.txp && spmv_tma_ok(l)) {
-      // TMA-fed SpMV (pairtma.cuh): faces from the padded Tx copy of this level
-      // z-slab levels: every map starts one (ghost) plane below the slab
-      const int g = l.dist ? 1 : 0;
-      SpmvMaps M;
-      if (!tmap_get(ctx, &M.z, l.z - g * l.plane, 16, l.nx, l.ny, l.nz + 2 * g, SpmvGeo::ZW, SpmvGeo::ZH) ||
-          !tmap_get(ctx, &M.p, pin - g * l.plane, 16, l.nx, l.ny, l.nz + 2 * g, SpmvGeo::ZW, SpmvGeo::ZH) ||
-          !tmap_get(ctx, &M.tx, l.txp - g * (int64_t)(l.nx + 2) * l.ny, 17, l.nx + 2, l.ny, l.nz + 2 * g, SpmvGeo::XW,
-                    SpmvGeo::TY) ||
-          !tmap_get(ctx, &M.ty, l.Ty - g * (int64_t)l.nx * (l.ny + 1), 18, l.nx, l.ny + 1, l.nz + 2 * g, SpmvGeo::W,
-                    SpmvGeo::TY + 1) ||
-          !tmap_get(ctx, &M.tz, l.Tz - g * l.plane, 19, l.nx, l.ny, l.nz + 1 + 2 * g, SpmvGeo::W, SpmvGeo::TY))
-        return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
-      const int sbx = (l.nx / 2 + kPX - 1) / kPX, sby = (l.ny + SpmvGeo::TY - 1) / SpmvGeo::TY;
-      const char* nce = getenv("MSS_SPMV_NCH");
-      int snch = 1;
-      if (nce) {
-        snch = std::max(1, atoi(nce));
-      } else {
-        const int64_t tiles = (int64_t)sbx * sby;
-        int64_t best = -1;
-        for (int cc = 1; cc <= std::min(32, l.nz); ++cc) {
-          const int64_t kc = (l.nz + cc - 1) / cc;
-          const int64_t cost = ((tiles * cc + kSMs - 1) / kSMs) * (kc + 5);
-          if (best < 0 || cost < best) {
-            best = cost;
-            snch = cc;
-          }
-        }
-      }
-      int skch = (l.nz + snch - 1) / snch;
-      snch = (l.nz + skch - 1) / skch;
-      if ((int64_t)sbx * sby * snch > kMaxPartials) return set_err(MSS_EINVAL, "spmv grid too large");
-      const dim3 sgrid(sbx, sby, snch), sblk(kPX, SpmvGeo::TY);
-      const RedOut ro = red_to(ctx, &ds->pq, k, 0);
-      if (it == 0)
-        k_spmv_tma<true><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro, g);
-      else
-        k_spmv_tma<false><<<sgrid, sblk, SpmvGeo::SMEM, ctx->stream>>>(M, l.dev(), l.z, pin, pout, l.q, ds, skch, ro, g);
-      ctx->launches++;
+      TRY(spmv_tma_launch(ctx, k, false, it == 0, l.z, pin, pout, l.q, red_to(ctx, &ds->pq, k, 0)));
     } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
       k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
                                                                  kch, red_to(ctx, &ds->pq, k, 0));
@@ -1383,6 +1402,7 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
+      CK(cudaFuncSetAttribute(k_spmv_tma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
     }
   }
   TRY(tail_setup(ctx));

@@ -280,11 +280,14 @@ struct SpmvMaps {
   CUtensorMap z, p, tx, ty, tz;
 };
 
-template <bool FIRST>
+// RES: the residual r = b - A x (+ ||r||^2 when ro.out) instead — z = x, p = b (its own
+// cells only), q = r, pout unused — the same per-cell expressions as the SpMV with p = x.
+template <bool FIRST, bool RES = false>
 __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
     k_spmv_tma(const __grid_constant__ SpmvMaps M, LevelDev L, const double* __restrict__ z,
                const double* __restrict__ pin, double* __restrict__ pout, double* __restrict__ q, const Scal* sc,
                int kchunk, RedOut ro, int gz) {
+  static_assert(!RES || FIRST, "the residual forms p = x");
   using G = SpmvGeo;
   extern __shared__ __align__(128) double smd[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smd + G::NS * G::SD);
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
   const int i0 = 2 * m, lx = 2 * tx;
   const bool valid = i0 < nx && j < ny;
   const double beta = FIRST ? 0.0 : sc->rho / sc->rho_prev;
+  constexpr bool LOADP = !FIRST || RES;   // stage the p_in (or b) tile
   const bool top = (L.z0 + nz >= L.nzg);   // z-slab levels: ghost plane nz holds the neighbour's
   // planes k0 .. k1 are staged (plane k1: only the upper neighbours' z, p and the z faces);
   // gz: plane offset of every map (1 on a z-slab level, whose maps start at the ghost plane)
@@ -305,17 +309,16 @@ __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
     double* st = smd + s * G::SD;
     if (p >= k1) {
       const bool zx = !(top && p >= nz);
-      mbar_expect(&bar[s], G::BTz + (zx ? (FIRST ? 1u : 2u) * G::BZ : 0u));
-      if (zx) {
-        tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p + gz, &bar[s]);
-        if (!FIRST) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p + gz, &bar[s]);
-      }
+      const bool px = zx && !FIRST;   // b is read at own cells only: not above the walk
+      mbar_expect(&bar[s], G::BTz + (zx ? G::BZ : 0u) + (px ? G::BZ : 0u));
+      if (zx) tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p + gz, &bar[s]);
+      if (px) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p + gz, &bar[s]);
       tma_load3(st + G::oTz, &M.tz, x0, j0, p + gz, &bar[s]);
       return;
     }
-    mbar_expect(&bar[s], G::BT + (FIRST ? 1u : 2u) * G::BZ);
+    mbar_expect(&bar[s], G::BT + (LOADP ? 2u : 1u) * G::BZ);
     tma_load3(st + G::oZ, &M.z, x0 - 2, j0 - 1, p + gz, &bar[s]);
-    if (!FIRST) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p + gz, &bar[s]);
+    if (LOADP) tma_load3(st + G::oP, &M.p, x0 - 2, j0 - 1, p + gz, &bar[s]);
     tma_load3(st + G::oTx, &M.tx, x0, j0, p + gz, &bar[s]);
     tma_load3(st + G::oTy, &M.ty, x0, j0, p + gz, &bar[s]);
     tma_load3(st + G::oTz, &M.tz, x0, j0, p + gz, &bar[s]);
@@ -368,16 +371,23 @@ __global__ void __launch_bounds__(kPX * SpmvGeo::TY, 1)
       const double s0v = tx0 * pl + tx1 * pc.y + tyl.x * ps.x + tyu.x * pn.x + tzl.x * pdn.x + tzu.x * pup.x;
       const double s1v = tx1 * pc.x + tx2 * pr + tyl.y * ps.y + tyu.y * pn.y + tzl.y * pdn.y + tzu.y * pup.y;
       const double q0 = d0 * pc.x - s0v, q1 = d1 * pc.y - s1v;
-      *reinterpret_cast<double2*>(pout + c) = pc;
-      *reinterpret_cast<double2*>(q + c) = make_double2(q0, q1);
-      acc += pc.x * q0 + pc.y * q1;
+      if (RES) {
+        const double2 bb = *reinterpret_cast<const double2*>(S0 + G::oP + zo);
+        const double r0 = bb.x - q0, r1 = bb.y - q1;
+        *reinterpret_cast<double2*>(q + c) = make_double2(r0, r1);
+        acc += r0 * r0 + r1 * r1;
+      } else {
+        *reinterpret_cast<double2*>(pout + c) = pc;
+        *reinterpret_cast<double2*>(q + c) = make_double2(q0, q1);
+        acc += pc.x * q0 + pc.y * q1;
+      }
       pdn = pc;
       c += plane;
     }
     __syncthreads();   // plane k's slot is free: refill it with plane k+4
     if (tid == 0 && k + G::NS <= k1) issue(k + G::NS);
   }
-  grid_sum_finish(acc, ro);
+  if (!RES || ro.out) grid_sum_finish(acc, ro);
 }
 
 // Txp: Tx with row pitch n_x + 2 (faces 0..n_x, one zero pad) so TMA can describe it.
