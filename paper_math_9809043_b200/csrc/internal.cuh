@@ -58,6 +58,7 @@ struct Level {
   double h[3] = {1, 1, 1};
   double *Tx = nullptr, *Ty = nullptr, *Tz = nullptr;
   double* txp = nullptr;                 // Tx with row pitch nx+2 for the TMA pair kernel (pairtma.cuh)
+  double* resb = nullptr;                // black residual per cell pair (fused closing sweep + residual)
   // ghosted cell vectors (interior pointers)
   double *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *b = nullptr, *s = nullptr;
   double *p[2] = {nullptr, nullptr};

@@ -484,7 +484,8 @@ static bool pair_ok(const mss_ctx* ctx, int k) {
   return mode == 1 || l.N >= ((int64_t)1 << 24);
 }
 
-static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, double* zout, int col1, bool first) {
+static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, double* zout, int col1, bool first,
+                   bool res = false) {
   Level& l = ctx->lv[k];
   const int hx = l.nx / 2;
   const int bx = (hx + kPX - 3) / (kPX - 2), by = (l.ny + kPY - 3) / (kPY - 2);
@@ -533,7 +534,14 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     const int tkch = (l.nz + tnch - 1) / tnch;
     tnch = (l.nz + tkch - 1) / tkch;
     const dim3 tgrid(bx, tby, tnch), tblk(kPX, TY);
-    if (big) {
+    if (res) {
+      if (big)
+        k_sweep2t_col<false, PairBig, true><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch,
+                                                                                       gz, gf, l.resb);
+      else
+        k_sweep2t_col<false, PairSmall, true><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1,
+                                                                                           tkch, gz, gf, l.resb);
+    } else if (big) {
       if (first)
         k_sweep2t_col<true, PairBig><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch, gz, gf);
       else
@@ -767,13 +775,44 @@ static int read_scal(mss_ctx* ctx, int k) {
 static int pcg_level(mss_ctx* ctx, int k);
 
 // z_k = M_k^{-1} r_k  (Eq. 2.10 as the smoothing / coarse-correction sequence)
+// a5 + a6 of the pre-smoothing: 2m+1 half-sweeps from z = 0, then b_{k+1} = R (r - A z).
+// On TMA pair levels the closing red half-sweep and the black residual run in one fused
+// pass (the residual stored per cell pair, 4 B/cell), then the x-, y- and z-restrictions.
+static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
+  Level& l = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  const char* fe = getenv("MSS_FUSED_RESID");
+  const bool fused = sgs && nh >= 3 && (nh & 1) && l.resb && l.w[0] && l.uniform && !dist_level(ctx, k) &&
+                     (size_t)(l.nx / 2) * (5 * sizeof(double) + 4 * sizeof(int)) <= 48 * 1024 && pair_ok(ctx, k) &&
+                     l.txp && pair_tma_on() && (fe ? atoi(fe) != 0 : true);
+  if (!fused) {
+    TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));
+    return op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs);
+  }
+  TRY(op_smooth(ctx, k, l.r, l.z, nh - 1, 0, true));            // (nh-1)/2 pairs, z in l.z
+  {
+    ProfScope ps(ctx, KC_RESID, k, (8.0 * (ctx->ndim + 3) + 4.0) * l.N);
+    TRY(op_pair(ctx, k, l.r, l.z, l.s, 0, false, true));        // closing red sweep + black residual
+  }
+  std::swap(l.z, l.s);
+  tail_mark_dirty(ctx);
+  {
+    ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.nx * l.ny * l.nz);
+    const int kper = 16;
+    const size_t xshm = (size_t)(l.nx / 2) * (5 * sizeof(double) + 4 * sizeof(int));
+    k_restrict_x_black<<<dim3(l.ny, (l.nz + kper - 1) / kper), 128, xshm, ctx->stream>>>(
+        l.dev(), l.resb, l.t1, c.nx, ctx->prm.scale, reinterpret_cast<const W1*>(l.w[0]), kper);
+    ctx->launches++;
+  }
+  return op_restrict_yz(ctx, k, c.r);
+}
+
 static int precond(mss_ctx* ctx, int k) {
   Level& l = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   const int nh = 2 * ctx->prm.m + 1;
-  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));                 // pre-smoothing (a5)
   const int sgs = ctx->prm.splitting == 0;
-  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs));            // b_{k+1} = R (r - A z) (a6)
+  TRY(presmooth_restrict(ctx, k, nh, sgs));                      // pre-smoothing (a5) + R (r - A z) (a6)
   if (k + 1 == ctx->L) {                                         // coarsest: exact (a7)
     TRY(op_coarse_solve(ctx, c.r, c.x));
     ctx->info.iters[k + 1] += 1;
@@ -803,8 +842,7 @@ static int precond_tatebe(mss_ctx* ctx, int k) {
   Level& c = ctx->lv[k + 1];
   const int nh = 2 * ctx->prm.m + 1;
   const int sgs = ctx->prm.splitting == 0;
-  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));
-  TRY(op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs));
+  TRY(presmooth_restrict(ctx, k, nh, sgs));
   TRY(precond_tatebe(ctx, k + 1));
   TRY(op_prolong_add(ctx, k, c.z, l.z, sgs ? 1 : -1));
   return op_smooth(ctx, k, l.r, l.z, nh, 0, false, k == 0 ? &ctx->dscal[0].rho : nullptr);
@@ -1393,6 +1431,7 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       TRY(dalloc(ctx, (void**)&base, sizeof(double) * (size_t)(rows * (l.nx + 2))));
       LAUNCH(k_pad_tx, grid_for(rows * (l.nx + 2)), l.Tx - g * (int64_t)(l.nx + 1) * l.ny, base, l.nx, rows);
       l.txp = base + g * (int64_t)(l.nx + 2) * l.ny;
+      if (!l.dist) TRY(dalloc(ctx, (void**)&l.resb, sizeof(double) * (size_t)(l.N / 2)));
       any = true;
     }
     if (any) {
@@ -1400,6 +1439,9 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairBig::SMEM));
       CK(cudaFuncSetAttribute(k_sweep2t_col<true, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairBig, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairBig::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)PairSmall::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));

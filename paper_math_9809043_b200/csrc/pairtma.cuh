@@ -83,6 +83,7 @@ struct PairCtx {
   uint64_t* bar;
   const PairMaps* M;
   double* zout;
+  double* resB;    // RES: black residual per cell pair
   int64_t plane;
   int tx, ty, tid, lx, x0, j0, kb, ke, k0, k1, nz;
   int gz, gf;      // TMA plane offsets of the z map and of the face / r maps (ghost planes)
@@ -112,12 +113,24 @@ __device__ __forceinline__ void pair_issue(const PairCtx& C, int p, int s) {
   tma_load3(st + G::oR, &C.M->r, C.x0, C.j0, p + C.gf, b);
 }
 
+// RES variant: the second step keeps the old z of the second-colour cell (zo)
+template <bool RES>
+struct PairSecT : PairSec {};
+template <>
+struct PairSecT<true> : PairSec {
+  double zo;
+};
+
 // One plane step u of the unrolled walk: first colour at k (parity P), barrier, refill,
 // second colour at k-1 (its colour is then P as well).  Stage slot u % NS and ring slot u are
 // compile-time; sin holds plane k-1's second-colour cell, sout gets plane k's.
-template <bool FIRST, class G, int U, int P>
-__device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, double2& zdn, const PairSec& sin,
-                                          PairSec& sout) {
+// RES (a5's closing half-sweep fused with a6): the first colour is the closing red sweep;
+// the second step leaves the black cell unchanged and writes its residual r - A z (the red
+// residual is zero after the sweep) to resB, one value per cell pair, in the
+// operand order of k_resid_restrict_col.
+template <bool FIRST, class G, int U, int P, bool RES = false>
+__device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, double2& zdn,
+                                          const PairSecT<RES>& sin, PairSecT<RES>& sout) {
   if (k > C.ke + 1) return;   // block-uniform
   constexpr int S0i = U % G::NS, S1i = (U + 1) % G::NS;
   constexpr int R0 = U, Rm1 = (U + G::RN - 1) % G::RN, Rm2 = (U + G::RN - 2) % G::RN;
@@ -150,6 +163,7 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
         const double xl = P ? zc.x : xn, xh = P ? xn : zc.y;
         acc += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * (P ? zdn.y : zdn.x) + t5 * zu;
         zdn = zc;
+        if constexpr (RES) sout.zo = P ? zc.x : zc.y;   // the other cell's z (unchanged)
       }
       v1 = acc / (txl + txh + t2 + t3 + t4 + t5);
       sout.txl = P ? t01.x : t01.y;   // the other cell of the pair
@@ -177,22 +191,29 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
     const double zl = (kp > 0 || !C.bot) ? C.red[(Rm2 * G::TY + ty) * kPX + tx] : 0.0;
     const double zh = (kp < C.nz - 1 || !C.top) ? C.red[(R0 * G::TY + ty) * kPX + tx] : 0.0;
     const double xl = P ? own : xnb, xh = P ? xnb : own;
-    const double acc =
-        sin.r + (sin.txl * xl + sin.txh * xh + sin.tys * ys + sin.tyn * yn + sin.tzl * zl + sin.tzh * zh);
-    const double v2 = acc / (sin.txl + sin.txh + sin.tys + sin.tyn + sin.tzl + sin.tzh);
-    *reinterpret_cast<double2*>(C.zout + c - C.plane) = P ? make_double2(own, v2) : make_double2(v2, own);
+    if constexpr (RES) {
+      const double nb = sin.txl * xl + sin.txh * xh + sin.tys * ys + sin.tyn * yn + sin.tzl * zl + sin.tzh * zh;
+      const double res = sin.r - ((sin.txl + sin.txh + sin.tys + sin.tyn + sin.tzl + sin.tzh) * sin.zo - nb);
+      *reinterpret_cast<double2*>(C.zout + c - C.plane) = P ? make_double2(own, sin.zo) : make_double2(sin.zo, own);
+      C.resB[(c - C.plane) >> 1] = res;
+    } else {
+      const double acc =
+          sin.r + (sin.txl * xl + sin.txh * xh + sin.tys * ys + sin.tyn * yn + sin.tzl * zl + sin.tzh * zh);
+      const double v2 = acc / (sin.txl + sin.txh + sin.tys + sin.tyn + sin.tzl + sin.tzh);
+      *reinterpret_cast<double2*>(C.zout + c - C.plane) = P ? make_double2(own, v2) : make_double2(v2, own);
+    }
   }
   if (k <= C.ke) c += C.plane;
 }
 
 // UN consecutive plane steps starting at parity p0 (sa / sb ping-pong the second-colour state)
-template <bool FIRST, class G, int P0, int U = 0>
-__device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, double2& zdn, PairSec& sa,
-                                           PairSec& sb) {
+template <bool FIRST, class G, int P0, bool RES, int U = 0>
+__device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, double2& zdn, PairSecT<RES>& sa,
+                                           PairSecT<RES>& sb) {
   if constexpr (U < G::UN) {
-    if constexpr ((U & 1) == 0) pair_step<FIRST, G, U, P0 ^ (U & 1)>(C, k + U, c, zdn, sa, sb);
-    else pair_step<FIRST, G, U, P0 ^ (U & 1)>(C, k + U, c, zdn, sb, sa);
-    pair_group<FIRST, G, P0, U + 1>(C, k, c, zdn, sa, sb);
+    if constexpr ((U & 1) == 0) pair_step<FIRST, G, U, P0 ^ (U & 1), RES>(C, k + U, c, zdn, sa, sb);
+    else pair_step<FIRST, G, U, P0 ^ (U & 1), RES>(C, k + U, c, zdn, sb, sa);
+    pair_group<FIRST, G, P0, RES, U + 1>(C, k, c, zdn, sa, sb);
   }
 }
 
@@ -200,10 +221,11 @@ __device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, 
 // on a z-slab level, whose maps start at its ghost planes; there the first colour is also
 // computed on the ghost planes -1 and nz (redundantly, from the halo-exchanged z, r and
 // faces) so the second colour of the slab's end planes needs no exchange in between.
-template <bool FIRST, class G>
+template <bool FIRST, class G, bool RES = false>
 __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
     k_sweep2t_col(const __grid_constant__ PairMaps M, LevelDev L, const double* __restrict__ zin,
-                  double* __restrict__ zout, int col1, int kchunk, int gz, int gf) {
+                  double* __restrict__ zout, int col1, int kchunk, int gz, int gf, double* __restrict__ resB = nullptr) {
+  static_assert(!(RES && FIRST), "the fused residual follows a sweep from a nonzero z");
   extern __shared__ __align__(128) double smd[];
   PairCtx C;
   C.smd = smd;
@@ -211,6 +233,7 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
   C.bar = reinterpret_cast<uint64_t*>(C.red + G::RN * G::TY * kPX);
   C.M = &M;
   C.zout = zout;
+  C.resB = resB;
   C.tx = threadIdx.x;
   C.ty = threadIdx.y;
   C.tid = C.ty * kPX + C.tx;
@@ -247,11 +270,61 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
   if (!FIRST && C.valid && (C.kb > 0 || !C.bot)) zdn = ld2(zin + c - C.plane);
   // first-colour parity at the start of every group (warp-uniform: a warp is a row)
   const int pA = (i0 + j + L.z0 + col1 + C.kb) & 1;
-  PairSec sa = {0, 0, 0, 0, 0, 0, 0}, sb = sa;
+  PairSecT<RES> sa{}, sb{};
   mbar_wait(&C.bar[0], 0);
   for (int k = C.kb; k <= C.ke + 1; k += G::UN) {
-    if (pA) pair_group<FIRST, G, 1>(C, k, c, zdn, sa, sb);
-    else pair_group<FIRST, G, 0>(C, k, c, zdn, sa, sb);
+    if (pA) pair_group<FIRST, G, 1, RES>(C, k, c, zdn, sa, sb);
+    else pair_group<FIRST, G, 0, RES>(C, k, c, zdn, sa, sb);
+  }
+}
+
+// a6 after the fused sweep: t1[I, j, k] = sum over the pairs q of I's window of the black
+// cell's weight to I times resB[q] — the pair-major order of k_resid_restrict_col.  One CTA
+// per fine row j and group of `kper` planes: the black cells' weight entries (one table per
+// row parity) and each row's residuals are staged in shared memory with coalesced loads
+// (reading them straight from L1 at the windows' strides saturated the L1 pipe).
+__global__ void __launch_bounds__(128) k_restrict_x_black(LevelDev L, const double* __restrict__ resB,
+                                                          double* __restrict__ t1, int ncx, int s,
+                                                          const W1* __restrict__ wx, int kper) {
+  extern __shared__ double shx[];
+  const int nx = L.nx, hx = nx >> 1;
+  double* w0s = shx;              // [2][hx]
+  double* w1s = w0s + 2 * hx;     // [2][hx]
+  double* rbs = w1s + 2 * hx;     // [hx]
+  int* i0s = reinterpret_cast<int*>(rbs + hx);   // [2][hx]
+  int* i1s = i0s + 2 * hx;                        // [2][hx]
+  for (int e = threadIdx.x; e < 2 * hx; e += blockDim.x) {
+    const int pb = e / hx, q = e - pb * hx;
+    const W1 w = wx[2 * q + pb];   // the level's x weight table (w1 = 0 when I1 == I0)
+    w0s[e] = w.w0;
+    w1s[e] = w.w1;
+    i0s[e] = w.I0;
+    i1s[e] = w.I1;
+  }
+  const int j = blockIdx.x;
+  const int kend = min(L.nz, (int)(blockIdx.y + 1) * kper);
+  for (int k = blockIdx.y * kper; k < kend; ++k) {
+    const int64_t row = j + (int64_t)L.ny * k;
+    const int pb = (j + k + L.z0 + 1) & 1;   // the black cell of every pair of this row: 2q + pb
+    const double* rb = resB + row * hx;
+    __syncthreads();   // the previous row's readers are done (and the tables are in)
+    for (int q = threadIdx.x; q < hx; q += blockDim.x) rbs[q] = rb[q];
+    __syncthreads();
+    const double* W0 = w0s + pb * hx;
+    const double* W1v = w1s + pb * hx;
+    const int* J0 = i0s + pb * hx;
+    const int* J1 = i1s + pb * hx;
+    double* out = t1 + row * ncx;
+    for (int I = threadIdx.x; I < ncx; I += blockDim.x) {
+      const int mlo = max(0, (s * (I - 1)) >> 1), mhi = min(hx, (s * (I + 2) + 1) >> 1);
+      double acc = 0.0;
+      for (int q = mlo; q < mhi; ++q) {
+        const double res = rbs[q];
+        if (J0[q] == I) acc += __dmul_rn(W0[q], res);    // the product is rounded first, as when
+        if (J1[q] == I) acc += __dmul_rn(W1v[q], res);   // staged in shared memory (no contraction)
+      }
+      out[I] = acc;
+    }
   }
 }
 
