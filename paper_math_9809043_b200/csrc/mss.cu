@@ -493,8 +493,9 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
   if ((int64_t)nch * bx * by > kMaxPartials) nch = std::max(1, kMaxPartials / (bx * by));
   const int kch = (l.nz + nch - 1) / nch;
   nch = (l.nz + kch - 1) / kch;
-  // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero)
-  ProfScope ps(ctx, KC_PAIR, k, 8.0 * (ctx->ndim + (first ? 2 : 3)) * l.N);
+  // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero);
+  // the fused closing sweep + black residual is booked as the residual class (+ 4 B/cell)
+  ProfScope ps(ctx, res ? KC_RESID : KC_PAIR, k, (8.0 * (ctx->ndim + (first ? 2 : 3)) + (res ? 4.0 : 0.0)) * l.N);
   if (l.txp && pair_tma_on()) {
     // tile rows: 16 (one 190 KB CTA per SM) on big levels, 8 (two 80 KB CTAs per SM) below
     const char* tye = getenv("MSS_PAIR_TY");
@@ -790,10 +791,7 @@ static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
     return op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs);
   }
   TRY(op_smooth(ctx, k, l.r, l.z, nh - 1, 0, true));            // (nh-1)/2 pairs, z in l.z
-  {
-    ProfScope ps(ctx, KC_RESID, k, (8.0 * (ctx->ndim + 3) + 4.0) * l.N);
-    TRY(op_pair(ctx, k, l.r, l.z, l.s, 0, false, true));        // closing red sweep + black residual
-  }
+  TRY(op_pair(ctx, k, l.r, l.z, l.s, 0, false, true));          // closing red sweep + black residual
   std::swap(l.z, l.s);
   tail_mark_dirty(ctx);
   {
