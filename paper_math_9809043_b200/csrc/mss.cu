@@ -1622,6 +1622,7 @@ int mss_profile(mss_ctx* ctx, int enable, int max_level) {
 
 int mss_profile_read(const mss_ctx* ctx, int kclass, int level, int64_t* count, double* ms, double* bytes) {
   if (!ctx || kclass < 0 || kclass >= MSS_NUM_KCLASS || level < 0 || level >= MSS_MAX_LEVELS) return MSS_EINVAL;
+  prof_flush(const_cast<mss_ctx*>(ctx));   // records of launches made outside a solve (hooks)
   if (count) *count = ctx->prof_cnt[kclass][level];
   if (ms) *ms = ctx->prof_ms[kclass][level];
   if (bytes) *bytes = ctx->prof_bytes[kclass][level];

@@ -535,3 +535,37 @@ def test_spmv_tma_solves(torch_mod, name, n, bc, monkeypatch):
     o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=1)
     xo, _ = o.solve(w.f, rel_tol=1e-10)
     assert rel(xb.cpu().numpy(), xo.ravel()) <= 1e-8
+
+
+@pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
+                                     ("3d_ragged", CASES[1][1])], ids=["C2", "C5_128", "3d_ragged"])
+def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
+    """The pre-smoothing's closing red sweep fused with the black residual (TMA pair kernel,
+    RES mode) + the x-restriction of the stored residual, forced onto these levels, against
+    the unfused half-sweep + residual/restriction path: one preconditioner application and
+    full solves agree to 1e-12 with identical counts (Eq. 2.10)."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = mk()
+    K = torch.from_numpy(w.K).cuda()
+    monkeypatch.setenv("MSS_PAIR", "1")
+    rng = np.random.default_rng(9)
+    out = {}
+    for fused in ("0", "1"):
+        monkeypatch.setenv("MSS_FUSED_RESID", fused)
+        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+        r = cu(torch, rng.standard_normal(s.level_N(0)) if fused == "0" else out["r"])
+        s.profile(True, 0)
+        z, its = s.precond(0, r, rel_tol=w.rel_tol)
+        prof = s.profile_read()
+        s.profile(False, 0)
+        # the fused path books its x-restriction as a second restrict-class launch
+        assert prof[("restrict", 0)][0] == (2 if fused == "1" else 1), prof
+        x, rep = s.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+        out[fused] = (z.cpu().numpy(), list(its), x.cpu().numpy(), list(rep.iters))
+        out["r"] = r.cpu().numpy()
+    za, ia, xa, ra = out["0"]
+    zb, ib, xb, rb = out["1"]
+    assert ia == ib and ra == rb
+    assert rel(zb, za) <= 1e-12
+    assert rel(xb, xa) <= 1e-12
