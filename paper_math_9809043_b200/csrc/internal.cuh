@@ -137,6 +137,17 @@ struct mss_ctx {
   std::vector<char> tsm_h;
   bool tsm_dirty = true;
   long long* tsm_phase = nullptr;
+  // kernel-selection knobs (environment, read once at setup; DESIGN.md §9 "Runtime knobs")
+  struct Knobs {
+    int pair = -1;            // MSS_PAIR: -1 pairs on levels >= 2^24 cells, 0 off, 1 every eligible level
+    bool pair_tma = true;     // MSS_PAIR_TMA
+    int pair_ty = 0;          // MSS_PAIR_TY: 0 auto (16 on big levels, 8 below)
+    int pair_nch = 0;         // MSS_PAIR_NCH: 0 cost model
+    bool spmv_tma = true;     // MSS_SPMV_TMA
+    int spmv_nch = 0;         // MSS_SPMV_NCH: 0 cost model
+    bool fused_resid = true;  // MSS_FUSED_RESID
+    bool prolong_pairs = true;// MSS_PROLONG_PAIRS
+  } kn;
   // TMA tensor maps (pairtma.cuh), cached by base pointer and kind (opaque 128-byte images)
   struct TmapEnt {
     const void* ptr;

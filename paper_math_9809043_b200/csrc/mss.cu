@@ -301,7 +301,7 @@ static int op_dot(mss_ctx* ctx, int level, int64_t n, const double* a, const dou
 
 static int spmv_tma_launch(mss_ctx* ctx, int k, bool residual, bool first, const double* zx, const double* pb,
                            double* pout, double* qr, RedOut ro);
-static bool spmv_tma_ok(const Level& l);
+static bool spmv_tma_ok(const mss_ctx* ctx, const Level& l);
 
 static int op_residual(mss_ctx* ctx, int k, const double* b, const double* x, double* r, double* rr_out) {
   Level& l = ctx->lv[k];
@@ -309,7 +309,7 @@ static int op_residual(mss_ctx* ctx, int k, const double* b, const double* x, do
   {
     ProfScope ps(ctx, KC_RESID, k, cell_bytes(ctx, KC_RESID) * l.N);
     // the SpMV's TMA kernel in residual mode where it runs (x's ghost planes are current)
-    if (b && l.txp && spmv_tma_ok(l)) {
+    if (b && l.txp && spmv_tma_ok(ctx, l)) {
       TRY(spmv_tma_launch(ctx, k, true, true, x, b, nullptr, r, ro));
     } else {
       DISPATCH(ctx->ndim, k_residual, grid_for(l.N), l.dev(), b, x, r, ro);
@@ -367,9 +367,22 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
 }
 
 // ---- TMA tensor maps (driver entry point fetched through the runtime: no -lcuda)
-static bool pair_tma_on() {
-  const char* e = getenv("MSS_PAIR_TMA");   // read per call so tests can toggle it
-  return !e || atoi(e) != 0;
+static bool pair_tma_on(const mss_ctx* ctx) { return ctx->kn.pair_tma; }
+
+// the kernel-selection knobs, read from the environment once per context (setup)
+static void read_knobs(mss_ctx* ctx) {
+  auto geti = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+  };
+  ctx->kn.pair = geti("MSS_PAIR", -1);
+  ctx->kn.pair_tma = geti("MSS_PAIR_TMA", 1) != 0;
+  ctx->kn.pair_ty = geti("MSS_PAIR_TY", 0);
+  ctx->kn.pair_nch = geti("MSS_PAIR_NCH", 0);
+  ctx->kn.spmv_tma = geti("MSS_SPMV_TMA", 1) != 0;
+  ctx->kn.spmv_nch = geti("MSS_SPMV_NCH", 0);
+  ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
+  ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
@@ -414,11 +427,9 @@ static bool tmap_get(mss_ctx* ctx, CUtensorMap* out, const void* base, int kind,
 
 // TMA SpMV on every padded level (measured: 1.09 vs 1.37 ms at 512^3, 25 vs 31 us at
 // 128^3); MSS_SPMV_TMA=0 disables (tests compare against the column-walk SpMV).
-static bool spmv_tma_ok(const Level& l) {
+static bool spmv_tma_ok(const mss_ctx* ctx, const Level& l) {
   (void)l;
-  const char* e = getenv("MSS_SPMV_TMA");
-  if (e) return atoi(e) != 0;
-  return pair_tma_on();
+  return ctx->kn.spmv_tma && pair_tma_on(ctx);
 }
 
 // TMA direction + SpMV + p.q (pairtma.cuh), or in residual mode r = b - A x (+ ||r||^2):
@@ -438,10 +449,9 @@ static int spmv_tma_launch(mss_ctx* ctx, int k, bool residual, bool first, const
       !tmap_get(ctx, &M.tz, l.Tz - g * l.plane, 19, l.nx, l.ny, l.nz + 1 + 2 * g, SpmvGeo::W, SpmvGeo::TY))
     return set_err(MSS_ECUDA, "cuTensorMapEncodeTiled failed");
   const int sbx = (l.nx / 2 + kPX - 1) / kPX, sby = (l.ny + SpmvGeo::TY - 1) / SpmvGeo::TY;
-  const char* nce = getenv("MSS_SPMV_NCH");
   int snch = 1;
-  if (nce) {
-    snch = std::max(1, atoi(nce));
+  if (ctx->kn.spmv_nch > 0) {
+    snch = ctx->kn.spmv_nch;
   } else {
     const int64_t tiles = (int64_t)sbx * sby;
     int64_t best = -1;
@@ -474,12 +484,11 @@ static bool pair_ok(const mss_ctx* ctx, int k) {
   // Fused pairs beat two single sweeps on large levels only (512^3: 1.43 ms per pair vs
   // 1.96 ms; 128^3: slower, the per-plane block barrier dominates): default for levels of
   // at least 2^24 cells; MSS_PAIR=0 disables, MSS_PAIR=1 forces every eligible level.
-  const char* env = getenv("MSS_PAIR");   // read per call so tests can toggle it
-  const int mode = env ? atoi(env) : -1;
+  const int mode = ctx->kn.pair;
   const Level& l = ctx->lv[k];
   if (mode == 0 || !col_ok(ctx, l)) return false;
   // z-slab levels: only the TMA kernel computes the ghost planes' first colour
-  if (dist_level(ctx, k) && !(l.txp && pair_tma_on())) return false;
+  if (dist_level(ctx, k) && !(l.txp && pair_tma_on(ctx))) return false;
   // per-rank slab size decides (a z-slab of 512^2 x 64 is 2^24 cells)
   return mode == 1 || l.N >= ((int64_t)1 << 24);
 }
@@ -496,10 +505,9 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
   // algorithmic bytes of one pass (two half-sweeps): T + r + zout (+ zin when not from zero);
   // the fused closing sweep + black residual is booked as the residual class (+ 4 B/cell)
   ProfScope ps(ctx, res ? KC_RESID : KC_PAIR, k, (8.0 * (ctx->ndim + (first ? 2 : 3)) + (res ? 4.0 : 0.0)) * l.N);
-  if (l.txp && pair_tma_on()) {
+  if (l.txp && pair_tma_on(ctx)) {
     // tile rows: 16 (one 190 KB CTA per SM) on big levels, 8 (two 80 KB CTAs per SM) below
-    const char* tye = getenv("MSS_PAIR_TY");
-    const bool big = tye ? atoi(tye) >= 16 : l.N >= ((int64_t)1 << 24);
+    const bool big = ctx->kn.pair_ty ? ctx->kn.pair_ty >= 16 : l.N >= ((int64_t)1 << 24);
     const int TY = big ? PairBig::TY : PairSmall::TY;
     const int occ = big ? PairBig::MINB : PairSmall::MINB;
     // z-slab levels: the z map starts 2 ghost planes below the slab, the face / r maps 1
@@ -516,10 +524,9 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     const int tby = (l.ny + TY - 3) / (TY - 2);
     // z chunks per tile column: minimise waves x (planes + 2 halo planes + ~4 planes of
     // pipeline fill); 512^3 -> 4 chunks of 128 planes, 1332 CTAs = 9 waves of 148
-    const char* nce = getenv("MSS_PAIR_NCH");
     int tnch = 1;
-    if (nce) {
-      tnch = std::max(1, atoi(nce));
+    if (ctx->kn.pair_nch > 0) {
+      tnch = ctx->kn.pair_nch;
     } else {
       const int64_t tiles = (int64_t)bx * tby, slots = (int64_t)kSMs * occ;
       int64_t best = -1;
@@ -734,9 +741,8 @@ static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int c
     ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
     dim3 cgrid;
     int kch = 0;
-    const char* pve = getenv("MSS_PROLONG_PAIRS");
     if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && !dist_level(ctx, k) && f.w[0] && f.w[1] && f.w[2] &&
-        (pve ? atoi(pve) != 0 : true) && (int64_t)(f.nx / 2) * f.ny * f.nz < ((int64_t)1 << 32)) {
+        ctx->kn.prolong_pairs && (int64_t)(f.nx / 2) * f.ny * f.nz < ((int64_t)1 << 32)) {
       const int64_t np = (int64_t)(f.nx / 2) * f.ny * f.nz;
       LAUNCH(k_prolong_pairs, grid_for(np), f.dev(), c.nx, c.ny, y, z, reinterpret_cast<const W1*>(f.w[0]),
              reinterpret_cast<const W1*>(f.w[1]), reinterpret_cast<const W1*>(f.w[2]));
@@ -782,10 +788,9 @@ static int pcg_level(mss_ctx* ctx, int k);
 static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
   Level& l = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
-  const char* fe = getenv("MSS_FUSED_RESID");
   const bool fused = sgs && nh >= 3 && (nh & 1) && l.resb && l.w[0] && l.uniform && !dist_level(ctx, k) &&
                      (size_t)(l.nx / 2) * (5 * sizeof(double) + 4 * sizeof(int)) <= 48 * 1024 && pair_ok(ctx, k) &&
-                     l.txp && pair_tma_on() && (fe ? atoi(fe) != 0 : true);
+                     l.txp && pair_tma_on(ctx) && ctx->kn.fused_resid;
   if (!fused) {
     TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));
     return op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs);
@@ -887,7 +892,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
                                                                        it == 0 ? 1 : 0, kch,
                                                                        red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
       ctx->launches++;
-    } else if (l.txp && spmv_tma_ok(l)) {
+    } else if (l.txp && spmv_tma_ok(ctx, l)) {
       TRY(spmv_tma_launch(ctx, k, false, it == 0, l.z, pin, pout, l.q, red_to(ctx, &ds->pq, k, 0)));
     } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
       k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
@@ -1418,7 +1423,7 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   cudaFree(X);
   compute_lift(ctx);
   // padded Tx copies for the TMA pair kernel on every single-GPU column-walk level
-  if (ndim == 3 && pair_tma_on() && tma_encoder()) {
+  if (ndim == 3 && pair_tma_on(ctx) && tma_encoder()) {
     bool any = false;
     for (int k = 0; k <= ctx->L; ++k) {
       Level& l = ctx->lv[k];
@@ -1520,6 +1525,7 @@ static int setup_common(mss_ctx** out, mss::Comm* comm, int ndim, const int64_t 
   }
   if (!any_dir) return set_err(MSS_ESINGULAR, "all-Neumann operator is singular");
   mss_ctx* ctx = new mss_ctx();
+  read_knobs(ctx);
   ctx->ndim = ndim;
   ctx->prm = prm;
   ctx->comm = comm;
