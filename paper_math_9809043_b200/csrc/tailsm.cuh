@@ -18,6 +18,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -601,6 +604,20 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
 }  // namespace mss
 
 // ============================================================================ host side
+// The dynamic shared-memory limit is a per-kernel, process-wide attribute: contexts of
+// different sizes in one process (or concurrent loopback ranks) must only ever raise it,
+// else a smaller context's setup breaks a larger one's launches.
+static bool tailsm_raise_smem(const void* kern, size_t shm) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[kern];
+  if (shm <= c) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess) return false;
+  c = shm;
+  return true;
+}
+
 // the k_tailsm instantiation for a tail of depth D = L - L0 (1 .. kTsMaxLv - 1)
 static const void* tailsm_kernel(int ndim, int D) {
 #define TSK(N)                                                                           \
@@ -697,7 +714,7 @@ static void tailsm_setup(mss_ctx* ctx) {
   }
   auto kern = tailsm_kernel(ctx->ndim, ctx->L - L0);
   const size_t shm = (size_t)a.smem_doubles * sizeof(double);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess ||
+  if (!tailsm_raise_smem(kern, shm) ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     if (dbg) fprintf(stderr, "[mss] tailsm: attribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
     cudaGetLastError();
@@ -782,5 +799,6 @@ static int tailsm_launch(mss_ctx* ctx, int k) {
   void* args[] = {(void*)&dp};
   cudaError_t e = cudaLaunchKernelExC(&cfg, tailsm_kernel(ctx->ndim, a.L - a.L0), args);
   ctx->launches++;
-  return e == cudaSuccess ? MSS_OK : MSS_ECUDA;
+  if (e != cudaSuccess) return set_err(MSS_ECUDA, std::string("cluster tail launch: ") + cudaGetErrorString(e));
+  return MSS_OK;
 }

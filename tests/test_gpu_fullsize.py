@@ -190,3 +190,16 @@ def test_big_ragged_pair_tiles():
     assert np.linalg.norm(zb - za) <= 1e-12 * np.linalg.norm(za)
     assert ia == ib and rb <= 1e-10
     assert np.linalg.norm(xb - xa) <= 1e-12 * np.linalg.norm(xa)
+
+
+def test_fullsize_solves_bitwise_repeatable(c5):
+    """At the bench's size and launch configuration (TMA pairs 32 x 16, fused closing sweep +
+    residual, TMA SpMV, cluster tail) two solves give identical bits: no race in the staged
+    rings, barriers or reductions."""
+    torch, w, s = c5
+    f = torch.from_numpy(w.f.ravel()).cuda()
+    x1, r1 = s.solve(f, rel_tol=w.rel_tol)
+    a = x1.cpu().numpy()
+    x2, r2 = s.solve(f, rel_tol=w.rel_tol)
+    assert list(r1.iters) == list(r2.iters) and r1.true_rel_res == r2.true_rel_res
+    assert np.array_equal(a, x2.cpu().numpy())

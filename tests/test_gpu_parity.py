@@ -569,3 +569,48 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
     assert ia == ib and ra == rb
     assert rel(zb, za) <= 1e-12
     assert rel(xb, xa) <= 1e-12
+
+
+@pytest.mark.parametrize("ty", ["16", "8"])
+def test_hot_paths_are_bitwise_deterministic(torch_mod, ty, monkeypatch):
+    """Race check (compute-sanitizer is closed on this pool): the TMA pair sweeps (both tile
+    geometries, fused closing sweep + residual), the TMA SpMV, the deterministic grid
+    reductions and the cluster tail give identical bits on 5 repetitions of the same inputs —
+    a shared-memory ring, mbarrier or DSMEM race would show up as run-to-run differences."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    monkeypatch.setenv("MSS_PAIR", "1")
+    monkeypatch.setenv("MSS_PAIR_TY", ty)
+    w = make_workload("C5", n=128)
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth)
+    rng = np.random.default_rng(12)
+    r = cu(torch, rng.standard_normal(s.level_N(0)))
+    f = cu(torch, w.f)
+    ref = None
+    for _ in range(5):
+        zs = s.smooth(0, r, None, 9, 0).cpu().numpy()
+        zp, its = s.precond(0, r, rel_tol=w.rel_tol)
+        x, rep = s.solve(f, rel_tol=w.rel_tol)
+        cur = (zs, zp.cpu().numpy(), list(its), x.cpu().numpy(), list(rep.iters), rep.true_rel_res)
+        if ref is None:
+            ref = cur
+            continue
+        assert np.array_equal(cur[0], ref[0]) and np.array_equal(cur[1], ref[1]) and np.array_equal(cur[3], ref[3])
+        assert cur[2] == ref[2] and cur[4] == ref[4] and cur[5] == ref[5]
+
+
+def test_contexts_of_different_tail_sizes_coexist(torch_mod):
+    """Regression: the cluster tail's dynamic shared-memory limit is a process-wide kernel
+    attribute; setting up a context with a smaller tail after one with a larger tail must not
+    break the larger one's launches (found by the full-size repeatability test)."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    wa, wb = make_workload("C5", n=128), make_workload("C2", n=32)
+    a = Solver(wa.ndim, wa.n, torch.from_numpy(wa.K).cuda(), wa.bc, depth=wa.depth)
+    xa1, ra1 = a.solve(cu(torch, wa.f), rel_tol=wa.rel_tol)
+    b = Solver(wb.ndim, wb.n, torch.from_numpy(wb.K).cuda(), wb.bc, depth=wb.depth)
+    xb, rb = b.solve(cu(torch, wb.f), rel_tol=wb.rel_tol)
+    xa2, ra2 = a.solve(cu(torch, wa.f), rel_tol=wa.rel_tol)
+    assert ra1.tail_kind == 2 and rb.tail_kind == 2
+    assert list(ra1.iters) == list(ra2.iters)
+    assert np.array_equal(xa1.cpu().numpy(), xa2.cpu().numpy())
