@@ -605,7 +605,7 @@ def test_contexts_of_different_tail_sizes_coexist(torch_mod):
     break the larger one's launches (found by the full-size repeatability test)."""
     torch = torch_mod
     from paper_math_9809043_b200.mss import Solver
-    wa, wb = make_workload("C5", n=128), make_workload("C2", n=32)
+    wa, wb = make_workload("C5", n=128), make_workload("C2")   # tails on 32^3 and on 16^3
     a = Solver(wa.ndim, wa.n, torch.from_numpy(wa.K).cuda(), wa.bc, depth=wa.depth)
     xa1, ra1 = a.solve(cu(torch, wa.f), rel_tol=wa.rel_tol)
     b = Solver(wb.ndim, wb.n, torch.from_numpy(wb.K).cuda(), wb.bc, depth=wb.depth)
