@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -106,52 +108,45 @@ static RedOut red_to(mss_ctx* ctx, double* out, int level, int mode) {
 // z-neighbour planes are still in L2 when reused.  A two-wave grid-stride launch let
 // each wave sweep the whole 512^3 domain and moved 1.5x the algorithmic bytes (ncu,
 // profiles/r01).
-static int wave_clamp(const void* kern, int grid) {
-  static std::vector<std::pair<const void*, int>> cache;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
+// Process-wide host caches are shared by every context, and loopback ranks drive their
+// contexts from parallel host threads: the SM count is a magic static, the occupancy cache
+// is guarded by a mutex.
+static int sm_count() {
+  static const int nsm = [] {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = kSMs;
-  }
-  int occ = 0;
-  for (auto& e : cache)
-    if (e.first == kern) occ = e.second;
-  if (!occ) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
-    cache.push_back({kern, occ});
-  }
-  const int w = occ * nsm;
-  return grid < w ? grid : (w < kMaxGrid ? w : kMaxGrid);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : kSMs;
+  }();
+  return nsm;
 }
 
 static int occupancy_of(const void* kern, int threads) {
-  static std::vector<std::pair<const void*, int>> cache;
-  for (auto& e : cache)
-    if (e.first == kern) return e.second;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({kern, threads});
+  if (it != cache.end()) return it->second;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0) != cudaSuccess || occ < 1) occ = 1;
-  cache.push_back({kern, occ});
+  cache[{kern, threads}] = occ;
   return occ;
+}
+
+static int wave_clamp(const void* kern, int grid) {
+  const int w = occupancy_of(kern, kBlock) * sm_count();
+  return grid < w ? grid : (w < kMaxGrid ? w : kMaxGrid);
 }
 
 // Column-walk kernels (colwalk.cuh) for 3-D levels with even n_x: grid = (pairs/32,
 // rows/8, z-chunks) with the chunk count chosen so the grid is one resident wave.
 static bool col_ok(const mss_ctx* ctx, const Level& l) {
-  static int disabled = -1;
-  if (disabled < 0) disabled = getenv("MSS_NO_COLWALK") ? 1 : 0;
+  static const bool disabled = getenv("MSS_NO_COLWALK") != nullptr;
   return !disabled && ctx->ndim == 3 && (l.nx % 2) == 0 && l.N >= 32768;
 }
 
 static bool col_grid(const void* kern, const Level& l, dim3* grid, int* kchunk) {
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = kSMs;
-  }
+  const int nsm = sm_count();
   const int bx = (l.nx / 2 + kColX - 1) / kColX, by = (l.ny + kColY - 1) / kColY;
   const int layer = bx * by;
   if (layer > kMaxPartials) return false;
@@ -161,8 +156,7 @@ static bool col_grid(const void* kern, const Level& l, dim3* grid, int* kchunk) 
   // at least one full wave either way.
   int nch = (l.nz + kColChunk - 1) / kColChunk;
   if (nch * layer < resident) nch = (resident + layer - 1) / layer;
-  static int force = -1;
-  if (force < 0) force = getenv("MSS_COL_NCH") ? atoi(getenv("MSS_COL_NCH")) : 0;
+  static const int force = getenv("MSS_COL_NCH") ? atoi(getenv("MSS_COL_NCH")) : 0;
   if (force > 0) nch = force;
   if (nch < 1) nch = 1;
   if (nch > l.nz) nch = l.nz;
@@ -328,8 +322,7 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   RedOut ro = red_to(ctx, dot_out, k, 0);
   const LevelDev d = l.dev();
   if (col_ok(ctx, l)) {
-    static int minb = -1;
-    if (minb < 0) minb = getenv("MSS_COL_MINB") ? atoi(getenv("MSS_COL_MINB")) : 4;  // 64 regs: measured best
+    static const int minb = getenv("MSS_COL_MINB") ? atoi(getenv("MSS_COL_MINB")) : 4;  // 64 regs: measured best
 #define SWEEPCOL(MB, KFB)                                                                                   \
     {                                                                                                       \
       const void* kern = first ? (const void*)k_sweep_col<true, false, MB, KFB>                            \
@@ -385,17 +378,16 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
 }
 
+// looked up once, thread-safely (loopback ranks set up their contexts on parallel threads)
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 

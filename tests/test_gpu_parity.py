@@ -7,6 +7,8 @@ Gates (BASELINE.json north_star):
   * the coarsest dense solve: <= max(1e-12, 50 kappa eps) (two backward-stable exact
     solvers differ by O(kappa eps); DESIGN.md §5 derives the bound).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -614,3 +616,16 @@ def test_contexts_of_different_tail_sizes_coexist(torch_mod):
     assert ra1.tail_kind == 2 and rb.tail_kind == 2
     assert list(ra1.iters) == list(ra2.iters)
     assert np.array_equal(xa1.cpu().numpy(), xa2.cpu().numpy())
+
+
+def test_contexts_on_parallel_host_threads(torch_mod):
+    """Process-wide host state (occupancy cache, SM count, the TMA encoder lookup, the tail's
+    shared-memory attribute) is shared by every context; four contexts set up and solved
+    concurrently from host threads in a fresh process must give the same bits as the same
+    solves run one after another."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "_threaded_contexts.py")], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
