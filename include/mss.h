@@ -141,6 +141,21 @@ int mss_solve(mss_ctx* ctx, const double* f, double* x, double rel_tol,
 int mss_solve_host(mss_ctx* ctx, const double* f_host, double* x_host, double rel_tol,
                    int64_t* iters_per_level, double* true_rel_res);
 
+/* Solves nrhs problems with this context's operator, end to end from host memory:
+ * f_host[i] (N_local doubles, source density as in mss_solve) -> x_host[i] (N_local
+ * doubles; also the initial guess when use_lift == 0).  The copies are pipelined against
+ * the solves on a copy stream the context owns: f_{i+1} is uploaded and x_{i-1} read back
+ * while solve i runs (two device f / x buffers, 4 N_local doubles allocated on first use,
+ * kept until mss_free).  Host buffers should be pinned (pageable ones are correct but do
+ * not overlap).  Caller-owned: the host arrays, which must not be touched until the call
+ * returns; every x_host[i] holds its result on return.  iters_per_level: host, nrhs * L1
+ * (row i = solve i, nullable); true_rel_res: host, nrhs (nullable).  Returns the largest
+ * status of the solves (0 or MSS_NOT_CONVERGED); the first hard error aborts the batch and
+ * is returned (x_host of later problems is then unspecified).  Same threading rule as
+ * mss_solve.  The method per solve is mss_solve's (Eq. 2.10). */
+int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, double* const* x_host,
+                         double rel_tol, int64_t* iters_per_level, double* true_rel_res);
+
 int mss_get_info(const mss_ctx* ctx, mss_info* info);            /* last solve's report */
 
 /* ---- kernel-level hooks (parity tests; level-local compact device vectors) ---- */

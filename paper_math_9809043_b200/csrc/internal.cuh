@@ -101,6 +101,11 @@ struct mss_ctx {
   size_t stage_bytes = 0;
   double* dev_f = nullptr;                 // device f / x for mss_solve_host
   double* dev_x = nullptr;
+  // mss_solve_host_batch: a second f / x pair, a copy stream and its events (lazy)
+  double* dev_f1 = nullptr;
+  double* dev_x1 = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   // lift
   int lift_mode = 0;                       // 0 zero, 1 constant, 2 ramp in x
   double lift_a = 0, lift_b = 0;

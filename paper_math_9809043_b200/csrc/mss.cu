@@ -1168,6 +1168,14 @@ static int free_ctx(mss_ctx* ctx) {
   prof_flush(ctx);
   tailsm_report(ctx);
   for (cudaEvent_t e : ctx->ev_free) cudaEventDestroy(e);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->ev_in[b]) cudaEventDestroy(ctx->ev_in[b]);
+    if (ctx->ev_done[b]) cudaEventDestroy(ctx->ev_done[b]);
+  }
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->hscal) cudaFreeHost(ctx->hscal);
   if (ctx->comm) {
@@ -1598,6 +1606,68 @@ int mss_solve_host(mss_ctx* ctx, const double* f_host, double* x_host, double re
   CK(cudaMemcpyAsync(x_host, ctx->dev_x, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return rc;
+}
+
+// Pipelined host solves: f_{i+1} is uploaded and x_{i-1} read back on the context's copy
+// stream while solve i runs on the compute stream (double-buffered device f / x).  Solve i
+// waits for its upload (ev_in); the read-back of x_i and the upload of f_{i+2} into the same
+// buffer wait for solve i (ev_done), in copy-stream order.
+int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, double* const* x_host, double rel_tol,
+                         int64_t* iters, double* true_rel_res) {
+  if (!ctx || nrhs < 0 || (nrhs > 0 && (!f_host || !x_host))) return set_err(MSS_EINVAL, "bad batch arguments");
+  for (int i = 0; i < nrhs; ++i)
+    if (!f_host[i] || !x_host[i]) return set_err(MSS_EINVAL, "null host buffer in batch");
+  if (nrhs == 0) return MSS_OK;
+  const int64_t N = ctx->lv[0].N;
+  const size_t bytes = sizeof(double) * N;
+  if (!ctx->dev_f) {
+    TRY(dalloc(ctx, (void**)&ctx->dev_f, bytes));
+    TRY(dalloc(ctx, (void**)&ctx->dev_x, bytes));
+  }
+  if (!ctx->dev_f1) {
+    TRY(dalloc(ctx, (void**)&ctx->dev_f1, bytes));
+    TRY(dalloc(ctx, (void**)&ctx->dev_x1, bytes));
+  }
+  if (!ctx->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_done[b], cudaEventDisableTiming));
+    }
+  }
+  double* df[2] = {ctx->dev_f, ctx->dev_f1};
+  double* dx[2] = {ctx->dev_x, ctx->dev_x1};
+  cudaStream_t cs = ctx->copy_stream;
+  const int L1 = ctx->L + 1;
+  auto upload = [&](int i) -> int {
+    const int b = i & 1;
+    CK(cudaMemcpyAsync(df[b], f_host[i], bytes, cudaMemcpyHostToDevice, cs));
+    if (!ctx->prm.use_lift) CK(cudaMemcpyAsync(dx[b], x_host[i], bytes, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->ev_in[b], cs));
+    return MSS_OK;
+  };
+  // the compute stream may still be reading buffers from an earlier call
+  CK(cudaStreamSynchronize(ctx->stream));
+  TRY(upload(0));
+  if (nrhs > 1) TRY(upload(1));
+  int worst = MSS_OK;
+  for (int i = 0; i < nrhs; ++i) {
+    const int b = i & 1;
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[b], 0));
+    const int rc = mss_solve(ctx, df[b], dx[b], rel_tol, iters ? iters + (int64_t)i * L1 : nullptr,
+                             true_rel_res ? true_rel_res + i : nullptr);
+    if (rc < 0) {
+      cudaStreamSynchronize(cs);
+      return rc;
+    }
+    if (rc > worst) worst = rc;
+    CK(cudaEventRecord(ctx->ev_done[b], ctx->stream));
+    CK(cudaStreamWaitEvent(cs, ctx->ev_done[b], 0));
+    CK(cudaMemcpyAsync(x_host[i], dx[b], bytes, cudaMemcpyDeviceToHost, cs));
+    if (i + 2 < nrhs) TRY(upload(i + 2));
+  }
+  CK(cudaStreamSynchronize(cs));
+  return worst;
 }
 
 int mss_get_info(const mss_ctx* ctx, mss_info* info) {

@@ -95,6 +95,7 @@ SIGNATURES = [
     ("mss_level_dims", ctypes.c_int, [P, ctypes.c_int, I64P]),
     ("mss_solve", ctypes.c_int, [P, P, P, ctypes.c_double, I64P, DP]),
     ("mss_solve_host", ctypes.c_int, [P, P, P, ctypes.c_double, I64P, DP]),
+    ("mss_solve_host_batch", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_double, I64P, DP]),
     ("mss_get_info", ctypes.c_int, [P, ctypes.POINTER(Info)]),
     ("mss_get_faces", ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P]),
     ("mss_apply_A", ctypes.c_int, [P, ctypes.c_int, P, P]),
@@ -388,6 +389,25 @@ class Solver:
         rep = self.info()
         rep.rc = rc
         return x_host, rep
+
+    def solve_host_batch(self, f_hosts, x_hosts, rel_tol: float = 1e-10):
+        """mss_solve_host_batch: host f_hosts[i] -> x_hosts[i] with the copies pipelined
+        against the solves (pinned buffers overlap).  Returns (iters [nrhs][L1],
+        true_rel_res [nrhs], status)."""
+        n = len(f_hosts)
+        if len(x_hosts) != n:
+            raise ValueError("f_hosts and x_hosts differ in length")
+        for t in list(f_hosts) + list(x_hosts):
+            if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != self.N:
+                raise ValueError("expected contiguous float64 host tensors of N elements")
+        fp = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in f_hosts])
+        xp = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in x_hosts])
+        its = (ctypes.c_int64 * max(n * self.levels, 1))()
+        tr = (ctypes.c_double * max(n, 1))()
+        rc = self.lib.mss_solve_host_batch(self.ctx, n, fp, xp, float(rel_tol), its, tr)
+        _check(rc, "mss_solve_host_batch")
+        iters = [[its[i * self.levels + k] for k in range(self.levels)] for i in range(n)]
+        return iters, [tr[i] for i in range(n)], rc
 
     # ---------------------------------------------------------------- hooks
     def faces(self, level: int, d: int) -> torch.Tensor:

@@ -26,7 +26,7 @@ def lib_path():
 
 def test_header_declares_the_boundary():
     names = declared_functions()
-    for must in ["mss_setup", "mss_solve", "mss_free", "mss_solve_host", "mss_apply_A", "mss_smooth",
+    for must in ["mss_setup", "mss_solve", "mss_free", "mss_solve_host", "mss_solve_host_batch", "mss_apply_A", "mss_smooth",
                  "mss_residual_restrict", "mss_prolong_add", "mss_precond", "mss_coarse_solve",
                  "mss_dot", "mss_get_faces", "mss_setup_dist", "mss_nccl_unique_id"]:
         assert must in names

@@ -629,3 +629,37 @@ def test_contexts_on_parallel_host_threads(torch_mod):
     r = subprocess.run([sys.executable, os.path.join(here, "_threaded_contexts.py")], capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("use_lift,pinned", [(1, True), (0, True), (1, False)])
+def test_solve_host_batch_matches_device_solves(torch_mod, use_lift, pinned):
+    """mss_solve_host_batch (copies pipelined against the solves on the context's copy stream)
+    gives, per right-hand side, the same bits, counts and residual as mss_solve on device
+    copies of the same inputs; with use_lift = 0 the host x is the initial guess.  Pageable
+    buffers are correct too (they only lose the overlap).  nrhs = 0 and 1 are valid."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = make_workload("C2", n=32)
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth, params={"use_lift": use_lift})
+    rng = np.random.default_rng(31)
+    base = np.ascontiguousarray(w.f, dtype=np.float64).ravel()
+    fs = [base, -0.5 * base + rng.standard_normal(base.size), 2.0 * base, rng.uniform(0.0, 1.0, base.size)]
+    x0s = [rng.standard_normal(base.size) if not use_lift else np.zeros(base.size) for _ in fs]
+
+    def host(a):
+        t = torch.from_numpy(np.array(a, dtype=np.float64))
+        return t.pin_memory() if pinned else t
+
+    fh = [host(a) for a in fs]
+    xh = [host(a) for a in x0s]
+    iters, trr, rc = s.solve_host_batch(fh, xh, rel_tol=w.rel_tol)
+    assert rc == 0 and len(iters) == len(fs)
+    for i, a in enumerate(fs):
+        xd, rep = s.solve(cu(torch, a), cu(torch, x0s[i]), rel_tol=w.rel_tol)
+        assert list(iters[i]) == list(rep.iters), i
+        assert trr[i] == rep.true_rel_res, i
+        assert np.array_equal(xh[i].numpy(), xd.cpu().numpy()), i
+    assert s.solve_host_batch([], [], rel_tol=w.rel_tol)[2] == 0
+    one = [host(x0s[0])]
+    it1, _, _ = s.solve_host_batch([fh[0]], one, rel_tol=w.rel_tol)
+    assert list(it1[0]) == list(iters[0]) and np.array_equal(one[0].numpy(), xh[0].numpy())
