@@ -122,3 +122,31 @@ def test_loopback_fused_pairs_on_slabs(name, cfg, n, P, params, ty, monkeypatch)
     monkeypatch.setenv("MSS_PAIR", "0")
     _, reps0 = run_loopback(torch, w, P, params)
     assert reps[0].kernel_launches < reps0[0].kernel_launches, (reps[0].kernel_launches, reps0[0].kernel_launches)
+
+
+@pytest.mark.parametrize("cfg,n,params", [("C5", 128, {"gather_below": 32768}), ("C2", None, {})],
+                         ids=["C5_128", "C2"])
+def test_nccl_transport_single_rank(cfg, n, params):
+    """The NCCL transport itself (mss_nccl_unique_id, ncclCommInitRank, the CG-scalar
+    allreduces, the gather of the first replicated level, ncclGroupStart/End around the
+    halo send/recv) on a one-rank communicator: the only NCCL configuration one GPU can run
+    without ranks waiting on one another.  Gated like the loopback slabs: the slab layout
+    may pick other grids (another summation order in the dots), so level-0 counts are equal,
+    coarser counts within max(2, 1 %), the solution within 1e-9."""
+    import torch
+    from paper_math_9809043_b200 import build
+    build.build()
+    from paper_math_9809043_b200.mss import Solver, nccl_unique_id
+    w = make_workload(cfg, n=n)
+    K = torch.from_numpy(w.K).cuda()
+    f = torch.from_numpy(w.f.ravel()).cuda()
+    s1 = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=params)
+    x1, r1 = s1.solve(f, rel_tol=w.rel_tol)
+    sn = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=params, comm=("nccl", 0, 1, nccl_unique_id()))
+    xn, rn = sn.solve(f, rel_tol=w.rel_tol)
+    assert rn.true_rel_res <= 1e-10
+    assert rn.iters[0] == r1.iters[0]
+    for a, b in zip(rn.iters[1:], r1.iters[1:]):
+        assert abs(a - b) <= max(2, 0.01 * b)
+    assert rel(xn.cpu().numpy(), x1.cpu().numpy()) <= 1e-9
+    sn.close()
