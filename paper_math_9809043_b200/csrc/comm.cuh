@@ -151,17 +151,19 @@ struct NcclComm : Comm {
   }
   int exch(cudaStream_t st, const double* send_lo, double* recv_lo, const double* send_hi, double* recv_hi,
            size_t n) override {
+    // a failed call inside the group still closes it, so later collectives are not absorbed
     if (ncclGroupStart() != ncclSuccess) return MSS_ENCCL;
+    bool ok = true;
     if (rank > 0) {
-      if (ncclSend(send_lo, n, ncclDouble, rank - 1, c, st) != ncclSuccess) return MSS_ENCCL;
-      if (ncclRecv(recv_lo, n, ncclDouble, rank - 1, c, st) != ncclSuccess) return MSS_ENCCL;
+      ok = ok && ncclSend(send_lo, n, ncclDouble, rank - 1, c, st) == ncclSuccess;
+      ok = ok && ncclRecv(recv_lo, n, ncclDouble, rank - 1, c, st) == ncclSuccess;
     }
     if (rank < size - 1) {
-      if (ncclSend(send_hi, n, ncclDouble, rank + 1, c, st) != ncclSuccess) return MSS_ENCCL;
-      if (ncclRecv(recv_hi, n, ncclDouble, rank + 1, c, st) != ncclSuccess) return MSS_ENCCL;
+      ok = ok && ncclSend(send_hi, n, ncclDouble, rank + 1, c, st) == ncclSuccess;
+      ok = ok && ncclRecv(recv_hi, n, ncclDouble, rank + 1, c, st) == ncclSuccess;
     }
-    if (ncclGroupEnd() != ncclSuccess) return MSS_ENCCL;
-    return MSS_OK;
+    const bool closed = ncclGroupEnd() == ncclSuccess;
+    return (ok && closed) ? MSS_OK : MSS_ENCCL;
   }
   int allreduce_sum(cudaStream_t st, double* dev_val) override {
     if (ncclAllGather(dev_val, gbuf, 1, ncclDouble, c, st) != ncclSuccess) return MSS_ENCCL;
@@ -170,12 +172,13 @@ struct NcclComm : Comm {
   }
   int gather(cudaStream_t st, double* full, const std::vector<int64_t>& off, const std::vector<int64_t>& len) override {
     if (ncclGroupStart() != ncclSuccess) return MSS_ENCCL;
-    for (int q = 0; q < size; ++q) {
+    bool ok = true;
+    for (int q = 0; q < size && ok; ++q) {
       if (len[q] == 0) continue;
-      if (ncclBroadcast(full + off[q], full + off[q], len[q], ncclDouble, q, c, st) != ncclSuccess) return MSS_ENCCL;
+      ok = ncclBroadcast(full + off[q], full + off[q], len[q], ncclDouble, q, c, st) == ncclSuccess;
     }
-    if (ncclGroupEnd() != ncclSuccess) return MSS_ENCCL;
-    return MSS_OK;
+    const bool closed = ncclGroupEnd() == ncclSuccess;
+    return (ok && closed) ? MSS_OK : MSS_ENCCL;
   }
   int barrier(cudaStream_t st) override {
     // an allreduce of one element is the cheapest stream-ordered barrier
