@@ -102,29 +102,30 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------ cpu baseline
 def oracle_sample(cfg, n, repeats=1):
-    """Time the CPU oracle (as it stands) on a bounded sample of the same recipe."""
-    try:
-        from threadpoolctl import threadpool_limits
-        lim = threadpool_limits(1)
-    except Exception:
-        lim = None
+    """Time the CPU oracle (as it stands) on a bounded sample of the same recipe, on one
+    host thread.  numpy's BLAS pool exists only once the oracle (numpy) is imported, so the
+    limit is applied after the import; the CPU-time / wall-time ratio of the solve is
+    measured and reported so the `cores` claim is checked, not assumed."""
     from oracle.mss_oracle import MultiScaleOracle
     from workloads import make_workload
+    from threadpoolctl import threadpool_limits
     w = make_workload(cfg, n=n)
     o = MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth)
-    times = []
+    times, cpus = [], []
     info = None
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        x, info = o.solve(w.f, w.rel_tol)
-        times.append(time.perf_counter() - t0)
-    if lim is not None:
-        lim.unregister() if hasattr(lim, "unregister") else None
+    with threadpool_limits(1):
+        for _ in range(repeats):
+            t0, c0 = time.perf_counter(), time.process_time()
+            x, info = o.solve(w.f, w.rel_tol)
+            times.append(time.perf_counter() - t0)
+            cpus.append(time.process_time() - c0)
     t = statistics.median(times)
-    return {"value": w.N / t, "unit": "unknowns/s", "cores": 1, "kind": "oracle",
+    ratio = sum(cpus) / max(sum(times), 1e-9)
+    return {"value": w.N / t, "unit": "unknowns/s", "cores": max(1, round(ratio)), "kind": "oracle",
             "sample": f"{cfg} recipe at {w.n[0]}^{w.ndim} ({w.N} unknowns), one solve to rel 1e-10, "
-                      f"{t:.2f} s, iters {info.iters}, numpy single-threaded",
-            "seconds": t, "host_cpus": os.cpu_count()}
+                      f"{t:.2f} s, iters {info.iters}, numpy with its BLAS pool limited to 1 thread "
+                      f"(measured CPU/wall {ratio:.2f})",
+            "cpu_per_wall": ratio, "seconds": t, "host_cpus": os.cpu_count()}
 
 
 def run_reference(args, rank, world):
@@ -146,7 +147,8 @@ def run_reference(args, rank, world):
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": f"{cfg}-recipe-{n}^3 (bounded CPU sample)",
                                            "parallelism": "single process"},
-           "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": 1, "kind": "oracle", "sample": r["sample"]},
+           "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": r["cores"], "kind": "oracle",
+                            "sample": r["sample"]},
            "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
