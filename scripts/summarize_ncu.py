@@ -63,9 +63,11 @@ def full(path):
 
 
 if __name__ == "__main__":
+    # usage: summarize_ncu.py TAG LAUNCH_CSV|- REPORT.ncu-rep
     tag, lcsv, rep = sys.argv[1], sys.argv[2], sys.argv[3]
-    open(f"profiles/{tag}_launches.txt", "w").write(launches(lcsv) + "\n")
+    if lcsv != "-":
+        open(f"profiles/{tag}_launches.txt", "w").write(launches(lcsv) + "\n")
+        print(open(f"profiles/{tag}_launches.txt").read()[:3000])
     txt, recs = full(rep)
     open(f"profiles/{tag}_ncu_full.txt", "w").write(txt + "\n")
-    print(open(f"profiles/{tag}_launches.txt").read()[:3000])
     print(txt[:6000])
