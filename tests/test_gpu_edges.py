@@ -1,0 +1,112 @@
+"""GPU: edge cases and degenerate inputs of the C ABI (include/mss.h error contract,
+SURVEY §8(b)), against the oracle where a solution exists.
+
+  * error codes, not just "an error": K <= 0 / NaN / inf and a bad scale -> MSS_EINVAL;
+    an all-Neumann operator (singular, P:366-371 needs a Dirichlet face) -> MSS_ESINGULAR;
+    a depth the grid cannot coarsen to -> MSS_EINVAL; negative rel_tol -> MSS_EINVAL;
+  * a NaN source fails loudly (the divergence guard, DESIGN Q16) instead of looping;
+  * degenerate grids: a single cell, 1-D strips (n_y = 1), a one-plane 3-D slab, depth 0
+    (the fine grid is the coarsest: one exact Cholesky solve), dims that stop the
+    automatic chain early (Q9/Q10) and prime dims that cannot coarsen at all.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import mss_oracle as O
+from workloads import random_problem
+from workloads.configs import DIRICHLET, bc_table
+
+pytestmark = pytest.mark.gpu
+
+MSS_EINVAL, MSS_ESINGULAR, MSS_EBREAKDOWN = -1, -5, -6
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    from paper_math_9809043_b200 import build
+    build.build()
+    return torch
+
+
+def cu(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).ravel()).cuda()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def test_error_codes(torch_mod):
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import MSSError, Solver
+    n = (16, 16, 1)
+    bc = bc_table(2, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})
+    ones = torch.ones(1, 16, 16, dtype=torch.float64, device="cuda")
+
+    def code(fn):
+        with pytest.raises(MSSError) as e:
+            fn()
+        return e.value.code
+
+    for bad in (0.0, -1.0, float("nan"), float("inf")):
+        K = ones.clone()
+        K[0, 3, 5] = bad
+        assert code(lambda: Solver(2, n, K, bc)) == MSS_EINVAL, bad
+    assert code(lambda: Solver(2, n, ones, bc_table(2, {}))) == MSS_ESINGULAR
+    assert code(lambda: Solver(2, n, ones, bc, params={"scale": 1})) == MSS_EINVAL
+    assert code(lambda: Solver(2, n, ones, bc, depth=5)) == MSS_EINVAL   # 16 -> 4 -> 1 -> (none)
+    s = Solver(2, n, ones, bc)
+    f = torch.zeros(256, dtype=torch.float64, device="cuda")
+    assert code(lambda: s.solve(f, rel_tol=-1.0)) == MSS_EINVAL
+    # null pointers through the raw ABI
+    its = (ctypes.c_int64 * s.levels)()
+    assert s.lib.mss_solve(s.ctx, None, None, 1e-10, its, None) == MSS_EINVAL
+    assert s.lib.mss_solve_host_batch(s.ctx, 1, None, None, 1e-10, its, None) == MSS_EINVAL
+    assert s.lib.mss_solve_host_batch(None, 0, None, None, 1e-10, None, None) == MSS_EINVAL
+
+
+@pytest.mark.timeout(300)
+def test_nan_source_fails_loudly(torch_mod):
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import MSSError, Solver
+    w = random_problem(3, (32, 24, 16), seed=5)
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc)
+    f = w.f.copy()
+    f.flat[100] = np.nan
+    with pytest.raises(MSSError) as e:
+        s.solve(cu(torch, f), rel_tol=1e-10)
+    assert e.value.code == MSS_EBREAKDOWN
+    # the context stays usable after the failed solve
+    x, rep = s.solve(cu(torch, w.f), rel_tol=1e-10)
+    assert rep.true_rel_res <= 1e-10
+
+
+DEGENERATE = [
+    ("one_cell_2d", 2, (1, 1, 1), 0, bc_table(2, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})),
+    ("strip_coarsens_2d", 2, (256, 4, 1), None, bc_table(2, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})),
+    ("strip_2d", 2, (64, 1, 1), None, bc_table(2, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})),
+    ("plane_3d", 3, (32, 16, 1), None, bc_table(3, {"x-": (DIRICHLET, 1.0), "y+": (DIRICHLET, 0.0)})),
+    ("depth0_ragged_2d", 2, (12, 10, 1), 0, bc_table(2, {"y-": (DIRICHLET, 2.0)})),
+    ("chain_stops_3d", 3, (36, 20, 12), None, bc_table(3, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})),
+    ("prime_dims_2d", 2, (37, 29, 1), None, bc_table(2, {"x-": (DIRICHLET, 1.0), "y-": (DIRICHLET, 0.0)})),
+]
+
+
+@pytest.mark.parametrize("name,ndim,n,depth,bc", DEGENERATE, ids=[c[0] for c in DEGENERATE])
+def test_degenerate_grids_match_oracle(torch_mod, name, ndim, n, depth, bc):
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = random_problem(ndim, n, seed=11, bc=bc, contrast=1e3, ell=2.0)
+    if w.K.size == 1:   # one cell: the seeded field's contrast rescaling is 0/0
+        w.K = np.full_like(w.K, 2.5)
+    s = Solver(ndim, n, torch.from_numpy(w.K).cuda(), bc, depth=depth)
+    x, rep = s.solve(cu(torch, w.f), rel_tol=1e-10)
+    o = O.MultiScaleOracle(ndim, n, w.K, bc, depth=depth)
+    xo, info = o.solve(w.f, 1e-10)
+    assert rep.true_rel_res <= 1e-10
+    assert len(rep.iters) == len(info.iters), (rep.dims, info.iters)
+    assert rep.iters[0] == info.iters[0]
+    assert rel(x.cpu().numpy(), xo) <= 1e-8
