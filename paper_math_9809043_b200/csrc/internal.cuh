@@ -152,6 +152,7 @@ struct mss_ctx {
     int spmv_nch = 0;         // MSS_SPMV_NCH: 0 cost model
     bool fused_resid = true;  // MSS_FUSED_RESID
     bool prolong_pairs = true;// MSS_PROLONG_PAIRS
+    bool tail_nbsync = false; // MSS_TAIL_NBSYNC: neighbour-only sync after tail half-sweeps
   } kn;
   // TMA tensor maps (pairtma.cuh), cached by base pointer and kind (opaque 128-byte images)
   struct TmapEnt {

@@ -376,6 +376,7 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.spmv_nch = geti("MSS_SPMV_NCH", 0);
   ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
+  ctx->kn.tail_nbsync = geti("MSS_TAIL_NBSYNC", 0) != 0;
 }
 
 // looked up once, thread-safely (loopback ranks set up their contexts on parallel threads)

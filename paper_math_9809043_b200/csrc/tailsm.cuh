@@ -75,6 +75,7 @@ struct TsArgs {
   int o_rfull;          // replicated full r_L (NL doubles)
   int o_red;            // reduction scratch (40 doubles)
   int smem_doubles;
+  int nbsync;           // 1: non-dot half-sweeps end with a neighbour-only sync (MSS_TAIL_NBSYNC)
   TsLevel lv[kTsMaxLv]; // index = level - L0
 };
 
@@ -88,8 +89,11 @@ struct TailSm {
   int rank, cs;
   int phase;
   long long tmark;
+  unsigned* nbf;    // [0]: phase counter written by CTA rank-1, [1]: by CTA rank+1
+  unsigned nbph;    // neighbour-sync phases completed (thread 0)
 
-  __device__ TailSm(const TsArgs* a, double* s) : A(a), cl(cg::this_cluster()), sm(s), phase(0) {
+  __device__ TailSm(const TsArgs* a, double* s, unsigned* nb)
+      : A(a), cl(cg::this_cluster()), sm(s), phase(0), nbf(nb), nbph(0) {
     rank = (int)cl.block_rank();
     cs = (int)cl.num_blocks();
     sm_lo = rank > 0 ? cl.map_shared_rank(sm, rank - 1) : nullptr;
@@ -106,6 +110,33 @@ struct TailSm {
     }
   }
   __device__ __forceinline__ void sync() { cl.sync(); }
+  // A half-sweep reads only the boundary slices of CTAs rank-1 and rank+1, so its end needs
+  // ordering with those two only: after the CTA barrier, thread 0 publishes the phase number
+  // into both neighbours' counters (release, cluster scope) and waits until both neighbours
+  // have published it into its own (acquire).  Counters, not mbarrier parities: a neighbour
+  // may already be one phase ahead (it needs this CTA's store to get further).
+  __device__ __forceinline__ void nb_sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++nbph;
+      if (rank > 0) {
+        unsigned* p = cl.map_shared_rank(nbf + 1, rank - 1);
+        asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(p), "r"(nbph) : "memory");
+      }
+      if (rank < cs - 1) {
+        unsigned* p = cl.map_shared_rank(nbf, rank + 1);
+        asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(p), "r"(nbph) : "memory");
+      }
+      for (int side = 0; side < 2; ++side) {
+        if (side == 0 ? rank == 0 : rank == cs - 1) continue;
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.cluster.u32 %0, [%1];" : "=r"(v) : "l"(nbf + side) : "memory");
+        } while (v < nbph);
+      }
+    }
+    __syncthreads();
+  }
   __device__ __forceinline__ const TsLevel& lvl(int q) const { return A->lv[q - A->L0]; }
   __device__ __forceinline__ int olo(const TsLevel& l) const { return min(l.no, rank * l.ppc); }
   __device__ __forceinline__ int ohi(const TsLevel& l) const { return min(l.no, (rank + 1) * l.ppc); }
@@ -281,7 +312,10 @@ struct TailSm {
       mark(0);
       return d;
     }
-    sync();
+    if (A->nbsync)
+      nb_sync();
+    else
+      sync();
     mark(0);
     return 0.0;
   }
@@ -580,7 +614,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
     __syncthreads();
   }
   const TsArgs* A = &As;
-  TailSm<NDIM> T(A, sm_dyn);
+  __shared__ unsigned nbflag[2];
+  if (threadIdx.x < 2) nbflag[threadIdx.x] = 0u;   // published by the cluster barrier below
+  TailSm<NDIM> T(A, sm_dyn, nbflag);
   // stage faces and weight tables of every PCG level, and the top level's residual
   for (int q = A->L0; q < A->L; ++q) T.stage(q);
   {
@@ -647,6 +683,7 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
   a.s = ctx->prm.scale;
   a.interp = ctx->prm.interp;
   a.max_iter = ctx->prm.max_iter;
+  a.nbsync = ctx->kn.tail_nbsync ? 1 : 0;
   a.NL = ctx->NL;
   a.Ainv = ctx->Ainv;
   for (int q = L0; q <= ctx->L; ++q) {
