@@ -38,7 +38,8 @@ def full(path):
     h, u = rows[0], rows[1]
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
-            "launch__registers_per_thread", "lts__t_sector_hit_rate.pct", "smsp__inst_executed.sum"]
+            "launch__registers_per_thread", "lts__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
+            "lts__t_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
     out = ["# ncu --set full --clock-control none (one capture per listed launch)",
            "# units: " + ", ".join(f"{w}={u[h.index(w)]}" for w in want if w in h)]
     recs = []
