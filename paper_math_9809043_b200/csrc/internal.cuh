@@ -153,6 +153,7 @@ struct mss_ctx {
     bool fused_resid = true;  // MSS_FUSED_RESID
     bool prolong_pairs = true;// MSS_PROLONG_PAIRS
     bool tail_nbsync = false; // MSS_TAIL_NBSYNC: neighbour-only sync after tail half-sweeps
+    bool fused_prolong = false;// MSS_FUSED_PROLONG: a8 inside the first post-smoothing TMA pair
   } kn;
   // TMA tensor maps (pairtma.cuh), cached by base pointer and kind (opaque 128-byte images)
   struct TmapEnt {

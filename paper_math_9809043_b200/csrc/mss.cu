@@ -377,6 +377,7 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
   ctx->kn.tail_nbsync = geti("MSS_TAIL_NBSYNC", 0) != 0;
+  ctx->kn.fused_prolong = geti("MSS_FUSED_PROLONG", 0) != 0;
 }
 
 // looked up once, thread-safely (loopback ranks set up their contexts on parallel threads)
@@ -487,7 +488,7 @@ static bool pair_ok(const mss_ctx* ctx, int k) {
 }
 
 static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, double* zout, int col1, bool first,
-                   bool res = false) {
+                   bool res = false, const ProArgs* pro = nullptr) {
   Level& l = ctx->lv[k];
   const int hx = l.nx / 2;
   const int bx = (hx + kPX - 3) / (kPX - 2), by = (l.ny + kPY - 3) / (kPY - 2);
@@ -535,7 +536,14 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     const int tkch = (l.nz + tnch - 1) / tnch;
     tnch = (l.nz + tkch - 1) / tkch;
     const dim3 tgrid(bx, tby, tnch), tblk(kPX, TY);
-    if (res) {
+    if (pro) {
+      if (big)
+        k_sweep2t_col<false, PairBig, false, true><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(
+            M, l.dev(), zin, zout, col1, tkch, gz, gf, nullptr, *pro);
+      else
+        k_sweep2t_col<false, PairSmall, false, true><<<tgrid, tblk, PairSmall::SMEM, ctx->stream>>>(
+            M, l.dev(), zin, zout, col1, tkch, gz, gf, nullptr, *pro);
+    } else if (res) {
       if (big)
         k_sweep2t_col<false, PairBig, true><<<tgrid, tblk, PairBig::SMEM, ctx->stream>>>(M, l.dev(), zin, zout, col1, tkch,
                                                                                        gz, gf, l.resb);
@@ -558,6 +566,7 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
     ctx->launches++;
     return MSS_OK;
   }
+  if (pro) return set_err(MSS_EINVAL, "fused prolongation needs the TMA pair kernel");
   const dim3 grid(bx, by, nch), blk(kPX, kPY);
   if (first) k_sweep2_col<true, kPY><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
   else k_sweep2_col<false, kPY><<<grid, blk, 0, ctx->stream>>>(l.dev(), r, zin, zout, col1, kch);
@@ -570,7 +579,7 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
 // run as fused pairs ping-ponging between the level's z and s buffers (the Level's z
 // pointer is swapped when the result lands in s, so z must be the level's own z).
 static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero,
-                     double* dot_last = nullptr) {
+                     double* dot_last = nullptr, const ProArgs* pro = nullptr) {
   Level& l = ctx->lv[k];
   if (ctx->prm.splitting == 1) {
     // modified Jacobi: the m = (n_half-1)/2 SGS steps become m Jacobi steps,
@@ -601,7 +610,7 @@ static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half
     if (!z_zero) TRY(do_halo(ctx, k, cur, 2));
     for (int pi = 0; pi < npairs; ++pi) {
       const int col1 = (first_colour + 2 * pi) & 1;
-      TRY(op_pair(ctx, k, r, cur, oth, col1, z_zero && pi == 0));
+      TRY(op_pair(ctx, k, r, cur, oth, col1, z_zero && pi == 0, false, pi == 0 ? pro : nullptr));
       std::swap(cur, oth);
       TRY(do_halo(ctx, k, cur, 2));
     }
@@ -803,6 +812,15 @@ static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
   return op_restrict_yz(ctx, k, c.r);
 }
 
+// MSS_FUSED_PROLONG: exactly the levels where op_prolong_add would run k_prolong_pairs and
+// the post-smoothing's first step is a TMA pair (so the fused values are bit-identical)
+static bool fused_prolong_ok(mss_ctx* ctx, int k, int nh, int sgs) {
+  const Level& f = ctx->lv[k];
+  return ctx->kn.fused_prolong && sgs && nh >= 2 && ctx->ndim == 3 && col_ok(ctx, f) && !dist_level(ctx, k) &&
+         f.w[0] && f.w[1] && f.w[2] && ctx->kn.prolong_pairs &&
+         (int64_t)(f.nx / 2) * f.ny * f.nz < ((int64_t)1 << 32) && pair_ok(ctx, k) && f.txp && pair_tma_on(ctx);
+}
+
 static int precond(mss_ctx* ctx, int k) {
   Level& l = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
@@ -819,6 +837,14 @@ static int precond(mss_ctx* ctx, int k) {
   } else {
     CK(cudaMemsetAsync(c.x, 0, sizeof(double) * c.N, ctx->stream));
     TRY(pcg_level(ctx, k + 1));
+  }
+  if (fused_prolong_ok(ctx, k, nh, sgs)) {
+    // a8 inside the first post-smoothing pair: its red sweep is the only reader of the
+    // prolongated black values (the black sweep after it overwrites them)
+    const ProArgs pa{c.x, reinterpret_cast<const W1*>(l.w[0]), reinterpret_cast<const W1*>(l.w[1]),
+                     reinterpret_cast<const W1*>(l.w[2]), (int)c.nx, (int)c.ny};
+    TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho, &pa));
+    return MSS_OK;
   }
   TRY(op_prolong_add(ctx, k, c.x, l.z, sgs ? 1 : -1));           // z_black += (E y) (a8)
   TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho));  // post-smoothing (a9), rho = r.z
@@ -1445,6 +1471,10 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairSmall::SMEM));
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairBig, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairBig::SMEM));
       CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)PairSmall::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairBig, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)PairBig::SMEM));
+      CK(cudaFuncSetAttribute(k_sweep2t_col<false, PairSmall, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)PairSmall::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
       CK(cudaFuncSetAttribute(k_spmv_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));

@@ -77,6 +77,14 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* m, int c
       : "memory");
 }
 
+// a8 fused into the first post-smoothing pair (MSS_FUSED_PROLONG): the coarse correction
+// y of level+1 and the fine level's 1-D weight tables (k_prolong_pairs' operands)
+struct ProArgs {
+  const double* y;
+  const W1 *wx, *wy, *wz;
+  int ncx, ncy;
+};
+
 struct PairCtx {
   double* smd;
   double* red;
@@ -89,7 +97,44 @@ struct PairCtx {
   int gz, gf;      // TMA plane offsets of the z map and of the face / r maps (ghost planes)
   bool bot, top;   // the slab touches the global bottom / top of the domain
   bool valid, interior;
+  int nx, ny, mb;
+  ProArgs pro;
 };
+
+// (E y) at fine cell (i, j, k): the expression and operand order of k_prolong_pairs, so the
+// fused path adds bit-identical values
+__device__ __forceinline__ double pro_ey(const ProArgs& A, int i, int j, int k) {
+  const int64_t cp = (int64_t)A.ncx * A.ncy;
+  const W1 ax = A.wx[i], ay = A.wy[j], az = A.wz[k];
+  auto Yv = [&](int a, int bb, int cc) { return __ldg(A.y + a + (int64_t)A.ncx * bb + cp * cc); };
+  double acc = ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0, az.I0) + ax.w1 * Yv(ax.I1, ay.I0, az.I0)) +
+               ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1, az.I0) + ax.w1 * Yv(ax.I1, ay.I1, az.I0));
+  acc *= az.w0;
+  acc += az.w1 * (ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0, az.I1) + ax.w1 * Yv(ax.I1, ay.I0, az.I1)) +
+                  ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1, az.I1) + ax.w1 * Yv(ax.I1, ay.I1, az.I1)));
+  return acc;
+}
+
+// add (E y) to the black cells of plane p's staged z tile that this thread is responsible for:
+// its own pair's black cell (index b) and, on the tile's edge, the apron cells the ring reads
+// at plane p: left apron pair cell 1 (tx = 0, b = 1), right apron pair cell 0 (tx = last,
+// b = 0), and rows j0-1 / j0+TY (black index 1-b there).  Out-of-domain cells stay 0.
+template <class G>
+__device__ __forceinline__ void pro_fix_plane(const PairCtx& C, double* S, int p, int b) {
+  if (p < 0 || p >= C.nz) return;
+  double* Z = S + G::oZ;
+  auto fix = [&](int zr, int zc, int i, int j) {   // zr, zc: row / column in the z tile
+    if (i >= 0 && i < C.nx && j >= 0 && j < C.ny) Z[zr * G::ZW + zc] += pro_ey(C.pro, i, j, p);
+  };
+  const int i0 = 2 * (C.mb + C.tx), j = C.j0 + C.ty;
+  fix(C.ty + 1, C.lx + 2 + b, i0 + b, j);
+  if (C.tx == 0 && b == 1) fix(C.ty + 1, C.lx + 1, i0 - 1, j);
+  if (C.tx == kPX - 1 && b == 0) fix(C.ty + 1, C.lx + 4, i0 + 2, j);
+  if (C.ty == 0) fix(0, C.lx + 2 + (1 - b), i0 + 1 - b, j - 1);
+  if (C.ty == G::TY - 1) fix(G::TY + 1, C.lx + 2 + (1 - b), i0 + 1 - b, j + 1);
+  // these generic-proxy writes precede the slot's later TMA (async-proxy) refill
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // plane p -> slot s; its fill number (p - kb) >> 2 gives the mbarrier parity
 template <bool FIRST, class G>
@@ -128,7 +173,7 @@ struct PairSecT<true> : PairSec {
 // the second step leaves the black cell unchanged and writes its residual r - A z (the red
 // residual is zero after the sweep) to resB, one value per cell pair, in the
 // operand order of k_resid_restrict_col.
-template <bool FIRST, class G, int U, int P, bool RES = false>
+template <bool FIRST, class G, int U, int P, bool RES = false, bool PRO = false>
 __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, double2& zdn,
                                           const PairSecT<RES>& sin, PairSecT<RES>& sout) {
   if (k > C.ke + 1) return;   // block-uniform
@@ -140,6 +185,9 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
     mbar_wait(&C.bar[S1i], ((k + 1 - C.kb) / G::NS) & 1);   // plane k's own stage was awaited a step ago
     const double* S0 = C.smd + S0i * G::SD;
     const double* S1 = C.smd + S1i * G::SD;
+    // PRO: plane k+1's black cells get (E y) from their owners now; nobody else reads that
+    // stage before this step's barrier, every later read comes after it
+    if constexpr (PRO) pro_fix_plane<G>(C, C.smd + S1i * G::SD, k + 1, P);
     double v1 = 0.0;
     if (C.valid) {
       const double* txr = S0 + G::oTx + ty * XW + lx;
@@ -207,13 +255,13 @@ __device__ __forceinline__ void pair_step(const PairCtx& C, int k, int64_t& c, d
 }
 
 // UN consecutive plane steps starting at parity p0 (sa / sb ping-pong the second-colour state)
-template <bool FIRST, class G, int P0, bool RES, int U = 0>
+template <bool FIRST, class G, int P0, bool RES, bool PRO, int U = 0>
 __device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, double2& zdn, PairSecT<RES>& sa,
                                            PairSecT<RES>& sb) {
   if constexpr (U < G::UN) {
-    if constexpr ((U & 1) == 0) pair_step<FIRST, G, U, P0 ^ (U & 1), RES>(C, k + U, c, zdn, sa, sb);
-    else pair_step<FIRST, G, U, P0 ^ (U & 1), RES>(C, k + U, c, zdn, sb, sa);
-    pair_group<FIRST, G, P0, RES, U + 1>(C, k, c, zdn, sa, sb);
+    if constexpr ((U & 1) == 0) pair_step<FIRST, G, U, P0 ^ (U & 1), RES, PRO>(C, k + U, c, zdn, sa, sb);
+    else pair_step<FIRST, G, U, P0 ^ (U & 1), RES, PRO>(C, k + U, c, zdn, sb, sa);
+    pair_group<FIRST, G, P0, RES, PRO, U + 1>(C, k, c, zdn, sa, sb);
   }
 }
 
@@ -221,11 +269,13 @@ __device__ __forceinline__ void pair_group(const PairCtx& C, int k, int64_t& c, 
 // on a z-slab level, whose maps start at its ghost planes; there the first colour is also
 // computed on the ghost planes -1 and nz (redundantly, from the halo-exchanged z, r and
 // faces) so the second colour of the slab's end planes needs no exchange in between.
-template <bool FIRST, class G, bool RES = false>
+template <bool FIRST, class G, bool RES = false, bool PRO = false>
 __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
     k_sweep2t_col(const __grid_constant__ PairMaps M, LevelDev L, const double* __restrict__ zin,
-                  double* __restrict__ zout, int col1, int kchunk, int gz, int gf, double* __restrict__ resB = nullptr) {
+                  double* __restrict__ zout, int col1, int kchunk, int gz, int gf, double* __restrict__ resB = nullptr,
+                  ProArgs pro = ProArgs{}) {
   static_assert(!(RES && FIRST), "the fused residual follows a sweep from a nonzero z");
+  static_assert(!(PRO && (FIRST || RES)), "the fused prolongation precedes the first post-smoothing pair");
   extern __shared__ __align__(128) double smd[];
   PairCtx C;
   C.smd = smd;
@@ -252,6 +302,10 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
   C.interior = C.valid && C.tx >= 1 && C.tx <= kPX - 2 && C.ty >= 1 && C.ty <= G::TY - 2;
   C.gz = gz;
   C.gf = gf;
+  C.nx = nx;
+  C.ny = ny;
+  C.mb = mb;
+  C.pro = pro;
   C.bot = (L.z0 == 0);
   C.top = (L.z0 + C.nz >= L.nzg);
   C.kb = max(C.k0 - 1, C.bot ? 0 : -1);
@@ -272,9 +326,20 @@ __global__ void __launch_bounds__(kPX * G::TY, G::MINB)
   const int pA = (i0 + j + L.z0 + col1 + C.kb) & 1;
   PairSecT<RES> sa{}, sb{};
   mbar_wait(&C.bar[0], 0);
+  if constexpr (PRO) {
+    // plane kb's black cells (index 1 - pA) in the stage, and the carried plane kb-1 (black
+    // index pA there) in registers, before the first step reads them
+    pro_fix_plane<G>(C, C.smd, C.kb, 1 - pA);   // bounds-checked per cell, apron duties included
+    if (C.valid && C.kb - 1 >= 0) {
+      const double e = pro_ey(C.pro, i0 + pA, j, C.kb - 1);
+      if (pA) zdn.y += e;
+      else zdn.x += e;
+    }
+    __syncthreads();
+  }
   for (int k = C.kb; k <= C.ke + 1; k += G::UN) {
-    if (pA) pair_group<FIRST, G, 1, RES>(C, k, c, zdn, sa, sb);
-    else pair_group<FIRST, G, 0, RES>(C, k, c, zdn, sa, sb);
+    if (pA) pair_group<FIRST, G, 1, RES, PRO>(C, k, c, zdn, sa, sb);
+    else pair_group<FIRST, G, 0, RES, PRO>(C, k, c, zdn, sa, sb);
   }
 }
 

@@ -663,3 +663,42 @@ def test_solve_host_batch_matches_device_solves(torch_mod, use_lift, pinned):
     one = [host(x0s[0])]
     it1, _, _ = s.solve_host_batch([fh[0]], one, rel_tol=w.rel_tol)
     assert list(it1[0]) == list(iters[0]) and np.array_equal(one[0].numpy(), xh[0].numpy())
+
+
+FUSED_PRO_CASES = [
+    ("C5_128", lambda: make_workload("C5", n=128)),
+    ("C2", lambda: make_workload("C2")),
+    ("3d_ragged", lambda: random_problem(3, (44, 36, 28), seed=2)),
+    ("3d_ragged_tiles", lambda: random_problem(3, (100, 52, 24), seed=7,
+                                               bc=bc_table(3, {"x-": (DIRICHLET, 1.0), "y+": (DIRICHLET, -1.0)}))),
+]
+
+
+@pytest.mark.parametrize("ty", ["16", "8"])
+@pytest.mark.parametrize("name,mk", FUSED_PRO_CASES, ids=[c[0] for c in FUSED_PRO_CASES])
+def test_fused_prolongation_is_bitwise(torch_mod, name, mk, ty, monkeypatch):
+    """MSS_FUSED_PROLONG (a8 inside the first post-smoothing TMA pair: each black cell gets
+    (E y) in the shared ring from its owner thread, apron cells from the tile's edge threads,
+    plane kb-1 in registers) gives the same bits as the separate k_prolong_pairs pass: same
+    expression, same operand order, and the prolongated black values are read only by that
+    pair's red sweep."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    monkeypatch.setenv("MSS_PAIR", "1")
+    monkeypatch.setenv("MSS_PAIR_TY", ty)
+    w = mk()
+    out = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("MSS_FUSED_PROLONG", fused)
+        s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth)
+        rng = np.random.default_rng(3)
+        r = cu(torch, rng.standard_normal(s.level_N(0)))
+        zp, its = s.precond(0, r, rel_tol=w.rel_tol)
+        x, rep = s.solve(cu(torch, w.f), rel_tol=w.rel_tol)
+        launches = rep.kernel_launches
+        out.append((zp.cpu().numpy(), list(its), x.cpu().numpy(), list(rep.iters), rep.true_rel_res, launches))
+        s.close()
+    a, b = out
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+    assert np.array_equal(a[2], b[2]) and a[3] == b[3] and a[4] == b[4]
+    assert b[5] < a[5]   # the separate prolongation launches are gone
