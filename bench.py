@@ -41,6 +41,9 @@ def parse():
                     help="take the multi-rank path (process group, NCCL z-slab context) even at one rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=96, help="oracle sample grid size (same recipe)")
+    ap.add_argument("--control", default="graph", choices=["graph", "host"],
+                    help="graph: host-driven levels as one captured CUDA graph with device-side loop "
+                         "control (a12, default); host: the host loop (MSS_GRAPH=0)")
     return ap.parse_args()
 
 
@@ -128,6 +131,23 @@ def oracle_sample(cfg, n, repeats=1):
             "cpu_per_wall": ratio, "seconds": t, "host_cpus": os.cpu_count()}
 
 
+def cpu_full_config(cfg, N):
+    """The oracle's one full run on the bench's own config (tests/golden/<cfg>_oracle.json,
+    written by scripts/oracle_c5.py on the build container's host, one thread): a stored
+    measurement for context beside the live bounded sample, not re-timed here."""
+    path = os.path.join(ROOT, "tests", "golden", f"{cfg.lower()}_oracle.json")
+    try:
+        g = json.load(open(path))
+    except Exception:
+        return None
+    if list(g.get("n", [])) == [] or g["n"][0] * g["n"][1] * g["n"][2] != N:
+        return None
+    sec = g["seconds"]["solve"]
+    return {"value": N / sec, "unit": "unknowns/s", "solve_s": sec, "iters": g["iters"], "cores": 1,
+            "kind": "oracle", "where": "build-container host CPU, one thread, scripts/oracle_c5.py (stored, not re-run)",
+            "peak_rss_gib": g.get("peak_rss_gib")}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -176,6 +196,7 @@ def main():
     import numpy as np
     import torch
 
+    os.environ["MSS_GRAPH"] = "0" if args.control == "host" else os.environ.get("MSS_GRAPH", "1")
     torch.cuda.set_device(local)
     dist = None
     multi = world > 1 or args.force_dist
@@ -204,7 +225,11 @@ def main():
     K = torch.from_numpy(np.ascontiguousarray(w.K[:, z0:z1])).to(dev)
     f_np = np.ascontiguousarray(w.f[z0:z1]).ravel() if w.ndim == 3 else w.f.ravel()
     f = torch.from_numpy(f_np).to(dev)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, comm=comm)
+    setup_wall_ms = 1e3 * (time.perf_counter() - t_setup)
+    info0 = s.info()
     x = torch.zeros(s.N, dtype=torch.float64, device=dev)
     del K
     meas = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -219,7 +244,6 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    s.profile(True, 0)
     launches0 = s.kernel_launches()
     if dist:
         dist.barrier()
@@ -235,13 +259,29 @@ def main():
         dist.barrier()
     ms_total = e0.elapsed_time(e1)
     launches = s.kernel_launches() - launches0
-    prof = s.profile_read()
-    s.profile(False, 0)
-    ck = clocks.stop()
     ms_max = D.max_over_ranks(ms_total) if dist else ms_total
     ms_step = ms_max / args.steps
     # strong scaling: the same global problem is split across the ranks
     value = w.N / (ms_step / 1e3)
+
+    # Per-kernel timing: a second pass of K steps with every launch of every level bracketed
+    # by CUDA events on the library's stream (the bracketing needs the host-driven loop, so
+    # this pass runs it; the kernels are the same ones the graph launches).
+    s.profile(True, s.levels - 1)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        x, rep_p = s.solve(f, x, rel_tol=w.rel_tol)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    ms_prof_total = p0.elapsed_time(p1)
+    prof = s.profile_read()
+    s.profile(False, 0)
+    ck = clocks.stop()
 
     # roofline: the dominant kernel = the level-0 kernel class with the most device time
     # (the fused red+black pair on 512^3, a single half-sweep where pairs are off)
@@ -251,10 +291,20 @@ def main():
             dom = key
     cnt, ms, by = prof[dom]
     achieved = (by / cnt) / (ms / cnt / 1e3) / 1e9
-    step_share = ms / ms_total
+    step_share = ms / ms_prof_total
     breakdown = {f"{k[0]}@L{k[1]}": {"launches": v[0], "ms": round(v[1], 3),
-                                      "GB/s": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[1] > 0 else None}
+                                      "GB/s": round(v[2] / (v[1] / 1e3) / 1e9, 1) if v[1] > 0 and v[2] > 0 else None}
                  for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    # per-level device time per step (the tail's whole cluster launch is booked on its level)
+    per_level = [0.0] * s.levels
+    for (name, lvl), (c_, ms_, _) in prof.items():
+        per_level[lvl] += ms_ / args.steps
+    split = {"ms_per_step_by_level": [round(v, 3) for v in per_level],
+             "profiled_ms_per_step": round(ms_prof_total / args.steps, 3)}
+    if dist:
+        allsplit = [None] * world
+        dist.all_gather_object(allsplit, split)
+        split = {"per_rank": allsplit}
 
     # e2e through the public API with host buffers (pinned), copies inside the region:
     # mss_solve_host_batch over the K steps (step i's f uploaded and step i-1's x read back
@@ -304,7 +354,15 @@ def main():
                          "traffic": load_traffic(args.config, dom[0]), "share_of_step": step_share,
                          "launch_ms": ms / cnt},
             "kernels": breakdown,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": ck,
+            "kernel_timing": "second pass of the same K steps, every launch bracketed by CUDA events on the "
+                             "library stream (host-driven loop); share_of_step is relative to that pass",
+            "level_split": split,
+            "control": "graph (a12: host-driven levels in one CUDA graph, device-side stop tests)"
+                       if rep.graph else "host loop",
+            "setup_ms": info0.setup_ms, "setup_wall_ms": setup_wall_ms,
+            "setup_coarsest_ms": info0.setup_coarsest_ms,
+            "cpu_baseline": cpu, "cpu_full_config": cpu_full_config(args.config, w.N) if rank == 0 else None,
+            "e2e": e2e, "gpu_launches": launches, "clocks": ck,
         }
         print(json.dumps(out), flush=True)
     if dist:

@@ -55,7 +55,8 @@ typedef struct {
   int     interp;       /* 0 = linear extension (default), 1 = piecewise constant */
   int     max_iter;     /* PCG iteration cap per call per level; default 500 (paper silent, Q16) */
   int     coarse_min;   /* stop coarsening once N_k <= coarse_min; default 512 (Q10)            */
-  int     use_lift;     /* 1 = x0 = P_bf (default); 0 = x0 = 0                       */
+  int     use_lift;     /* 1 = x0 = P_bf (default); 0 = x0 = the caller's x on entry
+                           to mss_solve (pass zeros for x0 = 0)                                */
   int64_t tail_cells;   /* levels with N_k <= tail_cells run inside one persistent cluster
                            kernel per call (device-resident control); default 65536; 0 = off  */
   int64_t gather_below; /* distributed: levels with N_k < gather_below are replicated; 64^3     */
@@ -88,6 +89,11 @@ typedef struct {
   int64_t kernel_launches;               /* library kernels launched during the solve */
   int     tail_level;                    /* first level run device-resident (-1 = none) */
   int     tail_kind;                     /* 0 none, 1 L2-resident cluster, 2 smem-resident cluster */
+  double  setup_ms;                      /* wall time of mss_setup* (excluded from the solve time,
+                                            P:544-545, reported separately) */
+  double  setup_coarsest_ms;             /* of which: blocked Cholesky + inverse of A_L (a3) */
+  int     graph;                         /* 1: the host-driven levels ran as one captured CUDA graph
+                                            with device-side loop control (a12); 0: host loop */
 } mss_info;
 
 int         mss_default_params(mss_params* p);
@@ -148,7 +154,9 @@ int mss_solve_host(mss_ctx* ctx, const double* f_host, double* x_host, double re
  * while solve i runs (two device f / x buffers, 4 N_local doubles allocated on first use,
  * kept until mss_free).  Host buffers should be pinned (pageable ones are correct but do
  * not overlap).  Caller-owned: the host arrays, which must not be touched until the call
- * returns; every x_host[i] holds its result on return.  iters_per_level: host, nrhs * L1
+ * returns; every x_host[i] holds its result on return.  With use_lift == 0 the upload of
+ * x_host[i+1] may run before x_host[i] is written back, so the x_host entries must not alias
+ * (they may alias freely with use_lift == 1, where x_host is output only).  iters_per_level: host, nrhs * L1
  * (row i = solve i, nullable); true_rel_res: host, nrhs (nullable).  Returns the largest
  * status of the solves (0 or MSS_NOT_CONVERGED); the first hard error aborts the batch and
  * is returned (x_host of later problems is then unspecified).  Same threading rule as
@@ -158,9 +166,20 @@ int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, do
 
 int mss_get_info(const mss_ctx* ctx, mss_info* info);            /* last solve's report */
 
-/* ---- kernel-level hooks (parity tests; level-local compact device vectors) ---- */
-int mss_get_faces(const mss_ctx* ctx, int level, int dir, double* T);        /* device out */
-int mss_apply_A(mss_ctx* ctx, int level, const double* x, double* y);        /* y = A_k x   */
+/* ---- kernel-level hooks (parity tests) ---------------------------------------------
+ * Level-local compact device vectors (N_k doubles, x fastest; caller-owned, read or written
+ * only during the call, which synchronises the context's stream before returning).  Every
+ * hook copies its inputs into the level's own ghosted work buffers and runs the solver's own
+ * dispatch on them.  Errors: MSS_EINVAL (bad level / null pointer), MSS_ECUDA. */
+/* T: device out, the level's face transmissibilities along dir (0 x, 1 y, 2 z) in the
+ * layout of internal.cuh ((n_x+1) n_y n_z for dir 0, ...): a1 (harmonic-mean K, Dirichlet
+ * 2K A/h, Neumann 0) on level 0, a2 (Reading B)
+ * on the coarse levels. */
+int mss_get_faces(const mss_ctx* ctx, int level, int dir, double* T);
+/* y = A_k x, (A p)_c = sum_f T_f (p_c - p_nbr(f)) (O4), by the generic
+ * one-thread-per-cell kernel (the solver's own SpMV is mss_cg_direction). */
+int mss_apply_A(mss_ctx* ctx, int level, const double* x, double* y);
+/* *out (host) = a . b over the level's cells (the CG inner products of P:440-441). */
 int mss_dot(mss_ctx* ctx, int level, const double* a, const double* b, double* out /*host*/);
 /* n_half alternating half-sweeps on z starting with colour first_color (0 = red, the
  * (i+j+k)-even cells); z_is_zero = 1 takes z = 0 on entry (O12). */
@@ -176,8 +195,35 @@ int mss_prolong_add(mss_ctx* ctx, int level, const double* coarse_y, double* z, 
 int mss_precond(mss_ctx* ctx, int level, const double* r, double* z, double rel_tol,
                 int64_t* iters_per_level);
 int mss_coarse_solve(mss_ctx* ctx, const double* b, double* x);   /* x = A_L^{-1} b */
-/* b (O5) and x0 = P_bf (O6) for a source density f. */
+/* b (O5: b_c = f_c V_c + sum_Dirichlet T_f g_f + sum_Neumann A_f q_f) and
+ * x0 = P_bf (O6) for a source density f.  x0 nullable. */
 int mss_rhs_lift(mss_ctx* ctx, const double* f, double* b, double* x0);
+
+/* a10 exactly as the solver runs it (Templates CG): p_out = z + (rho/rho_prev) p_in
+ * (p_out = z when first != 0; p_in may then be NULL), q = A_k p_out and *pq (host) = p_out . q,
+ * by the level's production kernel (TMA-staged SpMV on padded levels, else the column walk,
+ * else the generic kernel). */
+int mss_cg_direction(mss_ctx* ctx, int level, const double* z, const double* p_in, double rho, double rho_prev,
+                     int first, double* p_out, double* q, double* pq);
+/* a11 exactly as the solver runs it: alpha = rho / pq; x += alpha p; r -= alpha q
+ * (x, r updated in place); *rr (host) = ||r||^2 after the update. */
+int mss_cg_update(mss_ctx* ctx, int level, double* x, double* r, const double* p, const double* q, double rho,
+                  double pq, double* rr);
+/* r = b - A_k x and *rr (host, nullable) = ||r||^2 by the solver's residual kernel (the TMA
+ * SpMV in residual mode on padded levels): a4's r0 and O15's true residual. */
+int mss_residual(mss_ctx* ctx, int level, const double* b, const double* x, double* r, double* rr);
+/* a5 + a6 exactly as the preconditioner runs them (Eq. 2.10): z = 2m+1
+ * alternating half-sweeps from z = 0 starting red (O12), then
+ * coarse_b = R (r - A_k z) on level+1 (R = E^T).  Under SGS the residual is taken on black
+ * cells only (after the closing red sweep the red residual is zero up to rounding); on TMA
+ * pair levels the closing red sweep and the black residual are one fused pass.  z: device
+ * out, N_k; coarse_b: device out, N_{k+1}. */
+int mss_presmooth_restrict(mss_ctx* ctx, int level, const double* r, double* z, double* coarse_b);
+/* a8 + a9 exactly as the preconditioner runs them (Eq. 2.10): z += E y
+ * (y = coarse_y on level+1), then 2m+1 half-sweeps starting red with *rho (host, nullable)
+ * = r . z fused into the last.  z: device in/out, N_k. */
+int mss_prolong_postsmooth(mss_ctx* ctx, int level, const double* coarse_y, const double* r, double* z,
+                           double* rho);
 
 /* ---- distributed (z-slabs across ranks; NCCL over NVLink / NVSwitch) ---------------
  * The global grid is split into z-slabs: rank r owns global planes [z_begin, z_end) of

@@ -112,6 +112,7 @@ struct mss_ctx {
   // solve state
   double eps2 = 0;
   int64_t launches = 0;
+  int64_t nswap = 0;                       // Level z/s pointer swaps so far (a captured graph bakes pointers in)
   mss_info info;
   std::vector<void*> allocs;
   // live per-kernel timing (mss_profile)
@@ -174,4 +175,21 @@ struct mss_ctx {
   int64_t slab_unit = 1;                   // slab boundaries are multiples of this many level-0 planes
   mss::Comm* comm = nullptr;
   void* loop_group = nullptr;              // loopback group (tests)
+  // device-resident control of the host-driven levels (a12): the level-0 PCG, with every
+  // nested host-driven level, captured once into a CUDA graph whose loops are conditional
+  // WHILE / IF nodes set on the device (control.cuh); re-captured when Level pointers swap
+  int graph_knob = 1;                      // MSS_GRAPH: 1 single-GPU contexts (default), 2 also NCCL, 0 off
+  bool capturing = false;
+  bool graph_failed = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_gen = -1;                  // nswap at capture
+  std::vector<cudaStream_t> cap_streams;   // one per nesting depth of the capture
+  int cap_depth = 0;
+  cudaGraph_t cap_top = nullptr;
+  void* dctl = nullptr;                    // mss::LevelCtl[MSS_MAX_LEVELS]
+  int64_t g_per_call[MSS_MAX_LEVELS] = {}; // launches per call / per iteration of a captured level
+  int64_t g_per_iter[MSS_MAX_LEVELS] = {};
+  int64_t g_nested_launches = 0;           // capture bookkeeping (pcg_graph)
+  int g_tail_level = -1, g_tail_kind = 0;  // the tail the captured graph launches
 };

@@ -271,61 +271,7 @@ __global__ void k_dense_assemble(LevelDev L, double* __restrict__ A) {
   }
 }
 
-// Hand-written unblocked right-looking Cholesky, A = L L^T, in place on the lower
-// triangle (row-major), one CTA.  flag = 1 if a pivot is not positive.
-__global__ void k_cholesky(double* __restrict__ A, int n, int* flag) {
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x == 0) {
-      const double dj = A[(int64_t)j * n + j];
-      if (!(dj > 0.0)) bad = 1;
-      else A[(int64_t)j * n + j] = sqrt(dj);
-    }
-    __syncthreads();
-    if (bad) {
-      if (threadIdx.x == 0) *flag = 1;
-      return;
-    }
-    const double ljj = A[(int64_t)j * n + j];
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[(int64_t)i * n + j] /= ljj;
-    __syncthreads();
-    const int m = n - j - 1;
-    for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) {
-      const int ii = (int)(idx / m), kk = (int)(idx % m);
-      if (kk > ii) continue;
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      A[(int64_t)i * n + k] -= A[(int64_t)i * n + j] * A[(int64_t)k * n + j];
-    }
-    __syncthreads();
-  }
-}
-
-// X = (L L^T)^{-1}: thread j solves L y = e_j then L^T x = y (column j of X).
-__global__ void k_chol_inverse(const double* __restrict__ Lf, double* __restrict__ X, int n) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  for (int i = 0; i < j; ++i) X[(int64_t)i * n + j] = 0.0;
-  for (int i = j; i < n; ++i) {
-    double acc = (i == j) ? 1.0 : 0.0;
-    for (int k = j; k < i; ++k) acc -= Lf[(int64_t)i * n + k] * X[(int64_t)k * n + j];
-    X[(int64_t)i * n + j] = acc / Lf[(int64_t)i * n + i];
-  }
-  for (int i = n - 1; i >= 0; --i) {
-    double acc = X[(int64_t)i * n + j];
-    for (int k = i + 1; k < n; ++k) acc -= Lf[(int64_t)k * n + i] * X[(int64_t)k * n + j];
-    X[(int64_t)i * n + j] = acc / Lf[(int64_t)i * n + i];
-  }
-}
-
-__global__ void k_symmetrize(const double* __restrict__ X, double* __restrict__ S, int n) {
-  const int64_t total = (int64_t)n * n;
-  for (int64_t t = gtid(); t < total; t += gstride()) {
-    const int64_t i = t / n, j = t % n;
-    S[t] = 0.5 * (X[i * n + j] + X[j * n + i]);
-  }
-}
+// The coarsest level's blocked Cholesky and inverse are in dense.cuh (a3).
 
 // ------------------------------------------------------------------ a4: RHS and lift
 struct BCDev {

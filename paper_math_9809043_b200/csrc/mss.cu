@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -25,6 +26,8 @@
 #include "colwalk.cuh"
 #include "pairtma.cuh"
 #include "fields.cuh"
+#include "dense.cuh"
+#include "control.cuh"
 #include "comm.cuh"
 
 using namespace mss;
@@ -378,6 +381,7 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
   ctx->kn.tail_nbsync = geti("MSS_TAIL_NBSYNC", 0) != 0;
   ctx->kn.fused_prolong = geti("MSS_FUSED_PROLONG", 0) != 0;
+  ctx->graph_knob = geti("MSS_GRAPH", 1);
 }
 
 // looked up once, thread-safely (loopback ranks set up their contexts on parallel threads)
@@ -576,11 +580,22 @@ static int op_pair(mss_ctx* ctx, int k, const double* r, const double* zin, doub
 
 // n_half alternating half-sweeps starting with `first_colour`; the last one also
 // reduces r.z into *dot_last when given.  On pair-eligible levels consecutive half-sweeps
-// run as fused pairs ping-ponging between the level's z and s buffers (the Level's z
-// pointer is swapped when the result lands in s, so z must be the level's own z).
+// run as fused pairs ping-ponging between the level's z and s buffers (z must be the
+// level's own z).  From z = 0 the first pair reads no z, so the ping-pong starts on the
+// buffer that makes the last of the npairs + `extra` pair writes land in the level's z
+// (`extra` pairs follow in the caller, which then gets the current buffer in *last): the
+// Level's pointers never swap on that path, which a captured CUDA graph relies on.  Where
+// the parity cannot be arranged (a nonzero z with an odd pair count) the Level's z and s
+// pointers are swapped instead (counted in ctx->nswap).
 static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half, int first_colour, bool z_zero,
-                     double* dot_last = nullptr, const ProArgs* pro = nullptr) {
+                     double* dot_last = nullptr, const ProArgs* pro = nullptr, int extra = 0,
+                     double** last = nullptr) {
   Level& l = ctx->lv[k];
+  const bool pair_branch = ctx->prm.splitting == 0 && z == l.z && n_half >= 2 && pair_ok(ctx, k);
+  // a fused prolongation is consumed only by the first TMA pair; anything else would
+  // silently drop the coarse-grid correction (precond skips op_prolong_add for it)
+  if (pro && !(pair_branch && (n_half - (dot_last ? 1 : 0)) / 2 >= 1 && l.txp && pair_tma_on(ctx)))
+    return set_err(MSS_EINVAL, "fused prolongation requested where the first step is not a TMA pair");
   if (ctx->prm.splitting == 1) {
     // modified Jacobi: the m = (n_half-1)/2 SGS steps become m Jacobi steps,
     // ping-ponging between the level's z and s buffers (z must be the level's z)
@@ -594,16 +609,18 @@ static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half
                  red_to(ctx, dot, k, 0));
       }
       std::swap(l.z, l.s);
+      ctx->nswap++;
       tail_mark_dirty(ctx);
       TRY(do_halo(ctx, k, l.z));
       if (dot) TRY(do_allred(ctx, k, dot));
     }
     return MSS_OK;
   }
-  if (z == l.z && n_half >= 2 && pair_ok(ctx, k)) {
+  if (pair_branch) {
     const int npairs = (n_half - (dot_last ? 1 : 0)) / 2;
     double* cur = l.z;
     double* oth = l.s;
+    if (z_zero && npairs > 0 && ((npairs + extra) & 1)) std::swap(cur, oth);
     // z-slab levels: the pairs read 1 ghost plane of r and 2 of z (SURVEY §8(e) C-H1 with
     // the halo of two half-sweeps exchanged at once)
     TRY(do_halo(ctx, k, const_cast<double*>(r), 1));
@@ -614,9 +631,15 @@ static int op_smooth(mss_ctx* ctx, int k, const double* r, double* z, int n_half
       std::swap(cur, oth);
       TRY(do_halo(ctx, k, cur, 2));
     }
+    if (last) {
+      if (2 * npairs != n_half) return set_err(MSS_EINVAL, "op_smooth: trailing half-sweeps with a caller pair");
+      *last = cur;
+      return MSS_OK;
+    }
     if (cur != l.z) {
       l.s = l.z;
       l.z = cur;
+      ctx->nswap++;
       tail_mark_dirty(ctx);
     }
     for (int h = 2 * npairs; h < n_half; ++h) {
@@ -782,6 +805,7 @@ static int read_scal(mss_ctx* ctx, int k) {
 
 // ============================================================================ recursion
 static int pcg_level(mss_ctx* ctx, int k);
+static int pcg_graph(mss_ctx* ctx, int k);
 
 // z_k = M_k^{-1} r_k  (Eq. 2.10 as the smoothing / coarse-correction sequence)
 // a5 + a6 of the pre-smoothing: 2m+1 half-sweeps from z = 0, then b_{k+1} = R (r - A z).
@@ -797,10 +821,15 @@ static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
     TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, true));
     return op_resid_restrict(ctx, k, l.r, l.z, c.r, sgs);
   }
-  TRY(op_smooth(ctx, k, l.r, l.z, nh - 1, 0, true));            // (nh-1)/2 pairs, z in l.z
-  TRY(op_pair(ctx, k, l.r, l.z, l.s, 0, false, true));          // closing red sweep + black residual
-  std::swap(l.z, l.s);
-  tail_mark_dirty(ctx);
+  double* cur = nullptr;
+  TRY(op_smooth(ctx, k, l.r, l.z, nh - 1, 0, true, nullptr, nullptr, 1, &cur));   // (nh-1)/2 pairs
+  double* dst = (cur == l.z) ? l.s : l.z;
+  TRY(op_pair(ctx, k, l.r, cur, dst, 0, false, true));          // closing red sweep + black residual
+  if (dst != l.z) {                                             // not reached when nh-1 pairs' parity works out
+    std::swap(l.z, l.s);
+    ctx->nswap++;
+    tail_mark_dirty(ctx);
+  }
   {
     ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.nx * l.ny * l.nz);
     const int kper = 16;
@@ -821,6 +850,22 @@ static bool fused_prolong_ok(mss_ctx* ctx, int k, int nh, int sgs) {
          (int64_t)(f.nx / 2) * f.ny * f.nz < ((int64_t)1 << 32) && pair_ok(ctx, k) && f.txp && pair_tma_on(ctx);
 }
 
+// a8 + a9: z += E y (y = the coarse x_{k+1}; black cells only under SGS, whose first red
+// sweep overwrites the red ones), then 2m+1 half-sweeps with rho = r.z fused into the last.
+static int prolong_postsmooth(mss_ctx* ctx, int k, int nh, int sgs) {
+  Level& l = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  if (fused_prolong_ok(ctx, k, nh, sgs)) {
+    // a8 inside the first post-smoothing pair: its red sweep is the only reader of the
+    // prolongated black values (the black sweep after it overwrites them)
+    const ProArgs pa{c.x, reinterpret_cast<const W1*>(l.w[0]), reinterpret_cast<const W1*>(l.w[1]),
+                     reinterpret_cast<const W1*>(l.w[2]), (int)c.nx, (int)c.ny};
+    return op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho, &pa);
+  }
+  TRY(op_prolong_add(ctx, k, c.x, l.z, sgs ? 1 : -1));           // z_black += (E y) (a8)
+  return op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho);  // post-smoothing (a9), rho = r.z
+}
+
 static int precond(mss_ctx* ctx, int k) {
   Level& l = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
@@ -829,26 +874,18 @@ static int precond(mss_ctx* ctx, int k) {
   TRY(presmooth_restrict(ctx, k, nh, sgs));                      // pre-smoothing (a5) + R (r - A z) (a6)
   if (k + 1 == ctx->L) {                                         // coarsest: exact (a7)
     TRY(op_coarse_solve(ctx, c.r, c.x));
-    ctx->info.iters[k + 1] += 1;
-    ctx->info.calls[k + 1] += 1;
+    if (!ctx->capturing) {                                       // graph mode: counted from level k's iterations
+      ctx->info.iters[k + 1] += 1;
+      ctx->info.calls[k + 1] += 1;
+    }
   } else if (c.N <= ctx->prm.tail_cells && tail_supported(ctx, k + 1)) {
     ProfScope ps(ctx, KC_TAIL, k + 1, 0.0);
     TRY(tail_pcg(ctx, k + 1));                                   // device-resident coarse levels
   } else {
     CK(cudaMemsetAsync(c.x, 0, sizeof(double) * c.N, ctx->stream));
-    TRY(pcg_level(ctx, k + 1));
+    TRY(ctx->capturing ? pcg_graph(ctx, k + 1) : pcg_level(ctx, k + 1));
   }
-  if (fused_prolong_ok(ctx, k, nh, sgs)) {
-    // a8 inside the first post-smoothing pair: its red sweep is the only reader of the
-    // prolongated black values (the black sweep after it overwrites them)
-    const ProArgs pa{c.x, reinterpret_cast<const W1*>(l.w[0]), reinterpret_cast<const W1*>(l.w[1]),
-                     reinterpret_cast<const W1*>(l.w[2]), (int)c.nx, (int)c.ny};
-    TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho, &pa));
-    return MSS_OK;
-  }
-  TRY(op_prolong_add(ctx, k, c.x, l.z, sgs ? 1 : -1));           // z_black += (E y) (a8)
-  TRY(op_smooth(ctx, k, l.r, l.z, nh, 0, false, &ctx->dscal[k].rho));  // post-smoothing (a9), rho = r.z
-  return MSS_OK;
+  return prolong_postsmooth(ctx, k, nh, sgs);
 }
 
 // ---- the paper's comparison methods, same kernels
@@ -888,6 +925,51 @@ static int apply_precond0(mss_ctx* ctx) {
   }
 }
 
+// a10: p_out = z + beta p_in (p_out = z when first; beta = rho / rho_prev from the level's
+// device scalars); q = A p_out; p.q -> the level's pq (allreduced on z-slab levels).  The
+// kernel choice is the solver's: TMA SpMV on padded levels, else the column walk, else the
+// generic kernel (the mss_cg_direction hook runs exactly this).
+static int op_direction_spmv(mss_ctx* ctx, int k, bool first, const double* z, const double* pin, double* pout,
+                             double* q) {
+  Level& l = ctx->lv[k];
+  Scal* ds = ctx->dscal + k;
+  {
+    ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV, k) * l.N);
+    dim3 cgrid;
+    int kch = 0;
+    if (k == 0 && ctx->kfaces && col_grid((const void*)k_spmv_col<4, true>, l, &cgrid, &kch)) {
+      k_spmv_col<4, true><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), z, pin, pout, q, ds, first ? 1 : 0,
+                                                                       kch, red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
+      ctx->launches++;
+    } else if (l.txp && spmv_tma_ok(ctx, l)) {
+      TRY(spmv_tma_launch(ctx, k, false, first, z, pin, pout, q, red_to(ctx, &ds->pq, k, 0)));
+    } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
+      k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), z, pin, pout, q, ds, first ? 1 : 0, kch,
+                                                                 red_to(ctx, &ds->pq, k, 0));
+      ctx->launches++;
+    } else
+      DISPATCH(ctx->ndim, k_pdir_spmv_dot, grid_for(l.N), l.dev(), z, pin, pout, q, ds, first ? 1 : 0,
+               red_to(ctx, &ds->pq, k, 0));
+  }
+  if (dist_level(ctx, k)) {
+    LAUNCH(k_p_ghost, grid_for(2 * l.plane), l.plane, l.nz, z, pin, pout, ds, first ? 1 : 0);
+    TRY(do_allred(ctx, k, &ds->pq));
+  }
+  return MSS_OK;
+}
+
+// a11: alpha = rho / pq; x += alpha p; r -= alpha q; ||r||^2 -> the level's rr (and
+// rho_prev = rho); allreduced on z-slab levels.  The mss_cg_update hook runs exactly this.
+static int op_update_norm(mss_ctx* ctx, int k, double* x, double* r, const double* p, const double* q) {
+  Level& l = ctx->lv[k];
+  Scal* ds = ctx->dscal + k;
+  {
+    ProfScope ps(ctx, KC_AXPY, k, cell_bytes(ctx, KC_AXPY) * l.N);
+    LAUNCH(k_axpy_norm, grid_for(l.N), l.N, x, r, p, q, ds, red_to(ctx, &ds->rr, k, 1));
+  }
+  return do_allred(ctx, k, &ds->rr);
+}
+
 // PCG on level k; on entry r_k holds the residual of the current x_k (x_k = 0 and
 // r_k = b_k for k > 0).  Level thresholds are precomputed in l.thr.
 static int pcg_level(mss_ctx* ctx, int k) {
@@ -902,35 +984,9 @@ static int pcg_level(mss_ctx* ctx, int k) {
     TRY(k == 0 ? apply_precond0(ctx) : precond(ctx, k));                 // z = M r, rho = r.z
     double* pin = l.p[l.pcur];
     double* pout = l.p[l.pcur ^ 1];
-    {
-    ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV, k) * l.N);
-    dim3 cgrid;
-    int kch = 0;
-    if (k == 0 && ctx->kfaces && col_grid((const void*)k_spmv_col<4, true>, l, &cgrid, &kch)) {
-      k_spmv_col<4, true><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds,
-                                                                       it == 0 ? 1 : 0, kch,
-                                                                       red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
-      ctx->launches++;
-    } else if (l.txp && spmv_tma_ok(ctx, l)) {
-      TRY(spmv_tma_launch(ctx, k, false, it == 0, l.z, pin, pout, l.q, red_to(ctx, &ds->pq, k, 0)));
-    } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
-      k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), l.z, pin, pout, l.q, ds, it == 0 ? 1 : 0,
-                                                                 kch, red_to(ctx, &ds->pq, k, 0));
-      ctx->launches++;
-    } else
-    DISPATCH(ctx->ndim, k_pdir_spmv_dot, grid_for(l.N), l.dev(), l.z, pin, pout, l.q, ds,
-             it == 0 ? 1 : 0, red_to(ctx, &ds->pq, k, 0));                 // a10
-    }
-    if (dist_level(ctx, k)) {
-      LAUNCH(k_p_ghost, grid_for(2 * l.plane), l.plane, l.nz, l.z, pin, pout, ds, it == 0 ? 1 : 0);
-      TRY(do_allred(ctx, k, &ds->pq));
-    }
+    TRY(op_direction_spmv(ctx, k, it == 0, l.z, pin, pout, l.q));            // a10
     l.pcur ^= 1;
-    {
-    ProfScope ps(ctx, KC_AXPY, k, cell_bytes(ctx, KC_AXPY) * l.N);
-    LAUNCH(k_axpy_norm, grid_for(l.N), l.N, l.x, l.r, pout, l.q, ds, red_to(ctx, &ds->rr, k, 1));  // a11
-    }
-    TRY(do_allred(ctx, k, &ds->rr));
+    TRY(op_update_norm(ctx, k, l.x, l.r, pout, l.q));                        // a11
     TRY(read_scal(ctx, k));                                                // a12
     const Scal& h = ctx->hscal[k];
     it++;
@@ -947,6 +1003,216 @@ static int pcg_level(mss_ctx* ctx, int k) {
     }
   }
   ctx->info.iters[k] += it;
+  return MSS_OK;
+}
+
+// ============================================================================ device-resident control (a12)
+// Graph mode: the level-0 PCG (and every nested host-driven level) is captured once into a
+// CUDA graph.  Each level's loop is
+//     dot(r, r); enter -> h0;  IF(h0) { it; check -> hw;
+//                                       WHILE(hw) { it; check -> hw, hi;  IF(hi) { it; check -> hw } } }
+// so the iterations alternate the direction buffers p0 / p1 exactly as the host loop does
+// (the first iteration, p = z, is peeled).  The stop test, the counters and the breakdown
+// guard run on the device (control.cuh); the host reads them once per solve.  The capture
+// runs the host code path unchanged on a private stream per nesting depth
+// (cudaStreamBeginCaptureToGraph into each conditional body).
+static LevelCtl* dctl(mss_ctx* ctx, int k) { return reinterpret_cast<LevelCtl*>(ctx->dctl) + k; }
+
+static int cap_stream(mss_ctx* ctx, int depth, cudaStream_t* out) {
+  while ((int)ctx->cap_streams.size() <= depth) {
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    ctx->cap_streams.push_back(st);
+  }
+  *out = ctx->cap_streams[depth];
+  return MSS_OK;
+}
+
+// Add a conditional node (type, handle) at the current capture position of ctx->stream and
+// capture body() into its body graph on the next depth's stream.
+template <class F>
+static int cap_cond(mss_ctx* ctx, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type, F&& body) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, &g, &deps, &nd));
+  if (st != cudaStreamCaptureStatusActive) return set_err(MSS_ECUDA, "cap_cond: stream not capturing");
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = type;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+  cudaGraph_t bg = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(ctx->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaStream_t outer = ctx->stream, inner;
+  TRY(cap_stream(ctx, ++ctx->cap_depth, &inner));
+  CK(cudaStreamBeginCaptureToGraph(inner, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  ctx->stream = inner;
+  int rc = body();
+  cudaGraph_t done = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(inner, &done);
+  ctx->stream = outer;
+  ctx->cap_depth--;
+  if (rc < 0) return rc;
+  if (e != cudaSuccess) return set_err(MSS_ECUDA, std::string("cap_cond: ") + cudaGetErrorString(e));
+  return MSS_OK;
+}
+
+// one PCG iteration of level k (z = M r; a10; a11), the host loop's body
+static int pcg_iteration(mss_ctx* ctx, int k, bool first) {
+  Level& l = ctx->lv[k];
+  TRY(k == 0 ? apply_precond0(ctx) : precond(ctx, k));
+  double* pin = l.p[l.pcur];
+  double* pout = l.p[l.pcur ^ 1];
+  TRY(op_direction_spmv(ctx, k, first, l.z, pin, pout, l.q));
+  l.pcur ^= 1;
+  return op_update_norm(ctx, k, l.x, l.r, pout, l.q);
+}
+
+static int pcg_graph(mss_ctx* ctx, int k) {
+  Level& l = ctx->lv[k];
+  Scal* ds = ctx->dscal + k;
+  LevelCtl* c = dctl(ctx, k);
+  int* flags = ctx->tail_flags;
+  cudaGraphConditionalHandle h0, hw, hi;
+  CK(cudaGraphConditionalHandleCreate(&h0, ctx->cap_top, 0, 0));
+  CK(cudaGraphConditionalHandleCreate(&hw, ctx->cap_top, 0, 0));
+  CK(cudaGraphConditionalHandleCreate(&hi, ctx->cap_top, 0, 0));
+  const int64_t la = ctx->launches, nested0 = ctx->g_nested_launches;
+  TRY(op_dot(ctx, k, l.N, l.r, l.r, &ds->rr));
+  k_pcg_enter<<<1, 1, 0, ctx->stream>>>(c, ds, flags, h0);
+  ctx->launches++;
+  ctx->g_per_call[k] = ctx->launches - la;
+  const long long mi = ctx->prm.max_iter;
+  const int rc = cap_cond(ctx, h0, cudaGraphCondTypeIf, [&]() -> int {
+    TRY(pcg_iteration(ctx, k, true));
+    k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hw, 1);
+    ctx->launches++;
+    return cap_cond(ctx, hw, cudaGraphCondTypeWhile, [&]() -> int {
+      const int64_t lb = ctx->launches;
+      const int64_t nb = ctx->g_nested_launches;
+      TRY(pcg_iteration(ctx, k, false));
+      k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hi, 2);
+      ctx->launches++;
+      // launches of one iteration of this level alone (nested host-driven levels count their own)
+      ctx->g_per_iter[k] = (ctx->launches - lb) - (ctx->g_nested_launches - nb);
+      return cap_cond(ctx, hi, cudaGraphCondTypeIf, [&]() -> int {
+        TRY(pcg_iteration(ctx, k, false));
+        k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hw, 1);
+        ctx->launches++;
+        return MSS_OK;
+      });
+    });
+  });
+  // what this call captured, nested levels included, for the caller's per-iteration count
+  ctx->g_nested_launches = nested0 + (ctx->launches - la);
+  return rc;
+}
+
+static bool graph_eligible(const mss_ctx* ctx) {
+  if (ctx->graph_knob == 0 || ctx->graph_failed || ctx->prof_on || ctx->L < 1) return false;
+  if (ctx->prm.method != 0 || ctx->prm.splitting != 0) return false;
+  if (ctx->loop_group) return false;                                    // host-barrier transport
+  if (ctx->comm && ctx->comm->size > 1 && ctx->graph_knob < 2) return false;
+  return true;
+}
+
+// Capture pcg_level(0)'s graph equivalent; on failure graph mode is switched off for the
+// context (the host-driven loop is the fallback and computes the same bits).
+static int graph_capture(mss_ctx* ctx) {
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  if (ctx->graph) {
+    cudaGraphDestroy(ctx->graph);
+    ctx->graph = nullptr;
+  }
+  if (!ctx->dctl) TRY(dalloc(ctx, &ctx->dctl, sizeof(LevelCtl) * MSS_MAX_LEVELS));
+  if (!ctx->tail_flags) return set_err(MSS_ECUDA, "graph mode needs the control flags");
+  cudaGraph_t top;
+  CK(cudaGraphCreate(&top, 0));
+  cudaStream_t st;
+  TRY(cap_stream(ctx, 0, &st));
+  cudaStream_t saved = ctx->stream;
+  const int64_t launches0 = ctx->launches, nswap0 = ctx->nswap;
+  const int pcur0 = ctx->lv[0].pcur;
+  std::vector<int> pcur(ctx->L + 1);
+  for (int k = 0; k <= ctx->L; ++k) pcur[k] = ctx->lv[k].pcur;
+  ctx->cap_top = top;
+  ctx->cap_depth = 0;
+  ctx->g_nested_launches = 0;
+  int rc = MSS_OK;
+  cudaError_t e = cudaStreamBeginCaptureToGraph(st, top, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  if (e == cudaSuccess) {
+    ctx->stream = st;
+    ctx->capturing = true;
+    rc = pcg_graph(ctx, 0);
+    ctx->capturing = false;
+    ctx->stream = saved;
+    cudaGraph_t out = nullptr;
+    e = cudaStreamEndCapture(st, &out);
+  }
+  ctx->launches = launches0;
+  for (int k = 0; k <= ctx->L; ++k) ctx->lv[k].pcur = pcur[k];
+  (void)pcur0;
+  if (rc == MSS_OK && e == cudaSuccess && ctx->nswap == nswap0) e = cudaGraphInstantiate(&ctx->gexec, top, 0);
+  if (rc != MSS_OK || e != cudaSuccess || ctx->nswap != nswap0 || !ctx->gexec) {
+    if (getenv("MSS_DEBUG"))
+      fprintf(stderr, "[mss] graph capture failed (rc %d, %s, swaps %lld): host-driven loop\n", rc,
+              cudaGetErrorString(e), (long long)(ctx->nswap - nswap0));
+    cudaGetLastError();
+    cudaGraphDestroy(top);
+    ctx->graph_failed = true;
+    return MSS_OK;
+  }
+  ctx->graph = top;
+  ctx->graph_gen = ctx->nswap;
+  ctx->g_tail_level = ctx->info.tail_level;
+  ctx->g_tail_kind = ctx->info.tail_kind;
+  ctx->info.tail_level = -1;
+  ctx->info.tail_kind = 0;
+  return MSS_OK;
+}
+
+// The level-0 PCG in graph mode: per-solve values (thresholds, counters) are written to the
+// device, the graph runs, and the counters come back in one read.
+static int pcg_level0_graph(mss_ctx* ctx) {
+  // tail arguments (per-solve thresholds) before capture / launch: no copy inside the graph
+  for (int k = 1; k < ctx->L; ++k)
+    if (ctx->lv[k].N <= ctx->prm.tail_cells && tail_supported(ctx, k)) {
+      TRY(tail_prepare(ctx, k));
+      break;
+    }
+  if (!ctx->gexec || ctx->graph_gen != ctx->nswap) TRY(graph_capture(ctx));
+  if (!ctx->gexec) return pcg_level(ctx, 0);
+  LevelCtl h[MSS_MAX_LEVELS];
+  memset(h, 0, sizeof(h));
+  for (int k = 0; k <= ctx->L; ++k) h[k].thr = ctx->lv[k].thr;
+  CK(cudaMemcpyAsync(ctx->dctl, h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+  CK(cudaMemcpyAsync(h, ctx->dctl, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < ctx->L; ++k) {
+    if (h[k].calls == 0) continue;                      // tail levels count themselves
+    ctx->info.calls[k] += h[k].calls;
+    ctx->info.iters[k] += h[k].iters;
+    ctx->launches += h[k].calls * ctx->g_per_call[k] + h[k].iters * ctx->g_per_iter[k];
+  }
+  // the coarsest exact solve runs once per iteration of the level above it when that level
+  // is host-driven (inside the tail it is counted by the tail)
+  if (h[ctx->L - 1].calls) {
+    ctx->info.iters[ctx->L] += h[ctx->L - 1].iters;
+    ctx->info.calls[ctx->L] += h[ctx->L - 1].iters;
+  }
+  if (h[0].iters > 0 && ctx->g_tail_level >= 0) {
+    ctx->info.tail_level = ctx->g_tail_level;
+    ctx->info.tail_kind = ctx->g_tail_kind;
+  }
+  ctx->info.graph = 1;
   return MSS_OK;
 }
 
@@ -969,6 +1235,7 @@ static void reset_info(mss_ctx* ctx) {
   I.bnorm2 = 0;
   I.tail_level = -1;
   I.tail_kind = 0;
+  I.graph = 0;
 }
 
 static BCDev bc_dev(const mss_ctx* ctx) {
@@ -1048,7 +1315,7 @@ static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) 
       }
       ctx->info.iters[0] += it;
     } else {
-      rc = pcg_level(ctx, 0);
+      rc = graph_eligible(ctx) ? pcg_level0_graph(ctx) : pcg_level(ctx, 0);   // a12 on the device / host
       if (rc < 0 && rc != MSS_EBREAKDOWN) return rc;
     }
   }
@@ -1203,6 +1470,9 @@ static int free_ctx(mss_ctx* ctx) {
     if (ctx->ev_in[b]) cudaEventDestroy(ctx->ev_in[b]);
     if (ctx->ev_done[b]) cudaEventDestroy(ctx->ev_done[b]);
   }
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  for (cudaStream_t st : ctx->cap_streams) cudaStreamDestroy(st);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->hscal) cudaFreeHost(ctx->hscal);
   if (ctx->comm) {
@@ -1433,20 +1703,35 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   CK(cudaMalloc((void**)&X, sizeof(double) * nn));
   CK(cudaMemsetAsync(ctx->Achol, 0, sizeof(double) * nn, ctx->stream));
   DISPATCH(ndim, k_dense_assemble, grid_for(lc.N), lc.dev(), ctx->Achol);
-  LAUNCH(k_cholesky, 1, ctx->Achol, ctx->NL, ctx->dflag + 1);
-  CK(cudaMemcpyAsync(&hflag, ctx->dflag + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (hflag) {
-    cudaFree(X);
-    return set_err(MSS_ESINGULAR, "coarsest operator is not SPD");
-  }
   {
-    const int tb = 128;
-    k_chol_inverse<<<(ctx->NL + tb - 1) / tb, tb, 0, ctx->stream>>>(ctx->Achol, X, ctx->NL);
-    ctx->launches++;
+    // blocked Cholesky, L^{-1} and A^{-1} = L^{-T} L^{-1} (dense.cuh)
+    const auto td0 = std::chrono::steady_clock::now();
+    const int n = ctx->NL, nb = (n + kDB - 1) / kDB;
+    const dim3 tile(kDB, kDB);
+    for (int jb = 0; jb < nb; ++jb) {
+      k_potrf_diag<<<1, tile, 0, ctx->stream>>>(ctx->Achol, n, jb, ctx->dflag + 1);
+      const int T = nb - jb - 1;
+      if (T > 0) {
+        k_trsm_panel<<<T, tile, 0, ctx->stream>>>(ctx->Achol, n, jb, ctx->dflag + 1);
+        k_syrk_tiles<<<T * (T + 1) / 2, 256, 0, ctx->stream>>>(ctx->Achol, n, jb, ctx->dflag + 1);
+      }
+      ctx->launches += T > 0 ? 3 : 1;
+    }
+    CK(cudaMemcpyAsync(&hflag, ctx->dflag + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (hflag) {
+      cudaFree(X);
+      return set_err(MSS_ESINGULAR, "coarsest operator is not SPD");
+    }
+    k_trtri_diag<<<nb, tile, 0, ctx->stream>>>(ctx->Achol, X, n);
+    for (int sd = 1; sd < nb; ++sd) k_trtri_offdiag<<<nb - sd, 256, 0, ctx->stream>>>(ctx->Achol, X, n, sd);
+    k_gram_lower<<<nb * (nb + 1) / 2, 256, 0, ctx->stream>>>(X, ctx->Ainv, n);
+    ctx->launches += nb + 1;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    ctx->info.setup_coarsest_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
   }
-  LAUNCH(k_symmetrize, grid_for((int64_t)nn), X, ctx->Ainv, ctx->NL);
-  CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(X);
   compute_lift(ctx);
   // padded Tx copies for the TMA pair kernel on every single-GPU column-walk level
@@ -1575,11 +1860,13 @@ static int setup_common(mss_ctx** out, mss::Comm* comm, int ndim, const int64_t 
       return set_err(MSS_ENOMEM, "comm buffer");
     }
   }
+  const auto t0 = std::chrono::steady_clock::now();
   int rc = setup_impl(ctx, n, K, k_comp, depth);
   if (rc != MSS_OK) {
     free_ctx(ctx);
     return rc;
   }
+  ctx->info.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   ctx->info.levels = ctx->L + 1;
   for (int k = 0; k <= ctx->L; ++k) {
     ctx->info.dims[k][0] = ctx->lv[k].nx;
@@ -1669,6 +1956,12 @@ int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, do
   double* df[2] = {ctx->dev_f, ctx->dev_f1};
   double* dx[2] = {ctx->dev_x, ctx->dev_x1};
   cudaStream_t cs = ctx->copy_stream;
+  // every exit path (including the early error returns of CK / TRY) drains the copy stream
+  // before returning, so no copy still reads or writes the caller's host buffers afterwards
+  struct DrainCopies {
+    cudaStream_t s;
+    ~DrainCopies() { cudaStreamSynchronize(s); }
+  } drain{cs};
   const int L1 = ctx->L + 1;
   auto upload = [&](int i) -> int {
     const int b = i & 1;
@@ -1687,10 +1980,7 @@ int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, do
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[b], 0));
     const int rc = mss_solve(ctx, df[b], dx[b], rel_tol, iters ? iters + (int64_t)i * L1 : nullptr,
                              true_rel_res ? true_rel_res + i : nullptr);
-    if (rc < 0) {
-      cudaStreamSynchronize(cs);
-      return rc;
-    }
+    if (rc < 0) return rc;
     if (rc > worst) worst = rc;
     CK(cudaEventRecord(ctx->ev_done[b], ctx->stream));
     CK(cudaStreamWaitEvent(cs, ctx->ev_done[b], 0));
@@ -1850,6 +2140,111 @@ int mss_rhs_lift(mss_ctx* ctx, const double* f, double* b, double* x0) {
   Level& l = ctx->lv[0];
   DISPATCH(ctx->ndim, k_rhs_lift, grid_for(l.N), l.dev(), f, b, x0, cell_volume(ctx), bc_dev(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+// ---- production-path hooks: each runs exactly the dispatch the solver uses on that level
+// (TMA / column-walk / generic, fused or not, as selected at setup), on the level's own
+// ghosted buffers, so the parity tests check the kernels bench.py times.
+static int put_scal(mss_ctx* ctx, int k, double rho, double rho_prev, double pq) {
+  Scal& h = ctx->hscal[k];
+  h.rho = rho;
+  h.rho_prev = rho_prev;
+  h.pq = pq;
+  CK(cudaMemcpyAsync(ctx->dscal + k, &h, 3 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));   // the pinned mirror is rewritten by later reads
+  return MSS_OK;
+}
+
+static int to_level(mss_ctx* ctx, double* dst, const double* src, int64_t n) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  return MSS_OK;
+}
+
+int mss_cg_direction(mss_ctx* ctx, int level, const double* z, const double* p_in, double rho, double rho_prev,
+                     int first, double* p_out, double* q, double* pq) {
+  TRY(check_level(ctx, level));
+  if (!z || !p_out || !q || !pq || (!first && !p_in)) return set_err(MSS_EINVAL, "mss_cg_direction: null argument");
+  Level& l = ctx->lv[level];
+  TRY(put_scal(ctx, level, rho, rho_prev, 0.0));
+  double* pin = l.p[l.pcur];
+  double* pout = l.p[l.pcur ^ 1];
+  TRY(to_level(ctx, l.z, z, l.N));
+  if (!first) TRY(to_level(ctx, pin, p_in, l.N));
+  TRY(do_halo(ctx, level, l.z));
+  if (!first) TRY(do_halo(ctx, level, pin));
+  TRY(op_direction_spmv(ctx, level, first != 0, l.z, pin, pout, l.q));
+  TRY(to_level(ctx, p_out, pout, l.N));
+  TRY(to_level(ctx, q, l.q, l.N));
+  TRY(read_scal(ctx, level));
+  *pq = ctx->hscal[level].pq;
+  return MSS_OK;
+}
+
+int mss_cg_update(mss_ctx* ctx, int level, double* x, double* r, const double* p, const double* q, double rho,
+                  double pq, double* rr) {
+  TRY(check_level(ctx, level));
+  if (!x || !r || !p || !q || !rr) return set_err(MSS_EINVAL, "mss_cg_update: null argument");
+  Level& l = ctx->lv[level];
+  TRY(put_scal(ctx, level, rho, 0.0, pq));
+  double* pb = l.p[l.pcur];
+  TRY(to_level(ctx, l.x, x, l.N));
+  TRY(to_level(ctx, l.r, r, l.N));
+  TRY(to_level(ctx, pb, p, l.N));
+  TRY(to_level(ctx, l.q, q, l.N));
+  TRY(op_update_norm(ctx, level, l.x, l.r, pb, l.q));
+  TRY(to_level(ctx, x, l.x, l.N));
+  TRY(to_level(ctx, r, l.r, l.N));
+  TRY(read_scal(ctx, level));
+  *rr = ctx->hscal[level].rr;
+  return MSS_OK;
+}
+
+int mss_residual(mss_ctx* ctx, int level, const double* b, const double* x, double* r, double* rr) {
+  TRY(check_level(ctx, level));
+  if (!b || !x || !r) return set_err(MSS_EINVAL, "mss_residual: null argument");
+  Level& l = ctx->lv[level];
+  // b in the level's q buffer (on coarse levels the level's b aliases r), x in x (ghosted)
+  TRY(to_level(ctx, l.q, b, l.N));
+  TRY(to_level(ctx, l.x, x, l.N));
+  TRY(do_halo(ctx, level, l.x));
+  TRY(op_residual(ctx, level, l.q, l.x, l.s, &ctx->dscal[level].aux));
+  TRY(to_level(ctx, r, l.s, l.N));
+  TRY(read_scal(ctx, level));
+  if (rr) *rr = ctx->hscal[level].aux;
+  return MSS_OK;
+}
+
+int mss_presmooth_restrict(mss_ctx* ctx, int level, const double* r, double* z, double* coarse_b) {
+  TRY(check_level(ctx, level));
+  if (level >= ctx->L) return set_err(MSS_EINVAL, "no coarser level");
+  if (!r || !z || !coarse_b) return set_err(MSS_EINVAL, "mss_presmooth_restrict: null argument");
+  Level& l = ctx->lv[level];
+  Level& c = ctx->lv[level + 1];
+  TRY(to_level(ctx, l.r, r, l.N));
+  TRY(presmooth_restrict(ctx, level, 2 * ctx->prm.m + 1, ctx->prm.splitting == 0));
+  TRY(to_level(ctx, z, l.z, l.N));
+  TRY(to_level(ctx, coarse_b, c.r, c.N));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MSS_OK;
+}
+
+int mss_prolong_postsmooth(mss_ctx* ctx, int level, const double* coarse_y, const double* r, double* z,
+                           double* rho) {
+  TRY(check_level(ctx, level));
+  if (level >= ctx->L) return set_err(MSS_EINVAL, "no coarser level");
+  if (!coarse_y || !r || !z) return set_err(MSS_EINVAL, "mss_prolong_postsmooth: null argument");
+  Level& l = ctx->lv[level];
+  Level& c = ctx->lv[level + 1];
+  TRY(to_level(ctx, c.x, coarse_y, c.N));
+  TRY(to_level(ctx, l.r, r, l.N));
+  TRY(to_level(ctx, l.z, z, l.N));
+  TRY(do_halo(ctx, level, l.r));
+  TRY(do_halo(ctx, level, l.z));
+  TRY(prolong_postsmooth(ctx, level, 2 * ctx->prm.m + 1, ctx->prm.splitting == 0));
+  TRY(to_level(ctx, z, l.z, l.N));
+  TRY(read_scal(ctx, level));
+  if (rho) *rho = ctx->hscal[level].rho;
   return MSS_OK;
 }
 

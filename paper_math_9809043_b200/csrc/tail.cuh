@@ -253,8 +253,27 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const TailArgs* __rest
 }  // namespace mss
 
 // ============================================================================ host side
+#define TRY_TAIL(expr)            \
+  do {                            \
+    int _rc = (expr);             \
+    if (_rc < 0) return _rc;      \
+  } while (0)
+
 static int tail_setup(mss_ctx* ctx) {
   ctx->tail_cs = 0;
+  {
+    // device counters and flags (not-converged, breakdown level + 1): written by the tails
+    // and by the graph-mode control kernels (control.cuh), collected by tail_collect
+    void* p = nullptr;
+    if (cudaMalloc(&p, sizeof(long long) * 2 * MSS_MAX_LEVELS) != cudaSuccess) return MSS_ENOMEM;
+    ctx->allocs.push_back(p);
+    ctx->tail_cnt = (long long*)p;
+    if (cudaMalloc(&p, sizeof(int) * 2) != cudaSuccess) return MSS_ENOMEM;
+    ctx->allocs.push_back(p);
+    ctx->tail_flags = (int*)p;
+    cudaMemsetAsync(ctx->tail_cnt, 0, sizeof(long long) * 2 * MSS_MAX_LEVELS, ctx->stream);
+    cudaMemsetAsync(ctx->tail_flags, 0, sizeof(int) * 2, ctx->stream);
+  }
   if (ctx->prm.tail_cells <= 0) return MSS_OK;
   auto kern = (ctx->ndim == 3) ? (void*)mss::k_tail<3> : (void*)mss::k_tail<2>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -282,14 +301,6 @@ static int tail_setup(mss_ctx* ctx) {
   if (cudaMalloc(&p, sizeof(mss::TailArgs)) != cudaSuccess) return MSS_ENOMEM;
   ctx->allocs.push_back(p);
   ctx->tail_d = p;
-  if (cudaMalloc(&p, sizeof(long long) * 2 * MSS_MAX_LEVELS) != cudaSuccess) return MSS_ENOMEM;
-  ctx->allocs.push_back(p);
-  ctx->tail_cnt = (long long*)p;
-  if (cudaMalloc(&p, sizeof(int) * 2) != cudaSuccess) return MSS_ENOMEM;
-  ctx->allocs.push_back(p);
-  ctx->tail_flags = (int*)p;
-  cudaMemsetAsync(ctx->tail_cnt, 0, sizeof(long long) * 2 * MSS_MAX_LEVELS, ctx->stream);
-  cudaMemsetAsync(ctx->tail_flags, 0, sizeof(int) * 2, ctx->stream);
   ctx->tail_h.assign(sizeof(mss::TailArgs), 0);
   ctx->tail_dirty = true;
   tailsm_setup(ctx);
@@ -313,10 +324,12 @@ static void tail_mark_dirty(mss_ctx* ctx) {
   ctx->tsm_dirty = true;
 }
 
-static int tail_pcg(mss_ctx* ctx, int k) {
-  ctx->info.tail_level = k;
-  ctx->info.tail_kind = (k == ctx->tsm_L0) ? 2 : 1;
-  if (k == ctx->tsm_L0) return tailsm_launch(ctx, k);
+static int tailsm_upload(mss_ctx* ctx, int k);
+// Upload the tail's argument block (pointers, per-solve thresholds) if it changed; the tail
+// kernels read it from device memory, so a captured graph picks up new thresholds without
+// re-capture.  Synchronises the stream when it copies (never called while capturing).
+static int tail_prepare(mss_ctx* ctx, int k) {
+  if (k == ctx->tsm_L0) return tailsm_upload(ctx, k);
   if (ctx->tail_dirty) {
     mss::TailArgs& a = *reinterpret_cast<mss::TailArgs*>(ctx->tail_h.data());
     a.k0 = 0;
@@ -350,6 +363,17 @@ static int tail_pcg(mss_ctx* ctx, int k) {
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return MSS_ECUDA;
     ctx->tail_dirty = false;
   }
+  return MSS_OK;
+}
+
+static int tail_pcg(mss_ctx* ctx, int k) {
+  ctx->info.tail_level = k;
+  ctx->info.tail_kind = (k == ctx->tsm_L0) ? 2 : 1;
+  if (k == ctx->tsm_L0) return tailsm_launch(ctx, k);
+  if (ctx->tail_dirty) {
+    if (ctx->capturing) return set_err(MSS_ECUDA, "tail arguments changed during graph capture");
+    TRY_TAIL(tail_prepare(ctx, k));
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctx->tail_cs);
   cfg.blockDim = dim3(mss::kTailThreads);
@@ -370,7 +394,7 @@ static int tail_pcg(mss_ctx* ctx, int k) {
 
 // Add the device-side counters of the tail into ctx->info and reset them.
 static int tail_collect(mss_ctx* ctx) {
-  if (!ctx->tail_cs) return MSS_OK;
+  if (!ctx->tail_flags) return MSS_OK;
   long long c[2 * MSS_MAX_LEVELS];
   int fl[2];
   if (cudaMemcpyAsync(c, ctx->tail_cnt, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess) return MSS_ECUDA;

@@ -643,11 +643,15 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
 // The dynamic shared-memory limit is a per-kernel, process-wide attribute: contexts of
 // different sizes in one process (or concurrent loopback ranks) must only ever raise it,
 // else a smaller context's setup breaks a larger one's launches.
+// The attribute is per device: the cache is keyed by (device, kernel), so a context set up
+// on another GPU of the same process raises its own device's limit.
 static bool tailsm_raise_smem(const void* kern, size_t shm) {
   static std::mutex mu;
-  static std::map<const void*, size_t> cur;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
   std::lock_guard<std::mutex> lk(mu);
-  size_t& c = cur[kern];
+  size_t& c = cur[{dev, kern}];
   if (shm <= c) return true;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm) != cudaSuccess) return false;
   c = shm;
@@ -807,7 +811,7 @@ static void tailsm_report(mss_ctx* ctx) {
     fprintf(stderr, "[mss] tail phase %-10s %14lld cycles %5.1f%%\n", nm[i], h[i], tot ? 100.0 * h[i] / tot : 0.0);
 }
 
-static int tailsm_launch(mss_ctx* ctx, int k) {
+static int tailsm_upload(mss_ctx* ctx, int k) {
   mss::TsArgs& a = *reinterpret_cast<mss::TsArgs*>(ctx->tsm_h.data());
   if (ctx->tsm_dirty) {
     for (int q = a.L0; q <= a.L; ++q) a.lv[q - a.L0].thr = ctx->lv[q].thr;
@@ -819,6 +823,16 @@ static int tailsm_launch(mss_ctx* ctx, int k) {
     if (cudaMemcpyAsync(ctx->tsm_d, &a, sizeof(a), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) return MSS_ECUDA;
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return MSS_ECUDA;
     ctx->tsm_dirty = false;
+  }
+  return MSS_OK;
+}
+
+static int tailsm_launch(mss_ctx* ctx, int k) {
+  mss::TsArgs& a = *reinterpret_cast<mss::TsArgs*>(ctx->tsm_h.data());
+  if (ctx->tsm_dirty) {
+    if (ctx->capturing) return set_err(MSS_ECUDA, "tail arguments changed during graph capture");
+    const int rc = tailsm_upload(ctx, k);
+    if (rc < 0) return rc;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctx->tsm_cs);

@@ -68,6 +68,9 @@ class Info(ctypes.Structure):
         ("kernel_launches", ctypes.c_int64),
         ("tail_level", ctypes.c_int),
         ("tail_kind", ctypes.c_int),
+        ("setup_ms", ctypes.c_double),
+        ("setup_coarsest_ms", ctypes.c_double),
+        ("graph", ctypes.c_int),
     ]
 
 
@@ -106,6 +109,12 @@ SIGNATURES = [
     ("mss_precond", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_double, I64P]),
     ("mss_coarse_solve", ctypes.c_int, [P, P, P]),
     ("mss_rhs_lift", ctypes.c_int, [P, P, P, P]),
+    ("mss_cg_direction", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_int, P, P,
+                                        DP]),
+    ("mss_cg_update", ctypes.c_int, [P, ctypes.c_int, P, P, P, P, ctypes.c_double, ctypes.c_double, DP]),
+    ("mss_residual", ctypes.c_int, [P, ctypes.c_int, P, P, P, DP]),
+    ("mss_presmooth_restrict", ctypes.c_int, [P, ctypes.c_int, P, P, P]),
+    ("mss_prolong_postsmooth", ctypes.c_int, [P, ctypes.c_int, P, P, P, DP]),
     ("mss_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
     ("mss_slab_range", ctypes.c_int, [I64P, ctypes.c_int, ctypes.POINTER(Params), ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, I64P, I64P]),
@@ -248,6 +257,9 @@ class SolveReport:
     kernel_launches: int
     tail_level: int = -1
     tail_kind: int = 0
+    setup_ms: float = 0.0
+    setup_coarsest_ms: float = 0.0
+    graph: bool = False
 
 
 class Solver:
@@ -335,7 +347,8 @@ class Solver:
         L1 = inf.levels
         return SolveReport(0, list(inf.iters[:L1]), list(inf.calls[:L1]),
                            [tuple(inf.dims[k]) for k in range(L1)], bool(inf.not_converged),
-                           inf.true_rel_res, inf.kernel_launches, inf.tail_level, inf.tail_kind)
+                           inf.true_rel_res, inf.kernel_launches, inf.tail_level, inf.tail_kind,
+                           inf.setup_ms, inf.setup_coarsest_ms, bool(inf.graph))
 
     def manufacture_rhs(self, x_exact: torch.Tensor) -> torch.Tensor:
         """f' with discrete solution x_exact (mss_manufacture_rhs)."""
@@ -469,3 +482,53 @@ class Solver:
         x0 = torch.empty_like(f)
         _check(self.lib.mss_rhs_lift(self.ctx, _dev_ptr(f, self.N), b.data_ptr(), x0.data_ptr()), "mss_rhs_lift")
         return b, x0
+
+    # ---------------------------------------------------------------- production-path hooks
+    def cg_direction(self, level: int, z: torch.Tensor, p_in: Optional[torch.Tensor], rho: float, rho_prev: float,
+                     first: bool):
+        """(p_out, q, p_out.q) by the solver's own a10 kernel (mss_cg_direction)."""
+        n = self.level_N(level)
+        p_out = torch.empty_like(z)
+        q = torch.empty_like(z)
+        pq = ctypes.c_double()
+        _check(self.lib.mss_cg_direction(self.ctx, level, _dev_ptr(z, n), None if p_in is None else _dev_ptr(p_in, n),
+                                         float(rho), float(rho_prev), 1 if first else 0, p_out.data_ptr(),
+                                         q.data_ptr(), ctypes.byref(pq)), "mss_cg_direction")
+        return p_out, q, pq.value
+
+    def cg_update(self, level: int, x: torch.Tensor, r: torch.Tensor, p: torch.Tensor, q: torch.Tensor, rho: float,
+                  pq: float):
+        """(x + alpha p, r - alpha q, ||r||^2) by the solver's own a11 kernel (mss_cg_update)."""
+        n = self.level_N(level)
+        xx, rr_ = x.clone(), r.clone()
+        out = ctypes.c_double()
+        _check(self.lib.mss_cg_update(self.ctx, level, _dev_ptr(xx, n), _dev_ptr(rr_, n), _dev_ptr(p, n),
+                                      _dev_ptr(q, n), float(rho), float(pq), ctypes.byref(out)), "mss_cg_update")
+        return xx, rr_, out.value
+
+    def residual(self, level: int, b: torch.Tensor, x: torch.Tensor):
+        """(b - A x, ||b - A x||^2) by the solver's residual kernel (mss_residual)."""
+        n = self.level_N(level)
+        r = torch.empty_like(b)
+        out = ctypes.c_double()
+        _check(self.lib.mss_residual(self.ctx, level, _dev_ptr(b, n), _dev_ptr(x, n), r.data_ptr(),
+                                     ctypes.byref(out)), "mss_residual")
+        return r, out.value
+
+    def presmooth_restrict(self, level: int, r: torch.Tensor):
+        """(z, R (r - A z)) with z = 2m+1 half-sweeps from zero (mss_presmooth_restrict)."""
+        n = self.level_N(level)
+        z = torch.empty_like(r)
+        cb = torch.empty(self.level_N(level + 1), dtype=torch.float64, device=r.device)
+        _check(self.lib.mss_presmooth_restrict(self.ctx, level, _dev_ptr(r, n), z.data_ptr(), cb.data_ptr()),
+               "mss_presmooth_restrict")
+        return z, cb
+
+    def prolong_postsmooth(self, level: int, y: torch.Tensor, r: torch.Tensor, z: torch.Tensor):
+        """(z', r.z') with z' = 2m+1 half-sweeps on z + E y (mss_prolong_postsmooth)."""
+        n = self.level_N(level)
+        zz = z.clone()
+        rho = ctypes.c_double()
+        _check(self.lib.mss_prolong_postsmooth(self.ctx, level, _dev_ptr(y, self.level_N(level + 1)), _dev_ptr(r, n),
+                                               _dev_ptr(zz, n), ctypes.byref(rho)), "mss_prolong_postsmooth")
+        return zz, rho.value

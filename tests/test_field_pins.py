@@ -83,6 +83,28 @@ def test_P13_circulant_embedding_reproduces_gaussian_covariance(ndim, n, ell, th
         assert abs(ac - _cov_formula(0, lag, Lam)) < dropped + 1e-12
 
 
+@pytest.mark.parametrize("ndim,n,ell,theta", [(2, (40, 36, 1), (1.5, 1.0), 0.3),
+                                               (3, (20, 18, 16), (1.2, 1.0, 0.9), 0.5)])
+def test_P13_gaussian_embedding_exact_when_nothing_is_clipped(ndim, n, ell, theta):
+    """The F3 floor pinned on its own terms: where every mode of the Gaussian spectrum is
+    above 1e-8 S_0 (short correlation lengths), the floor drops nothing and the realised
+    covariance of the impulse response equals the covariance formula C(r) = exp(-r^T Lambda
+    r) lag by lag to rounding -- the pre-floor 1e-12 pin, with no allowance for dropped mass.
+    Where the floor does drop modes (test above), the allowance is the dropped mass itself,
+    bounded there by 1e-7 (far below any tolerance the solves use)."""
+    shape = O.shape_of(ndim, n)
+    S = np.fft.fftn(F.periodic_covariance(ndim, n, 0, ell, theta)).real
+    assert S.min() > 1e-6 * S.flat[0]
+    assert np.array_equal(F.clip_spectrum(S), S)
+    delta = np.zeros(shape)
+    delta[(0,) * ndim] = 1.0
+    h = F.gaussian_field(ndim, n, 0, ell, theta, seed=0, noise=delta)
+    Lam = F.lambda_matrix(ndim, ell, theta).tolist()
+    for lag in [(0,) * ndim, (1,) + (0,) * (ndim - 1), (0, 1) + (0,) * (ndim - 2), (2, -1) + (0,) * (ndim - 2),
+                (-3, 2) + ((1,) if ndim == 3 else ()), (4, 4) + ((-2,) if ndim == 3 else ())]:
+        assert abs(_circular_autocorr(h, lag) - _cov_formula(0, lag, Lam)) < 1e-12, lag
+
+
 def test_P13_power_law_embedding():
     """Power law on the unpadded torus (reading F3): the spectrum of the slowly
     decaying (r^-1/2) covariance has negative parts, which are clipped.  The pipeline's

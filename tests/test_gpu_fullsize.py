@@ -107,6 +107,167 @@ def test_fullsize_halfsweep_sampled(c5):
     assert worst <= 1e-12, worst
 
 
+def block_R(w, lo, hi):
+    """K sub-block [lo, hi) (clipped to the domain), its BC table (artificial sides: no
+    flow) and the oracle faces with the GLOBAL spacing."""
+    lo = [max(0, v) for v in lo]
+    hi = [min(w.n[d], hi[d]) for d in range(3)]
+    sl = (slice(lo[2], hi[2]), slice(lo[1], hi[1]), slice(lo[0], hi[0]))
+    bc = []
+    for d in range(3):
+        bc.append(w.bc[2 * d] if lo[d] == 0 else (0, 0.0))
+        bc.append(w.bc[2 * d + 1] if hi[d] == w.n[d] else (0, 0.0))
+    n_sub = tuple(hi[d] - lo[d] for d in range(3))
+    return sl, lo, oracle_faces_local(w, sl, bc, n_sub)
+
+
+def smooth_block(T, r, z, zoff, nhalf):
+    """nhalf alternating half-sweeps starting red on a block whose global parity offset is
+    zoff (the oracle's O12 with the global red-black colouring)."""
+    dg = O.diagonal(T, z.shape)
+    for h in range(nhalf):
+        col = h % 2
+        O.halfsweep(T, dg, r, z, col, O.colour_mask(z.shape, col, zoff=zoff))
+    return z
+
+
+def test_fullsize_cg_direction_and_residual_sampled(c5):
+    """a10 and a4 at 512^3 through the solver's own kernels (TMA SpMV in direction and in
+    residual mode): p_out, q and r at sampled cells against the oracle's formulas on the
+    3x3x3 block around each cell; p.q and ||r||^2 against a host reduction of the outputs."""
+    torch, w, s = c5
+    rng = np.random.default_rng(31)
+    z = rng.standard_normal(w.shape)
+    pin = rng.standard_normal(w.shape)
+    rho, rho_prev = 1.3, 0.9
+    pg, qg, pq = s.cg_direction(0, torch.from_numpy(z.ravel()).cuda(), torch.from_numpy(pin.ravel()).cuda(),
+                                rho, rho_prev, False)
+    pg = pg.cpu().numpy().reshape(w.shape)
+    qg = qg.cpu().numpy().reshape(w.shape)
+    beta = rho / rho_prev
+    worst = 0.0
+    for (i, j, k) in samples(w):
+        sl, bc, n_sub, cen = local_block(w, i, j, k)
+        T = oracle_faces_local(w, sl, bc, n_sub)
+        p = z[sl] + beta * pin[sl]
+        assert abs(pg[k, j, i] - p[cen]) <= 1e-15 * (abs(p[cen]) + 1.0)
+        ref = O.apply_A(T, p)[cen]
+        worst = max(worst, abs(qg[k, j, i] - ref) / (abs(ref) + 1e-300))
+    assert worst <= 1e-12, worst
+    host = float(np.dot(pg.ravel(), qg.ravel()))
+    assert abs(pq - host) <= 1e-12 * np.linalg.norm(pg) * np.linalg.norm(qg)
+    del pg, qg
+    b = rng.standard_normal(w.shape)
+    rgg, rr = s.residual(0, torch.from_numpy(b.ravel()).cuda(), torch.from_numpy(z.ravel()).cuda())
+    rgg = rgg.cpu().numpy().reshape(w.shape)
+    worst = 0.0
+    for (i, j, k) in samples(w, seed=6):
+        sl, bc, n_sub, cen = local_block(w, i, j, k)
+        T = oracle_faces_local(w, sl, bc, n_sub)
+        ref = b[k, j, i] - O.apply_A(T, z[sl])[cen]
+        worst = max(worst, abs(rgg[k, j, i] - ref) / (abs(ref) + 1e-300))
+    assert worst <= 1e-12, worst
+    assert abs(rr - float(np.dot(rgg.ravel(), rgg.ravel()))) <= 1e-12 * rr
+
+
+def test_fullsize_presmooth_restrict_sampled(c5):
+    """a5 + a6 at 512^3 exactly as the preconditioner runs them (4 TMA pairs from zero, the
+    fused closing red sweep + black residual, k_restrict_x_black, the y/z passes): z at
+    sampled fine cells and R (r - A z) at sampled coarse cells against the oracle's
+    half-sweeps on blocks wide enough that their artificial edges cannot reach the sample
+    (information moves one cell per half-sweep: 9 sweeps + the residual's stencil)."""
+    torch, w, s = c5
+    rng = np.random.default_rng(32)
+    r = rng.standard_normal(w.shape)
+    zg, cbg = s.presmooth_restrict(0, torch.from_numpy(r.ravel()).cuda())
+    zg = zg.cpu().numpy().reshape(w.shape)
+    nc = [w.n[d] // 4 for d in range(3)]
+    cbg = cbg.cpu().numpy().reshape(nc[2], nc[1], nc[0])
+    E = [O.interp_1d(w.n[d], 4) for d in range(3)]
+    R = 10
+    worst_z = 0.0
+    for (i, j, k) in samples(w, n=24, seed=7):
+        sl, lo, T = block_R(w, (i - R, j - R, k - R), (i + R + 1, j + R + 1, k + R + 1))
+        zz = smooth_block(T, r[sl], np.zeros(r[sl].shape), sum(lo), 9)
+        ref = zz[k - lo[2], j - lo[1], i - lo[0]]
+        worst_z = max(worst_z, abs(zg[k, j, i] - ref) / (abs(ref) + 1e-300))
+    assert worst_z <= 1e-12, worst_z
+    crng = np.random.default_rng(8)
+    cpts = [tuple(int(crng.integers(0, nc[d])) for d in range(3)) for _ in range(10)]
+    cpts += [(0, 0, 0), (nc[0] - 1, nc[1] - 1, nc[2] - 1), (0, nc[1] // 2, nc[2] - 1)]
+    worst = 0.0
+    for (I, J, K) in cpts:
+        sup = [np.nonzero(E[d][:, (I, J, K)[d]])[0] for d in range(3)]
+        lo = [int(sup[d].min()) - R for d in range(3)]
+        hi = [int(sup[d].max()) + R + 1 for d in range(3)]
+        sl, lo, T = block_R(w, lo, hi)
+        rb = r[sl]
+        zz = smooth_block(T, rb, np.zeros(rb.shape), sum(lo), 9)
+        sres = rb - O.apply_A(T, zz)
+        wx = E[0][lo[0]:lo[0] + rb.shape[2], I]
+        wy = E[1][lo[1]:lo[1] + rb.shape[1], J]
+        wz = E[2][lo[2]:lo[2] + rb.shape[0], K]
+        ref = float(np.einsum("kji,k,j,i->", sres, wz, wy, wx, optimize=True))
+        got = cbg[K, J, I]
+        worst = max(worst, abs(got - ref) / (abs(ref) + 1e-300))
+    assert worst <= 1e-12, worst
+
+
+def test_fullsize_prolong_postsmooth_sampled(c5):
+    """a8 + a9 at 512^3 exactly as the preconditioner runs them (black prolongation from
+    the weight tables, 4 TMA pairs, the closing red sweep with rho = r.z): z at sampled
+    cells against z + E y and 9 half-sweeps on blocks; rho against a host reduction."""
+    torch, w, s = c5
+    rng = np.random.default_rng(33)
+    nc = [w.n[d] // 4 for d in range(3)]
+    r = rng.standard_normal(w.shape)
+    z0 = rng.standard_normal(w.shape)
+    y = rng.standard_normal((nc[2], nc[1], nc[0]))
+    zg, rho = s.prolong_postsmooth(0, torch.from_numpy(y.ravel()).cuda(), torch.from_numpy(r.ravel()).cuda(),
+                                   torch.from_numpy(z0.ravel()).cuda())
+    zg = zg.cpu().numpy().reshape(w.shape)
+    E = [O.interp_1d(w.n[d], 4) for d in range(3)]
+    R = 10
+    worst = 0.0
+    for (i, j, k) in samples(w, n=24, seed=10):
+        sl, lo, T = block_R(w, (i - R, j - R, k - R), (i + R + 1, j + R + 1, k + R + 1))
+        sh = r[sl].shape
+        Ey = np.tensordot(E[2][lo[2]:lo[2] + sh[0]], y, axes=(1, 0))                       # (k, J, I)
+        Ey = np.moveaxis(np.tensordot(E[1][lo[1]:lo[1] + sh[1]], Ey, axes=(1, 1)), 0, 1)    # (k, j, I)
+        Ey = np.tensordot(Ey, E[0][lo[0]:lo[0] + sh[2]], axes=(2, 1))                      # (k, j, i)
+        zz = smooth_block(T, r[sl], z0[sl] + Ey, sum(lo), 9)
+        ref = zz[k - lo[2], j - lo[1], i - lo[0]]
+        worst = max(worst, abs(zg[k, j, i] - ref) / (abs(ref) + 1e-300))
+    assert worst <= 1e-12, worst
+    host = float(np.dot(r.ravel(), zg.ravel()))
+    assert abs(rho - host) <= 1e-12 * np.linalg.norm(r) * np.linalg.norm(zg)
+
+
+def test_fullsize_solve_matches_oracle_golden(c5):
+    """The bench solve against the CPU oracle run once on the full C5 problem
+    (tests/golden/c5_oracle.json, written by scripts/oracle_c5.py from oracle/ only):
+    per-level counts (reported; level 0 equal, coarse levels within 1 %), the solution at
+    the oracle's seeded sample of cells within the 1e-8 solve gate, and both true
+    residuals <= 1e-10."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c5_oracle.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c5_oracle.json not generated")
+    g = json.load(open(path))
+    torch, w, s = c5
+    x, rep = s.solve(torch.from_numpy(w.f.ravel()).cuda(), rel_tol=w.rel_tol)
+    print("C5 full: gpu iters", rep.iters, "oracle", g["iters"])
+    assert g["true_rel_res"] <= 1e-10 and rep.true_rel_res <= 1e-10
+    assert rep.iters[0] == g["iters"][0]
+    for a, b in zip(rep.iters[1:], g["iters"][1:]):
+        assert abs(a - b) <= max(2, 0.01 * b), (rep.iters, g["iters"])
+    xs = x.cpu().numpy()[np.asarray(g["sample_idx"])]
+    xo = np.asarray(g["sample_x"])
+    assert np.linalg.norm(xs - xo) <= 1e-8 * np.linalg.norm(xo)
+    assert abs(float(np.linalg.norm(x.cpu().numpy())) - g["x_l2"]) <= 1e-8 * g["x_l2"]
+
+
 def test_fullsize_solve_properties(c5):
     """The bench workload solved to rel 1e-10: the library's true residual, and the
     per-cell residual b - A x from the oracle's formulas at sampled cells."""

@@ -158,6 +158,41 @@ def test_P1_series_column_exact():
     assert np.allclose(x, np.broadcast_to(expect, (ny, nx)), rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("ndim", [2, 3])
+def test_P1_neumann_flux_column_exact(ndim):
+    """O5's Neumann term A_f q_f (inward flux q): a layered column K = K(x)
+    with flux q imposed through x-, Dirichlet g on x+ and no flow across the other sides
+    carries q A_x through every x-face, so the cell-centre pressure rises from g by q times
+    the resistance accumulated from the x+ boundary (half a cell at the Dirichlet face,
+    h/(2K) + h/(2K') between centres) -- Ohm's law with an imposed current, exactly.  A
+    wrong area, h factor or sign in the flux term fails it (the Dirichlet side of the same
+    column is pinned by test_P1_series_column_exact)."""
+    nx, ny, nz = 16, 3, (4 if ndim == 3 else 1)
+    rng = np.random.default_rng(6)
+    kx = 10 ** rng.uniform(-2, 2, nx)
+    shape = O.shape_of(ndim, (nx, ny, nz))
+    K = np.broadcast_to(kx, shape)[None].copy()
+    q, g = 0.7, -1.5
+    bc = bc_table(ndim, {"x-": (NEUMANN, q), "x+": (DIRICHLET, g)})
+    h = 1.0 / nx
+    A = (1.0 / ny) * ((1.0 / nz) if ndim == 3 else 1.0)
+    Rhalf = h / (2 * kx * A)                            # half-cell resistances
+    p = np.empty(nx)
+    p[-1] = g + q * A * Rhalf[-1]
+    for i in range(nx - 2, -1, -1):
+        p[i] = p[i + 1] + q * A * (Rhalf[i] + Rhalf[i + 1])
+    expect = np.broadcast_to(p, shape)
+    T = O.assemble_faces(ndim, (nx, ny, nz), K, bc)
+    b = O.rhs(ndim, (nx, ny, nz), T, np.zeros(shape), bc)
+    assert np.allclose(O.apply_A(T, expect), b, rtol=0, atol=1e-13 * np.abs(b).max())
+    # the flux enters only the x- boundary cells, as A_x q
+    bx0 = b[..., 0]
+    assert np.allclose(bx0, q * A, rtol=1e-14)
+    o = O.MultiScaleOracle(ndim, (nx, ny, nz), K, bc, depth=0)
+    x, info = o.solve(np.zeros(shape), rel_tol=1e-14)
+    assert np.allclose(x, expect, rtol=1e-11, atol=1e-11 * np.abs(expect).max())
+
+
 # ---------------------------------------------------------------- P2 closed forms
 @pytest.mark.parametrize("ndim,n,modes,interp", [
     (2, (32, 32, 1), (1, 2), "linear"),
