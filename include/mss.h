@@ -71,9 +71,19 @@ typedef struct {
                            1 = geometric per-axis chain n_k = round(n_0 / s_eff^k), s_eff =
                                (n_0 / n_L)^(1/L), non-integer ratios with partial-overlap
                                weights (Table 1's 1001..4 chain);
-                           2 = explicit: level_dims[0..n_level_dims-1] (level 0 = n)       */
+                           2 = explicit: level_dims[0..n_level_dims-1] (level 0 = n);
+                           3 = automatic semi-coarsening ("aimed for cells with an
+                               aspect ratio of 1"; DESIGN reading A1): effective cell lengths
+                               e_d = sqrt(V / geometric mean of the level-0 interior T_d); each
+                               level coarsens the smallest-e axis by scale and every other axis
+                               towards the same length, by the divisor <= scale of n_d nearest
+                               (in log) the target; single-GPU contexts only (else MSS_EINVAL);
+                           4 = as 3 with non-integer ratios n'_d = round(n_d / target)     */
   int     n_level_dims;
   int64_t level_dims[MSS_MAX_LEVELS][3];
+  int     log_events;   /* capacity of the level-tree event log (the paper's Fig. LevelTree,
+                           P:510-514); 0 = off (default).  Read with
+                           mss_level_events after a solve.                                     */
 } mss_params;
 
 /* Per-solve report (the schema of the paper's Tables 1-2). */
@@ -165,6 +175,15 @@ int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, do
                          double rel_tol, int64_t* iters_per_level, double* true_rel_res);
 
 int mss_get_info(const mss_ctx* ctx, mss_info* info);            /* last solve's report */
+/* mss_level_events — the last solve's level tree ("the transition between levels
+ * ... determined dynamically"; Fig. LevelTree), recorded when the context was set
+ * up with params.log_events > 0.  events (host, 2*cap ints) receives up to cap events in the
+ * order they happened, each a pair (code, iterations): code = 2*level + 0 on entering a PCG
+ * call on that level, 2*level + 1 on leaving it, iterations = that call's count (0 on enter).
+ * The coarsest level's exact solves are not events (they are counted in mss_info).
+ * *n_events = the number of events the solve produced (> cap: the log was truncated).
+ * Errors: MSS_EINVAL (null ctx / n_events, or cap > 0 with null events), MSS_ECUDA. */
+int mss_level_events(const mss_ctx* ctx, int* events, int cap, int* n_events);
 
 /* ---- kernel-level hooks (parity tests) ---------------------------------------------
  * Level-local compact device vectors (N_k doubles, x fastest; caller-owned, read or written

@@ -298,6 +298,82 @@ def geometric_hierarchy_dims(n, ndim, s=4, depth=None, coarse_min=512):
     return dims
 
 
+# ----------------------------------------------------------------------------- O8b
+def effective_lengths(ndim, n, T):
+    """Reading A1 of "the coarsening strategy aimed for cells with an aspect
+    ratio of 1", with anisotropic K folded in as the paper does ("10 to 1
+    aspect ratio ... equivalent to a non-isotropic permeability field with K_yy a factor
+    of 100 times K_xx"): the effective cell length along d is
+    e_d = sqrt(V / Tg_d), Tg_d the geometric mean of the interior d-faces' transmissibility
+    (for uniform K, T_d = K_d V / h_d^2, so e_d = h_d / sqrt(K_d)).  An axis with one cell
+    has no interior face: e_d = inf (it is never coarsened)."""
+    _, _, V = geometry(ndim, n)
+    e = []
+    for d in range(ndim):
+        ax = axis_of(ndim, d)
+        nd = T[d].shape[ax]
+        if nd <= 2:
+            e.append(math.inf)
+            continue
+        interior = T[d][_sl(ndim, ax, slice(1, nd - 1))]
+        e.append(math.sqrt(V / math.exp(float(np.mean(np.log(interior))))))
+    return e
+
+
+def aspect_step(cur, e, E, ndim, s, integer=True):
+    """One coarsening of the aspect rule (reading A1): each axis aims at the coarse
+    effective length E, target factor t_d = max(1, E / e_d).  integer: the factor is the
+    divisor q of n_d with 1 <= q <= s nearest t_d in log (ties: the larger); otherwise
+    n'_d = max(1, round(n_d / t_d)) (non-integer ratios).
+    Returns the coarse dims and effective lengths e'_d = e_d n_d / n'_d."""
+    nxt, en = list(cur), list(e)
+    for d in range(ndim):
+        if cur[d] <= 1:
+            continue
+        t = max(1.0, E / e[d])
+        if integer:
+            best, bd = 1, None
+            for q in range(1, min(s, cur[d]) + 1):
+                if cur[d] % q:
+                    continue
+                dq = abs(math.log(q) - math.log(t))
+                if bd is None or dq < bd - 1e-12 or abs(dq - bd) <= 1e-12:
+                    best, bd = q, dq
+            nxt[d] = cur[d] // best
+        else:
+            nxt[d] = max(1, _round_half_up(cur[d] / t))
+        en[d] = e[d] * cur[d] / nxt[d]
+    return tuple(nxt), en
+
+
+def aspect_hierarchy_dims(n, ndim, e0, s=4, depth=None, coarse_min=512, integer=True):
+    """NEXT-2 automatic semi-coarsening (reading A1): every level coarsens the
+    axis of smallest effective length by s and the others only as far as their cells reach
+    that length (E = s * min_d e_d); stops like O8 (explicit depth, or N_k <= coarse_min),
+    or when no axis can be coarsened."""
+    dims = [tuple(list(n[:ndim]) + [1] * (3 - ndim))]
+    e = list(e0)
+    while True:
+        cur = dims[-1]
+        if depth is not None:
+            if len(dims) - 1 >= depth:
+                break
+        elif int(np.prod(cur[:ndim])) <= coarse_min:
+            break
+        act = [e[d] for d in range(ndim) if cur[d] > 1]
+        if not act:
+            if depth is not None:
+                raise OracleError("explicit depth deeper than the aspect rule can coarsen")
+            break
+        nxt, e = aspect_step(cur, e, s * min(act), ndim, s, integer)
+        if nxt == cur:
+            if depth is not None:
+                raise OracleError("explicit depth deeper than the aspect rule can coarsen")
+            break
+        dims.append(nxt)
+    return dims
+
+
 # ----------------------------------------------------------------------------- O9
 def face_cv_weights(n, s, n_c=None):
     """w[F, i] = |CV_i ∩ CV_F| / |CV_i| (Reading B, Q2).
@@ -517,14 +593,18 @@ class MultiScaleOracle:
             raise OracleError("K must be finite and > 0")
         if not any(k == DIRICHLET for k, _ in bc):
             raise OracleError("all-Neumann operator is singular")
+        T = assemble_faces(ndim, self.n0, K, bc)                              # a1
         if level_dims is not None:
             dims = [tuple(list(d) + [1] * (3 - len(d))) for d in level_dims]
         elif dims_mode == "geometric":
             dims = geometric_hierarchy_dims(self.n0, ndim, s, depth, coarse_min)
+        elif dims_mode in ("aspect", "aspect_geometric"):
+            self.e0 = effective_lengths(ndim, self.n0, T)
+            dims = aspect_hierarchy_dims(self.n0, ndim, self.e0, s, depth, coarse_min,
+                                         integer=(dims_mode == "aspect"))
         else:
             dims = hierarchy_dims(self.n0, ndim, s, depth, coarse_min)
         self.dims = dims
-        T = assemble_faces(ndim, self.n0, K, bc)                              # a1
         self.levels: List[Level] = []
         for k, nk in enumerate(dims):
             if k > 0:

@@ -23,26 +23,45 @@ __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_ca
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double sel(const double2& v, int par) { return par ? v.y : v.x; }
 
-// Matrix-free faces for a scalar-K level 0: the transmissibility of a face is recomputed
-// from the two cell K values with exactly the expression of k_assemble_faces (harmonic
-// mean P:345-346, T = (A/h) K P:381-383, Dirichlet half-cell 2 (A/h) K, Neumann 0), so it
-// is bit-identical to the stored T while the kernel streams 1 word of K per cell instead
-// of 3 words of faces (HBM traffic traded for fp64 divisions, which the half-sweep has
-// spare: it is bandwidth-bound at ~0.3 flop/B).
-struct KFaces {
-  const double* K;        // scalar K with ghost planes (interior pointer)
-  double cx, cy, cz;      // A_d / h_d
-  int dxl, dxh, dyl, dyh, dzl, dzh;   // Dirichlet flags of the six sides
-};
-__device__ __forceinline__ double hmf(double ka, double kb, double coef) { return coef * (2.0 * ka * kb / (ka + kb)); }
-__device__ __forceinline__ double bndf(int dir, double coef, double k) { return dir ? 2.0 * coef * k : 0.0; }
+// L2 residency of a level's sweep operands (LevelDev::l2keep): the half-sweeps of a level
+// whose faces, r and z fit in L2 re-read them every pass, but its whole working set does
+// not fit (128^3: T + r + z 84 MB, all vectors ~170 MB), so plain LRU-like replacement
+// evicts them between passes.  Marked evict_last they stay; other data streams past.
+__device__ __forceinline__ uint64_t l2_policy(int keep) {
+  uint64_t p;
+  if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld2p(const double* a, uint64_t pol) {
+  double2 v;
+  asm("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ldg2p(const double* a, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld1p(const double* a, uint64_t pol) {
+  double v;
+  asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg1p(const double* a, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st1p(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
 
 // Half-sweep of colour `colour` over planes [blockIdx.z * kchunk, +kchunk).
-// KF: faces recomputed from scalar K (KFaces) instead of loaded from the face arrays.
-template <bool FIRST, bool DOT, int MINB, bool KF = false>
+template <bool FIRST, bool DOT, int MINB>
 __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, const double* __restrict__ r,
                                                               double* __restrict__ z, int colour, int kchunk,
-                                                              RedOut ro, KFaces kf = KFaces()) {
+                                                              RedOut ro) {
   const int m = blockIdx.x * kColX + threadIdx.x;
   const int j = blockIdx.y * kColY + threadIdx.y;
   const int k0 = blockIdx.z * kchunk;
@@ -50,85 +69,58 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, c
   const int nx = L.nx, ny = L.ny;
   const int64_t plane = L.plane;
   double acc = 0.0;
+  const uint64_t pol = l2_policy(L.l2keep);
   if (2 * m < nx && j < ny && k0 < k1) {
     const int i0 = 2 * m;
     const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
     int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
     double2 zdn = make_double2(0.0, 0.0), zc = make_double2(0.0, 0.0);
     if (!FIRST) {
-      zdn = ld2(z + c - plane);            // plane k0-1 (ghost plane when k0 == 0)
-      zc = ld2(z + c);
+      zdn = ld2p(z + c - plane, pol);            // plane k0-1 (ghost plane when k0 == 0)
+      zc = ld2p(z + c, pol);
     }
-    double2 tzl = make_double2(0.0, 0.0), Kd = make_double2(0.0, 0.0), Kc = make_double2(0.0, 0.0);
-    if (KF) {
-      Kd = ldg2(kf.K + c - plane);
-      Kc = ldg2(kf.K + c);
-    } else {
-      tzl = ldg2(L.Tz + c);
-    }
+    double2 tzl = ldg2p(L.Tz + c, pol);
     for (int k = k0; k < k1; ++k) {
       const int par = (i0 + j + k + L.z0 + colour) & 1;   // updated cell: i0 + par
       double txl, txh, t2, t3, t4, t5;
-      double2 tzu = make_double2(0.0, 0.0), Ku = make_double2(0.0, 0.0);
-      if (KF) {
-        const int kg = k + L.z0;
-        Ku = ldg2(kf.K + c + plane);
-        const double kc = sel(Kc, par);
-        if (par) {
-          txl = hmf(Kc.x, Kc.y, kf.cx);
-          txh = hasR ? hmf(Kc.y, __ldg(kf.K + c + 2), kf.cx) : bndf(kf.dxh, kf.cx, Kc.y);
-        } else {
-          txl = hasL ? hmf(__ldg(kf.K + c - 1), Kc.x, kf.cx) : bndf(kf.dxl, kf.cx, Kc.x);
-          txh = hmf(Kc.x, Kc.y, kf.cx);
-        }
-        t2 = hasS ? hmf(sel(ldg2(kf.K + c - nx), par), kc, kf.cy) : bndf(kf.dyl, kf.cy, kc);
-        t3 = hasN ? hmf(kc, sel(ldg2(kf.K + c + nx), par), kf.cy) : bndf(kf.dyh, kf.cy, kc);
-        t4 = (kg > 0) ? hmf(sel(Kd, par), kc, kf.cz) : bndf(kf.dzl, kf.cz, kc);
-        t5 = (kg < L.nzg - 1) ? hmf(kc, sel(Ku, par), kf.cz) : bndf(kf.dzh, kf.cz, kc);
-      } else {
-        const int64_t row = j + (int64_t)ny * k;
-        const int64_t fx = c + row;
-        const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
-        const int64_t fy = c + (int64_t)nx * k;
-        const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
-        tzu = ldg2(L.Tz + c + plane);
-        txl = par ? tx1 : tx0;
-        txh = par ? tx2 : tx1;
-        t2 = sel(tyl, par); t3 = sel(tyu, par); t4 = sel(tzl, par); t5 = sel(tzu, par);
-      }
-      const double2 rr = ld2(r + c);
+      double2 tzu = make_double2(0.0, 0.0);
+      const int64_t row = j + (int64_t)ny * k;
+      const int64_t fx = c + row;
+      const double tx0 = ldg1p(L.Tx + fx, pol), tx1 = ldg1p(L.Tx + fx + 1, pol), tx2 = ldg1p(L.Tx + fx + 2, pol);
+      const int64_t fy = c + (int64_t)nx * k;
+      const double2 tyl = ldg2p(L.Ty + fy, pol), tyu = ldg2p(L.Ty + fy + nx, pol);
+      tzu = ldg2p(L.Tz + c + plane, pol);
+      txl = par ? tx1 : tx0;
+      txh = par ? tx2 : tx1;
+      t2 = sel(tyl, par); t3 = sel(tyu, par); t4 = sel(tzl, par); t5 = sel(tzu, par);
+      const double2 rr = ldg2p(r + c, pol);
       const double rp = sel(rr, par);
       double zup_x = 0.0, zup_y = 0.0;
       double acc_c = rp;
       if (!FIRST) {
-        const double2 zup = ld2(z + c + plane);
+        const double2 zup = ld2p(z + c + plane, pol);
         zup_x = zup.x;
         zup_y = zup.y;
         double xl, xh;
         if (par) {
           xl = zc.x;
-          xh = hasR ? z[c + 2] : 0.0;
+          xh = hasR ? ld1p(z + c + 2, pol) : 0.0;
         } else {
-          xl = hasL ? z[c - 1] : 0.0;
+          xl = hasL ? ld1p(z + c - 1, pol) : 0.0;
           xh = zc.y;
         }
-        const double ys = hasS ? sel(ld2(z + c - nx), par) : 0.0;
-        const double yn = hasN ? sel(ld2(z + c + nx), par) : 0.0;
+        const double ys = hasS ? sel(ld2p(z + c - nx, pol), par) : 0.0;
+        const double yn = hasN ? sel(ld2p(z + c + nx, pol), par) : 0.0;
         acc_c += txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * (par ? zup_y : zup_x);
       }
       const double zn = acc_c / (txl + txh + t2 + t3 + t4 + t5);
-      z[c + par] = zn;
+      st1p(z + c + par, zn, pol);
       if (DOT) acc += rp * zn + sel(rr, 1 - par) * sel(zc, 1 - par);
       if (!FIRST) {
         zdn = zc;
         zc = make_double2(zup_x, zup_y);
       }
-      if (KF) {
-        Kd = Kc;
-        Kc = Ku;
-      } else {
-        tzl = tzu;
-      }
+      tzl = tzu;
       c += plane;
     }
   }
@@ -138,11 +130,11 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_sweep_col(LevelDev L, c
 // a10 column-walk: p_out = z + beta p_in (p = z when first); q = A p_out; p.q reduced.
 // Neighbour p values are formed on the fly from z and p_in (never from p_out), so the
 // pass has no intra-launch dependency.
-template <int MINB, bool KF = false>
+template <int MINB>
 __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, const double* __restrict__ z,
                                                              const double* __restrict__ pin, double* __restrict__ pout,
                                                              double* __restrict__ q, const Scal* sc, int first,
-                                                             int kchunk, RedOut ro, KFaces kf = KFaces()) {
+                                                             int kchunk, RedOut ro) {
   const int m = blockIdx.x * kColX + threadIdx.x;
   const int j = blockIdx.y * kColY + threadIdx.y;
   const int k0 = blockIdx.z * kchunk;
@@ -164,47 +156,16 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
     auto P1 = [&](int64_t idx) { return first ? z[idx] : z[idx] + beta * pin[idx]; };
     double2 pdn = P2(c - plane);
     double2 pc = P2(c);
-    double2 tzl = make_double2(0.0, 0.0), Kd = make_double2(0.0, 0.0), Kc = make_double2(0.0, 0.0);
-    if (KF) {
-      Kd = ldg2(kf.K + c - plane);
-      Kc = ldg2(kf.K + c);
-      const int kg = k0 + L.z0;
-      tzl = (kg > 0) ? make_double2(hmf(Kd.x, Kc.x, kf.cz), hmf(Kd.y, Kc.y, kf.cz))
-                     : make_double2(bndf(kf.dzl, kf.cz, Kc.x), bndf(kf.dzl, kf.cz, Kc.y));
-    } else {
-      tzl = ldg2(L.Tz + c);
-    }
+    double2 tzl = ldg2(L.Tz + c);
     for (int k = k0; k < k1; ++k) {
       double tx0, tx1, tx2;
-      double2 tyl, tyu, tzu, Ku = make_double2(0.0, 0.0);
-      if (KF) {
-        const int kg = k + L.z0;
-        Ku = ldg2(kf.K + c + plane);
-        tx0 = hasL ? hmf(__ldg(kf.K + c - 1), Kc.x, kf.cx) : bndf(kf.dxl, kf.cx, Kc.x);
-        tx1 = hmf(Kc.x, Kc.y, kf.cx);
-        tx2 = hasR ? hmf(Kc.y, __ldg(kf.K + c + 2), kf.cx) : bndf(kf.dxh, kf.cx, Kc.y);
-        if (hasS) {
-          const double2 Ks = ldg2(kf.K + c - nx);
-          tyl = make_double2(hmf(Ks.x, Kc.x, kf.cy), hmf(Ks.y, Kc.y, kf.cy));
-        } else {
-          tyl = make_double2(bndf(kf.dyl, kf.cy, Kc.x), bndf(kf.dyl, kf.cy, Kc.y));
-        }
-        if (hasN) {
-          const double2 Kn = ldg2(kf.K + c + nx);
-          tyu = make_double2(hmf(Kc.x, Kn.x, kf.cy), hmf(Kc.y, Kn.y, kf.cy));
-        } else {
-          tyu = make_double2(bndf(kf.dyh, kf.cy, Kc.x), bndf(kf.dyh, kf.cy, Kc.y));
-        }
-        tzu = (kg < L.nzg - 1) ? make_double2(hmf(Kc.x, Ku.x, kf.cz), hmf(Kc.y, Ku.y, kf.cz))
-                               : make_double2(bndf(kf.dzh, kf.cz, Kc.x), bndf(kf.dzh, kf.cz, Kc.y));
-      } else {
-        const int64_t row = j + (int64_t)ny * k;
-        const int64_t fx = c + row;
-        tx0 = __ldg(L.Tx + fx); tx1 = __ldg(L.Tx + fx + 1); tx2 = __ldg(L.Tx + fx + 2);
-        const int64_t fy = c + (int64_t)nx * k;
-        tyl = ldg2(L.Ty + fy); tyu = ldg2(L.Ty + fy + nx);
-        tzu = ldg2(L.Tz + c + plane);
-      }
+      double2 tyl, tyu, tzu;
+      const int64_t row = j + (int64_t)ny * k;
+      const int64_t fx = c + row;
+      tx0 = __ldg(L.Tx + fx); tx1 = __ldg(L.Tx + fx + 1); tx2 = __ldg(L.Tx + fx + 2);
+      const int64_t fy = c + (int64_t)nx * k;
+      tyl = ldg2(L.Ty + fy); tyu = ldg2(L.Ty + fy + nx);
+      tzu = ldg2(L.Tz + c + plane);
       const double2 pup = P2(c + plane);
       const double2 ps = hasS ? P2(c - nx) : make_double2(0.0, 0.0);
       const double2 pn = hasN ? P2(c + nx) : make_double2(0.0, 0.0);
@@ -222,10 +183,6 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
       pdn = pc;
       pc = pup;
       tzl = tzu;
-      if (KF) {
-        Kd = Kc;
-        Kc = Ku;
-      }
       c += plane;
     }
   }
@@ -237,11 +194,11 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
 // (the red residual is zero after the closing red sweep); the x-weighted
 // contributions meet in shared memory and thread I sums the pairs of coarse cell I in
 // a fixed order (deterministic).  t1 has dims (ncx, ny, nz).
-template <int MINB, bool KF = false>
+template <int MINB>
 __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, const double* __restrict__ r,
                                                                   const double* __restrict__ z,
                                                                   double* __restrict__ t1, int ncx, int s, int kind,
-                                                                  int kchunk, KFaces kf = KFaces()) {
+                                                                  int kchunk) {
   extern __shared__ double shc[];             // [2 * hx] contributions
   int* shi = reinterpret_cast<int*>(shc + 2 * blockDim.x);   // [2 * hx] coarse indices (per parity: 4 * hx)
   const int nx = L.nx, ny = L.ny;
@@ -265,48 +222,25 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
   const bool hasL = i0 > 0, hasR = i0 + 2 < nx, hasS = j > 0, hasN = j < ny - 1;
   int64_t c = i0 + (int64_t)nx * (j + (int64_t)ny * k0);
   double2 zdn = make_double2(0, 0), zc = make_double2(0, 0), tzl = make_double2(0, 0);
-  double2 Kd = make_double2(0, 0), Kc = make_double2(0, 0);
   if (act && k0 < k1) {
     zdn = ld2(z + c - plane);
     zc = ld2(z + c);
-    if (KF) {
-      Kd = ldg2(kf.K + c - plane);
-      Kc = ldg2(kf.K + c);
-    } else {
-      tzl = ldg2(L.Tz + c);
-    }
+    tzl = ldg2(L.Tz + c);
   }
   for (int k = k0; k < k1; ++k) {
     const int par = (i0 + j + k + L.z0 + 1) & 1;   // black cell of the pair: i0 + par
-    double2 zup = make_double2(0, 0), tzu = make_double2(0, 0), Ku = make_double2(0, 0);
+    double2 zup = make_double2(0, 0), tzu = make_double2(0, 0);
     if (act) {
       double txl, txh, t2, t3, t4, t5;
-      if (KF) {
-        const int kg = k + L.z0;
-        Ku = ldg2(kf.K + c + plane);
-        const double kc = sel(Kc, par);
-        if (par) {
-          txl = hmf(Kc.x, Kc.y, kf.cx);
-          txh = hasR ? hmf(Kc.y, __ldg(kf.K + c + 2), kf.cx) : bndf(kf.dxh, kf.cx, Kc.y);
-        } else {
-          txl = hasL ? hmf(__ldg(kf.K + c - 1), Kc.x, kf.cx) : bndf(kf.dxl, kf.cx, Kc.x);
-          txh = hmf(Kc.x, Kc.y, kf.cx);
-        }
-        t2 = hasS ? hmf(sel(ldg2(kf.K + c - nx), par), kc, kf.cy) : bndf(kf.dyl, kf.cy, kc);
-        t3 = hasN ? hmf(kc, sel(ldg2(kf.K + c + nx), par), kf.cy) : bndf(kf.dyh, kf.cy, kc);
-        t4 = (kg > 0) ? hmf(sel(Kd, par), kc, kf.cz) : bndf(kf.dzl, kf.cz, kc);
-        t5 = (kg < L.nzg - 1) ? hmf(kc, sel(Ku, par), kf.cz) : bndf(kf.dzh, kf.cz, kc);
-      } else {
-        const int64_t row = j + (int64_t)ny * k;
-        const int64_t fx = c + row;
-        const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
-        const int64_t fy = c + (int64_t)nx * k;
-        const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
-        tzu = ldg2(L.Tz + c + plane);
-        txl = par ? tx1 : tx0;
-        txh = par ? tx2 : tx1;
-        t2 = sel(tyl, par); t3 = sel(tyu, par); t4 = sel(tzl, par); t5 = sel(tzu, par);
-      }
+      const int64_t row = j + (int64_t)ny * k;
+      const int64_t fx = c + row;
+      const double tx0 = __ldg(L.Tx + fx), tx1 = __ldg(L.Tx + fx + 1), tx2 = __ldg(L.Tx + fx + 2);
+      const int64_t fy = c + (int64_t)nx * k;
+      const double2 tyl = ldg2(L.Ty + fy), tyu = ldg2(L.Ty + fy + nx);
+      tzu = ldg2(L.Tz + c + plane);
+      txl = par ? tx1 : tx0;
+      txh = par ? tx2 : tx1;
+      t2 = sel(tyl, par); t3 = sel(tyu, par); t4 = sel(tzl, par); t5 = sel(tzu, par);
       const double2 rr = ld2(r + c);
       zup = ld2(z + c + plane);
       double xl, xh;
@@ -341,10 +275,6 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
     zdn = zc;
     zc = zup;
     tzl = tzu;
-    if (KF) {
-      Kd = Kc;
-      Kc = Ku;
-    }
     c += plane;
   }
 }

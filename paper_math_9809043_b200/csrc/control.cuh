@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.cuh"
+#include "kernels.cuh"
 
 namespace mss {
 
@@ -21,10 +22,13 @@ struct LevelCtl {
 // Entry of a PCG call on level k: count the call, reset its iteration counter, and enter
 // the loop unless the residual already meets the level's criterion (reading Q6: the test
 // also runs before the first iteration) or an earlier breakdown aborted the solve.
-__global__ void k_pcg_enter(LevelCtl* c, const Scal* s, const int* flags, cudaGraphConditionalHandle h) {
+__global__ void k_pcg_enter(LevelCtl* c, const Scal* s, const int* flags, cudaGraphConditionalHandle h, int level,
+                            int* ev, int ev_cap) {
   c->calls += 1;
   c->it = 0;
   const bool go = flags[1] == 0 && !(s->rr < c->thr);
+  ev_push(ev, ev_cap, level, 0, 0);
+  if (!go) ev_push(ev, ev_cap, level, 1, 0);
   cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
@@ -32,7 +36,8 @@ __global__ void k_pcg_enter(LevelCtl* c, const Scal* s, const int* flags, cudaGr
 // non-finite residual -> flags[1] = level + 1), the stop test, and the per-call cap
 // (-> flags[0] = 1, MSS_NOT_CONVERGED).  Sets h1 (and h2 when nh == 2) to "continue".
 __global__ void k_pcg_check(LevelCtl* c, const Scal* s, int level, long long max_iter, int* flags,
-                            cudaGraphConditionalHandle h1, cudaGraphConditionalHandle h2, int nh) {
+                            cudaGraphConditionalHandle h1, cudaGraphConditionalHandle h2, int nh, int* ev,
+                            int ev_cap) {
   c->it += 1;
   c->iters += 1;
   unsigned go = 1;
@@ -47,6 +52,7 @@ __global__ void k_pcg_check(LevelCtl* c, const Scal* s, int level, long long max
     flags[0] = 1;
     go = 0;
   }
+  if (!go) ev_push(ev, ev_cap, level, 1, c->it);
   cudaGraphSetConditional(h1, go);
   if (nh == 2) cudaGraphSetConditional(h2, go);
 }

@@ -46,6 +46,8 @@ struct LevelDev {
   const double* Tx;
   const double* Ty;
   const double* Tz;   // nullptr in 2-D
+  int l2keep;         // 1: the column-walk kernels load / store T, r, z with an L2 evict_last
+                      // policy (a level whose sweep operands fit in L2, re-read every pass)
 };
 
 struct Level {
@@ -54,6 +56,7 @@ struct Level {
   int nzg = 0;                           // global nz
   bool dist = false;                     // true: z-slab distributed across ranks (ghost planes = halos)
   bool uniform = true;                   // transfer to level+1 is an integer scale factor on every axis
+  bool l2keep = false;                   // LevelDev::l2keep
   int64_t N = 0, plane = 0;
   double h[3] = {1, 1, 1};
   double *Tx = nullptr, *Ty = nullptr, *Tz = nullptr;
@@ -70,6 +73,7 @@ struct Level {
     LevelDev d;
     d.nx = nx; d.ny = ny; d.nz = nz; d.z0 = z0; d.nzg = nzg ? nzg : nz; d.plane = plane; d.N = N;
     d.Tx = Tx; d.Ty = Ty; d.Tz = Tz;
+    d.l2keep = l2keep ? 1 : 0;
     return d;
   }
 };
@@ -134,6 +138,9 @@ struct mss_ctx {
   std::vector<char> tail_h;                // host image of TailArgs
   long long* tail_cnt = nullptr;           // [2 * MSS_MAX_LEVELS] iters, calls
   int* tail_flags = nullptr;               // [0] not converged, [1] breakdown level + 1
+  int* d_ev = nullptr;                     // level-tree event log (kernels.cuh ev_push), null = off
+  int ev_cap = 0;
+  double eff_len[3] = {0, 0, 0};           // dims_mode 3/4: level-0 effective cell lengths e_d
   bool tail_dirty = true;
   // shared-memory-resident tail (tailsm.cuh)
   int tsm_L0 = -1;                         // top level it serves, -1 = unavailable
@@ -153,7 +160,6 @@ struct mss_ctx {
     int spmv_nch = 0;         // MSS_SPMV_NCH: 0 cost model
     bool fused_resid = true;  // MSS_FUSED_RESID
     bool prolong_pairs = true;// MSS_PROLONG_PAIRS
-    bool tail_nbsync = false; // MSS_TAIL_NBSYNC: neighbour-only sync after tail half-sweeps
     bool fused_prolong = false;// MSS_FUSED_PROLONG: a8 inside the first post-smoothing TMA pair
   } kn;
   // TMA tensor maps (pairtma.cuh), cached by base pointer and kind (opaque 128-byte images)
@@ -163,11 +169,6 @@ struct mss_ctx {
     alignas(64) unsigned char img[128];
   };
   std::vector<TmapEnt> tmaps;
-  // matrix-free level-0 faces from scalar K (colwalk.cuh KFaces)
-  bool kfaces = false;
-  double* kf_K = nullptr;                  // ghosted copy of K on level 0
-  double kf_c[3] = {0, 0, 0};
-  int kf_dir[6] = {0, 0, 0, 0, 0, 0};
   // distributed z-slabs (rank/nranks == 0/1 single GPU): levels [0, ndist) are split
   // across ranks, the rest are replicated on every rank
   int rank = 0, nranks = 1;

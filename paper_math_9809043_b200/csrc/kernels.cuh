@@ -15,6 +15,23 @@
 namespace mss {
 
 // ------------------------------------------------------------------ reductions (K10)
+// Level-tree event log (the paper's Fig. LevelTree: "the transition
+// between levels ... determined dynamically"): ev[0] counts the events recorded (it may
+// exceed cap), then (code, iterations) pairs from ev[2], code = 2 level + (0 enter | 1 leave),
+// iterations = the call's count on leave.  One PCG call = one enter and one leave, pushed in
+// stream order by one thread (host-driven levels, graph control kernels, the tails).
+__device__ __forceinline__ void ev_push(int* ev, int cap, int level, int leave, long long it) {
+  if (!ev) return;
+  const int i = atomicAdd(ev, 1);
+  if (i < cap) {
+    ev[2 + 2 * i] = 2 * level + leave;
+    ev[3 + 2 * i] = (int)it;
+  }
+}
+__global__ void k_ev_push(int* ev, int cap, int level, int leave, long long it) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ev_push(ev, cap, level, leave, it);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -178,6 +195,28 @@ __global__ void k_assemble_faces(const double* __restrict__ Kd, double* __restri
     }
     T[t] = val;
   }
+}
+
+// NEXT-2 automatic semi-coarsening (reading A1): per-block partial sums of
+// log T over the interior faces along d, T = the interior expression of k_assemble_faces;
+// the host adds the partials in block order (deterministic) for the geometric mean.
+__global__ void __launch_bounds__(256) k_logT_partial(const double* __restrict__ Kd, int nx, int ny, int nz, int d,
+                                                      double coef, double* __restrict__ part) {
+  const int Dx = nx - (d == 0), Dy = ny - (d == 1), Dz = nz - (d == 2);   // interior faces
+  const int64_t total = (int64_t)Dx * Dy * Dz;
+  double acc = 0.0;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int fi = (int)(t % Dx);
+    const int64_t rr = t / Dx;
+    const int fj = (int)(rr % Dy);
+    const int fk = (int)(rr / Dy);
+    const int64_t ca = fi + (int64_t)nx * (fj + (int64_t)ny * fk);
+    const int64_t cb = ca + ((d == 0) ? 1 : (d == 1) ? (int64_t)nx : (int64_t)nx * ny);
+    const double ka = Kd[ca], kb = Kd[cb];
+    acc += log(coef * (2.0 * ka * kb / (ka + kb)));
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 // a2: Reading B coarse faces:  1/T^c_F = sum_i w_i / sum_{rows} T_d(i, rows),

@@ -200,18 +200,6 @@ static void slab_of(int64_t nzg0, int64_t unit, int P, int r, int64_t* z0, int64
   *z1 = unit * (units * (r + 1) / P);
 }
 
-static KFaces kfaces_of(const mss_ctx* ctx) {
-  KFaces f;
-  f.K = ctx->kf_K;
-  f.cx = ctx->kf_c[0];
-  f.cy = ctx->kf_c[1];
-  f.cz = ctx->kf_c[2];
-  f.dxl = ctx->kf_dir[0]; f.dxh = ctx->kf_dir[1];
-  f.dyl = ctx->kf_dir[2]; f.dyh = ctx->kf_dir[3];
-  f.dzl = ctx->kf_dir[4]; f.dzh = ctx->kf_dir[5];
-  return f;
-}
-
 #define DISPATCH(ndim, kern, grid, ...)                               \
   do {                                                                \
     if ((ndim) == 3) LAUNCH(kern<3>, grid, __VA_ARGS__);              \
@@ -273,8 +261,8 @@ struct ProfScope {
 // Algorithmic bytes per cell (fp64 words x 8) of each kernel with the interleaved
 // layout (SURVEY §8(d) "interleaved" column): T = ndim words per cell.
 static double cell_bytes(const mss_ctx* ctx, int cls, int k = -1) {
-  // faces: ndim words per cell, or 1 word of K when level 0 recomputes them (kfaces)
-  const double T = (k == 0 && ctx->kfaces) ? 1.0 : (double)ctx->ndim;
+  // faces: ndim words per cell
+  const double T = (double)ctx->ndim;
   switch (cls) {
     case KC_SWEEP: return 8.0 * (T + 3);    // T + r + z(nbr lines) + z write (r.z fused: same lines)
     case KC_SWEEP0: return 8.0 * (T + 2);   // T + r + z write
@@ -326,26 +314,23 @@ static int op_halfsweep(mss_ctx* ctx, int k, const double* r, double* z, int col
   const LevelDev d = l.dev();
   if (col_ok(ctx, l)) {
     static const int minb = getenv("MSS_COL_MINB") ? atoi(getenv("MSS_COL_MINB")) : 4;  // 64 regs: measured best
-#define SWEEPCOL(MB, KFB)                                                                                   \
+#define SWEEPCOL(MB)                                                                                   \
     {                                                                                                       \
-      const void* kern = first ? (const void*)k_sweep_col<true, false, MB, KFB>                            \
-                               : (dot_out ? (const void*)k_sweep_col<false, true, MB, KFB>                  \
-                                          : (const void*)k_sweep_col<false, false, MB, KFB>);               \
+      const void* kern = first ? (const void*)k_sweep_col<true, false, MB>                            \
+                               : (dot_out ? (const void*)k_sweep_col<false, true, MB>                  \
+                                          : (const void*)k_sweep_col<false, false, MB>);               \
       dim3 grid;                                                                                            \
       int kch = 0;                                                                                          \
       if (col_grid(kern, l, &grid, &kch)) {                                                                 \
         const dim3 blk(kColX, kColY);                                                                       \
-        const KFaces kfs = kfaces_of(ctx);                                                                  \
-        if (first) k_sweep_col<true, false, MB, KFB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro, kfs); \
-        else if (dot_out) k_sweep_col<false, true, MB, KFB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro, kfs); \
-        else k_sweep_col<false, false, MB, KFB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro, kfs); \
+        if (first) k_sweep_col<true, false, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro); \
+        else if (dot_out) k_sweep_col<false, true, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro); \
+        else k_sweep_col<false, false, MB><<<grid, blk, 0, ctx->stream>>>(d, r, z, colour, kch, ro); \
         ctx->launches++;                                                                                    \
         return MSS_OK;                                                                                      \
       }                                                                                                     \
     }
-    if (k == 0 && ctx->kfaces && minb <= 2) SWEEPCOL(2, true)
-    else if (k == 0 && ctx->kfaces) SWEEPCOL(4, true)
-    else if (minb <= 3) SWEEPCOL(3, false) else if (minb == 4) SWEEPCOL(4, false) else SWEEPCOL(5, false)
+    if (minb <= 3) SWEEPCOL(3) else if (minb == 4) SWEEPCOL(4) else SWEEPCOL(5)
 #undef SWEEPCOL
   }
 #define HS(ND, F, D) LAUNCH((k_halfsweep<ND, F, D>), g, d, r, z, colour, ro)
@@ -379,7 +364,6 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.spmv_nch = geti("MSS_SPMV_NCH", 0);
   ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
-  ctx->kn.tail_nbsync = geti("MSS_TAIL_NBSYNC", 0) != 0;
   ctx->kn.fused_prolong = geti("MSS_FUSED_PROLONG", 0) != 0;
   ctx->graph_knob = geti("MSS_GRAPH", 1);
 }
@@ -718,7 +702,7 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
   {
-    const double by = 8.0 * ((k == 0 && ctx->kfaces ? 1 : ctx->ndim) + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
+    const double by = 8.0 * (ctx->ndim + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
     ProfScope ps(ctx, KC_RESID, k, by);
     const int hx = f.nx / 2;
     if (black_only && f.uniform && col_ok(ctx, f) && hx >= 32 && hx <= 512) {
@@ -728,11 +712,7 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
       const int kch = (f.nz + nch - 1) / nch;
       nch = (f.nz + kch - 1) / kch;
       const size_t shm = (size_t)bt * 2 * (sizeof(double) + sizeof(int));
-      if (k == 0 && ctx->kfaces)
-        k_resid_restrict_col<2, true><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(
-            f.dev(), r, z, f.t1, c.nx, ctx->prm.scale, ctx->prm.interp, kch, kfaces_of(ctx));
-      else
-        k_resid_restrict_col<2><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(f.dev(), r, z, f.t1, c.nx, ctx->prm.scale,
+      k_resid_restrict_col<2><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(f.dev(), r, z, f.t1, c.nx, ctx->prm.scale,
                                                                             ctx->prm.interp, kch);
       ctx->launches++;
     } else
@@ -937,11 +917,7 @@ static int op_direction_spmv(mss_ctx* ctx, int k, bool first, const double* z, c
     ProfScope ps(ctx, KC_SPMV, k, cell_bytes(ctx, KC_SPMV, k) * l.N);
     dim3 cgrid;
     int kch = 0;
-    if (k == 0 && ctx->kfaces && col_grid((const void*)k_spmv_col<4, true>, l, &cgrid, &kch)) {
-      k_spmv_col<4, true><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), z, pin, pout, q, ds, first ? 1 : 0,
-                                                                       kch, red_to(ctx, &ds->pq, k, 0), kfaces_of(ctx));
-      ctx->launches++;
-    } else if (l.txp && spmv_tma_ok(ctx, l)) {
+    if (l.txp && spmv_tma_ok(ctx, l)) {
       TRY(spmv_tma_launch(ctx, k, false, first, z, pin, pout, q, red_to(ctx, &ds->pq, k, 0)));
     } else if (col_ok(ctx, l) && col_grid((const void*)k_spmv_col<4>, l, &cgrid, &kch)) {
       k_spmv_col<4><<<cgrid, dim3(kColX, kColY), 0, ctx->stream>>>(l.dev(), z, pin, pout, q, ds, first ? 1 : 0, kch,
@@ -972,13 +948,21 @@ static int op_update_norm(mss_ctx* ctx, int k, double* x, double* r, const doubl
 
 // PCG on level k; on entry r_k holds the residual of the current x_k (x_k = 0 and
 // r_k = b_k for k > 0).  Level thresholds are precomputed in l.thr.
+// level-tree event (k_ev_push) from the host-driven loop, in stream order
+static int ev_host(mss_ctx* ctx, int k, int leave, int64_t it) {
+  if (!ctx->d_ev) return MSS_OK;
+  LAUNCH(k_ev_push, 1, ctx->d_ev, ctx->ev_cap, k, leave, (long long)it);
+  return MSS_OK;
+}
+
 static int pcg_level(mss_ctx* ctx, int k) {
   Level& l = ctx->lv[k];
   Scal* ds = ctx->dscal + k;
   ctx->info.calls[k] += 1;
+  TRY(ev_host(ctx, k, 0, 0));
   TRY(op_dot(ctx, k, l.N, l.r, l.r, &ds->rr));
   TRY(read_scal(ctx, k));
-  if (ctx->hscal[k].rr < l.thr) return MSS_OK;
+  if (ctx->hscal[k].rr < l.thr) return ev_host(ctx, k, 1, 0);
   int64_t it = 0;
   for (;;) {
     TRY(k == 0 ? apply_precond0(ctx) : precond(ctx, k));                 // z = M r, rho = r.z
@@ -993,6 +977,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
     if (!(h.rho > 0.0) || !(h.pq > 0.0) || !std::isfinite(h.rr)) {
       ctx->info.iters[k] += it;
       ctx->info.breakdown_level = k;
+      ev_host(ctx, k, 1, it);
       return set_err(MSS_EBREAKDOWN, "PCG breakdown (rho or pAp <= 0, or non-finite residual) at level " +
                                          std::to_string(k));
     }
@@ -1003,7 +988,7 @@ static int pcg_level(mss_ctx* ctx, int k) {
     }
   }
   ctx->info.iters[k] += it;
-  return MSS_OK;
+  return ev_host(ctx, k, 1, it);
 }
 
 // ============================================================================ device-resident control (a12)
@@ -1083,25 +1068,25 @@ static int pcg_graph(mss_ctx* ctx, int k) {
   CK(cudaGraphConditionalHandleCreate(&hi, ctx->cap_top, 0, 0));
   const int64_t la = ctx->launches, nested0 = ctx->g_nested_launches;
   TRY(op_dot(ctx, k, l.N, l.r, l.r, &ds->rr));
-  k_pcg_enter<<<1, 1, 0, ctx->stream>>>(c, ds, flags, h0);
+  k_pcg_enter<<<1, 1, 0, ctx->stream>>>(c, ds, flags, h0, k, ctx->d_ev, ctx->ev_cap);
   ctx->launches++;
   ctx->g_per_call[k] = ctx->launches - la;
   const long long mi = ctx->prm.max_iter;
   const int rc = cap_cond(ctx, h0, cudaGraphCondTypeIf, [&]() -> int {
     TRY(pcg_iteration(ctx, k, true));
-    k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hw, 1);
+    k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hw, 1, ctx->d_ev, ctx->ev_cap);
     ctx->launches++;
     return cap_cond(ctx, hw, cudaGraphCondTypeWhile, [&]() -> int {
       const int64_t lb = ctx->launches;
       const int64_t nb = ctx->g_nested_launches;
       TRY(pcg_iteration(ctx, k, false));
-      k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hi, 2);
+      k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hi, 2, ctx->d_ev, ctx->ev_cap);
       ctx->launches++;
       // launches of one iteration of this level alone (nested host-driven levels count their own)
       ctx->g_per_iter[k] = (ctx->launches - lb) - (ctx->g_nested_launches - nb);
       return cap_cond(ctx, hi, cudaGraphCondTypeIf, [&]() -> int {
         TRY(pcg_iteration(ctx, k, false));
-        k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hw, 1);
+        k_pcg_check<<<1, 1, 0, ctx->stream>>>(c, ds, k, mi, flags, hw, hw, 1, ctx->d_ev, ctx->ev_cap);
         ctx->launches++;
         return MSS_OK;
       });
@@ -1262,6 +1247,7 @@ static double cell_volume(const mss_ctx* ctx) {
 
 static int solve_impl(mss_ctx* ctx, const double* f, double* x, double rel_tol) {
   reset_info(ctx);
+  if (ctx->d_ev) CK(cudaMemsetAsync(ctx->d_ev, 0, sizeof(int) * 2, ctx->stream));
   const int64_t launches0 = ctx->launches;
   Level& l = ctx->lv[0];
   Scal* ds = ctx->dscal;
@@ -1392,6 +1378,104 @@ static int build_geometric_dims(int ndim, const int64_t n[3], int s, int depth, 
   return MSS_OK;
 }
 
+// NEXT-2 automatic semi-coarsening (mirrors the oracle's aspect_step / aspect_hierarchy_dims,
+// reading A1): each level coarsens the axis of smallest effective length e_d by s
+// and every other axis towards the same coarse length E = s min_d e_d, factor
+// t_d = max(1, E / e_d): integer = the divisor q <= s of n_d nearest t_d in log (ties: the
+// larger), else n'_d = round(n_d / t_d).
+static int build_aspect_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min, const double e0[3],
+                             bool integer, std::vector<std::array<int64_t, 3>>& dims) {
+  std::array<int64_t, 3> cur = {n[0], n[1], ndim == 3 ? n[2] : 1};
+  double e[3] = {e0[0], e0[1], e0[2]};
+  dims.push_back(cur);
+  for (;;) {
+    const int64_t N = cur[0] * cur[1] * cur[2];
+    if (depth >= 0) {
+      if ((int)dims.size() - 1 >= depth) break;
+    } else if (N <= coarse_min) {
+      break;
+    }
+    double emin = INFINITY;
+    for (int d = 0; d < ndim; ++d)
+      if (cur[d] > 1) emin = std::min(emin, e[d]);
+    std::array<int64_t, 3> nxt = cur;
+    if (std::isfinite(emin)) {
+      const double E = s * emin;
+      for (int d = 0; d < ndim; ++d) {
+        if (cur[d] <= 1) continue;
+        const double t = std::max(1.0, E / e[d]);
+        if (integer) {
+          int64_t best = 1;
+          double bd = -1.0;
+          for (int64_t q = 1; q <= std::min<int64_t>(s, cur[d]); ++q) {
+            if (cur[d] % q) continue;
+            const double dq = std::fabs(std::log((double)q) - std::log(t));
+            if (bd < 0 || dq < bd - 1e-12 || std::fabs(dq - bd) <= 1e-12) {
+              best = q;
+              bd = dq;
+            }
+          }
+          nxt[d] = cur[d] / best;
+        } else {
+          nxt[d] = std::max<int64_t>(1, round_half_up((double)cur[d] / t));
+        }
+      }
+    }
+    if (nxt == cur) {
+      if (depth >= 0) return set_err(MSS_EINVAL, "explicit depth deeper than the aspect rule can coarsen");
+      break;
+    }
+    if ((int)dims.size() >= MSS_MAX_LEVELS) return set_err(MSS_EINVAL, "too many levels");
+    for (int d = 0; d < ndim; ++d) e[d] = e[d] * (double)cur[d] / (double)nxt[d];
+    cur = nxt;
+    dims.push_back(cur);
+  }
+  return MSS_OK;
+}
+
+// e_d = sqrt(V / Tg_d), Tg_d the geometric mean of the level-0 interior d-face T (oracle
+// effective_lengths); inf for an axis of one cell.
+static int effective_lengths(mss_ctx* ctx, const int64_t n[3], const double* K, int k_comp, double e[3]) {
+  const int ndim = ctx->ndim;
+  const int64_t nn[3] = {n[0], n[1], ndim == 3 ? n[2] : 1};
+  const int64_t N = nn[0] * nn[1] * nn[2];
+  double h[3], V = 1.0;
+  for (int d = 0; d < 3; ++d) {
+    h[d] = ctx->extent[d] / (double)nn[d];
+    if (d < ndim) V *= h[d];
+  }
+  const int G = 4 * kSMs;
+  double* part = nullptr;
+  CK(cudaMalloc(&part, sizeof(double) * G));
+  std::vector<double> hp(G);
+  int rc = MSS_OK;
+  for (int d = 0; d < 3; ++d) {
+    e[d] = INFINITY;
+    if (d >= ndim || nn[d] <= 1) continue;
+    double area = 1.0;
+    for (int q = 0; q < ndim; ++q)
+      if (q != d) area *= h[q];
+    const double coef = area / h[d];
+    const double* Kd = K + (size_t)((k_comp == ndim) ? d : 0) * N;
+    k_logT_partial<<<G, 256, 0, ctx->stream>>>(Kd, (int)nn[0], (int)nn[1], (int)nn[2], d, coef, part);
+    if (cudaMemcpyAsync(hp.data(), part, sizeof(double) * G, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+      rc = set_err(MSS_ECUDA, "effective lengths");
+      break;
+    }
+    double sum = 0.0;
+    for (int b = 0; b < G; ++b) sum += hp[b];
+    const double M = (double)(nn[d] - 1) * (double)(N / nn[d]);
+    e[d] = std::sqrt(V / std::exp(sum / M));
+    if (!std::isfinite(e[d])) {
+      rc = set_err(MSS_EINVAL, "K must be finite and > 0");
+      break;
+    }
+  }
+  cudaFree(part);
+  return rc;
+}
+
 static int build_hierarchy_dims(int ndim, const int64_t n[3], int s, int depth, int coarse_min,
                                 std::vector<std::array<int64_t, 3>>& dims, const mss_params* prm = nullptr) {
   if (prm && prm->dims_mode == 1) return build_geometric_dims(ndim, n, s, depth, coarse_min, dims);
@@ -1487,7 +1571,16 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   const int ndim = ctx->ndim;
   const int s = ctx->prm.scale;
   std::vector<std::array<int64_t, 3>> dims;
-  TRY(build_hierarchy_dims(ndim, n, s, depth, ctx->prm.coarse_min, dims, &ctx->prm));
+  if (ctx->prm.dims_mode == 3 || ctx->prm.dims_mode == 4) {
+    if (ctx->comm && ctx->comm->size > 1)
+      return set_err(MSS_EINVAL, "automatic semi-coarsening (dims_mode 3/4) needs a single-GPU context");
+    double e[3];
+    TRY(effective_lengths(ctx, n, K, k_comp, e));
+    for (int d = 0; d < 3; ++d) ctx->eff_len[d] = e[d];
+    TRY(build_aspect_dims(ndim, n, s, depth, ctx->prm.coarse_min, e, ctx->prm.dims_mode == 3, dims));
+  } else {
+    TRY(build_hierarchy_dims(ndim, n, s, depth, ctx->prm.coarse_min, dims, &ctx->prm));
+  }
   ctx->L = (int)dims.size() - 1;
   ctx->lv.resize(dims.size());
   // z-slab decomposition: levels with N_k >= gather_below are split into
@@ -1542,6 +1635,20 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
   if (ctx->ndist > 0)
     for (int k = 0; k < ctx->L; ++k)
       if (!ctx->lv[k].uniform) return set_err(MSS_EINVAL, "distributed solves need an integer scale factor");
+  {
+    // L2 residency (LevelDev::l2keep): the first (largest) level whose sweep operands
+    // (faces, r, z) take at most MSS_L2KEEP_MB (default 96 of the 126 MB L2)
+    const char* e = getenv("MSS_L2KEEP_MB");
+    const double budget = (e ? atof(e) : 96.0) * 1048576.0;
+    for (int k = 0; k <= ctx->L; ++k) {
+      Level& l = ctx->lv[k];
+      const double by = 8.0 * (double)l.N * (ndim + 2);
+      if (by <= budget && by >= 4.0 * 1048576.0) {
+        l.l2keep = true;
+        break;
+      }
+    }
+  }
   for (int k = 0; k < ctx->L; ++k) {
     Level& f = ctx->lv[k];
     Level& c = ctx->lv[k + 1];
@@ -1612,23 +1719,6 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaStreamSynchronize(ctx->stream));
       cudaFree(Kext);
     }
-  }
-  // matrix-free level-0 faces (scalar K, 3-D, even n_x): keep a ghosted copy of K
-  ctx->kfaces = false;
-  // opt-in (MSS_KFACES=1): measured slower on B200 (the 6 IEEE divisions per updated cell
-  // make the sweep latency-bound, 1.44 ms vs 0.99 ms per 512^3 half-sweep)
-  if (ndim == 3 && k_comp == 1 && (l0.nx % 2) == 0 && getenv("MSS_KFACES")) {
-    TRY(valloc(ctx, l0, &ctx->kf_K));
-    CK(cudaMemcpyAsync(ctx->kf_K, K, sizeof(double) * l0.N, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (l0.dist) TRY(ctx->comm->halo(ctx->stream, ctx->kf_K, l0.plane, l0.nz, 1));
-    for (int d = 0; d < 3; ++d) {
-      double area = 1.0;
-      for (int e = 0; e < 3; ++e)
-        if (e != d) area *= l0.h[e];
-      ctx->kf_c[d] = area / l0.h[d];
-    }
-    for (int sd = 0; sd < 6; ++sd) ctx->kf_dir[sd] = ctx->bc[sd].kind == 1;
-    ctx->kfaces = true;
   }
   // a2: coarse faces, level by level
   for (int k = 1; k <= ctx->L; ++k) {
@@ -1766,6 +1856,11 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
       CK(cudaFuncSetAttribute(k_spmv_tma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpmvGeo::SMEM));
     }
   }
+  if (ctx->prm.log_events > 0) {
+    ctx->ev_cap = ctx->prm.log_events;
+    TRY(dalloc(ctx, (void**)&ctx->d_ev, sizeof(int) * (2 + 2 * (size_t)ctx->ev_cap)));
+    CK(cudaMemsetAsync(ctx->d_ev, 0, sizeof(int) * 2, ctx->stream));
+  }
   TRY(tail_setup(ctx));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
@@ -1791,6 +1886,7 @@ int mss_default_params(mss_params* p) {
   p->dims_mode = 0;
   p->n_level_dims = 0;
   memset(p->level_dims, 0, sizeof(p->level_dims));
+  p->log_events = 0;
   return MSS_OK;
 }
 
@@ -1833,6 +1929,7 @@ static int setup_common(mss_ctx** out, mss::Comm* comm, int ndim, const int64_t 
   if (prm.interp != 0 && prm.interp != 1) return set_err(MSS_EINVAL, "interp must be 0 or 1");
   if (prm.method < 0 || prm.method > 3) return set_err(MSS_EINVAL, "method must be 0..3");
   if (prm.splitting != 0 && prm.splitting != 1) return set_err(MSS_EINVAL, "splitting must be 0 or 1");
+  if (prm.dims_mode < 0 || prm.dims_mode > 4) return set_err(MSS_EINVAL, "dims_mode must be 0..4");
   bool any_dir = false;
   for (int s = 0; s < 2 * ndim; ++s) {
     if (bc[s].kind != 0 && bc[s].kind != 1) return set_err(MSS_EINVAL, "bad BC kind");
@@ -1989,6 +2086,22 @@ int mss_solve_host_batch(mss_ctx* ctx, int nrhs, const double* const* f_host, do
   }
   CK(cudaStreamSynchronize(cs));
   return worst;
+}
+
+int mss_level_events(const mss_ctx* ctx, int* events, int cap, int* n_events) {
+  if (!ctx || !n_events || (cap > 0 && !events)) return set_err(MSS_EINVAL, "mss_level_events: null argument");
+  *n_events = 0;
+  if (!ctx->d_ev) return MSS_OK;
+  int cnt[2] = {0, 0};
+  CK(cudaMemcpyAsync(cnt, ctx->d_ev, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n_events = cnt[0];
+  const int nc = std::min(std::min(cnt[0], ctx->ev_cap), std::max(cap, 0));
+  if (nc > 0) {
+    CK(cudaMemcpyAsync(events, ctx->d_ev + 2, sizeof(int) * 2 * (size_t)nc, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return MSS_OK;
 }
 
 int mss_get_info(const mss_ctx* ctx, mss_info* info) {

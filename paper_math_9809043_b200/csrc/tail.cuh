@@ -37,6 +37,8 @@ struct TailArgs {
   long long* iters;    // [MSS_MAX_LEVELS]
   long long* calls;    // [MSS_MAX_LEVELS]
   int* flags;          // [0] not converged, [1] breakdown level + 1
+  int* ev;             // level-tree event log (kernels.cuh ev_push), null = off
+  int ev_cap;
   TLevel lv[MSS_MAX_LEVELS];
 };
 
@@ -192,6 +194,7 @@ struct Tail {
     }
     const TLevel& l = A->lv[k];
     count(A->calls, k, 1);
+    if (tid == 0) ev_push(A->ev, A->ev_cap, k, 0, 0);
     double acc = 0.0;
     for (int64_t c = tid; c < l.g.N; c += nth) {
       l.x[c] = 0.0;
@@ -199,7 +202,10 @@ struct Tail {
       acc += rv * rv;
     }
     double rr = sum(acc);
-    if (rr < l.thr) return true;
+    if (rr < l.thr) {
+      if (tid == 0) ev_push(A->ev, A->ev_cap, k, 1, 0);
+      return true;
+    }
     long long it = 0;
     double rho_prev = 1.0;
     int cur = 0;
@@ -216,7 +222,10 @@ struct Tail {
       cur ^= 1;
       if (!(rho > 0.0) || !(pq > 0.0)) {
         count(A->iters, k, it + 1);
-        if (tid == 0) A->flags[1] = k + 1;
+        if (tid == 0) {
+          A->flags[1] = k + 1;
+          ev_push(A->ev, A->ev_cap, k, 1, it + 1);
+        }
         return false;
       }
       const double alpha = rho / pq;
@@ -232,6 +241,7 @@ struct Tail {
       }
     }
     count(A->iters, k, it);
+    if (tid == 0) ev_push(A->ev, A->ev_cap, k, 1, it);
     return true;
   }
 };
@@ -344,6 +354,8 @@ static int tail_prepare(mss_ctx* ctx, int k) {
     a.iters = ctx->tail_cnt;
     a.calls = ctx->tail_cnt + MSS_MAX_LEVELS;
     a.flags = ctx->tail_flags;
+    a.ev = ctx->d_ev;
+    a.ev_cap = ctx->ev_cap;
     for (int q = 0; q <= ctx->L; ++q) {
       const mss::Level& l = ctx->lv[q];
       mss::TLevel& t = a.lv[q];

@@ -30,6 +30,7 @@ namespace mss {
 
 constexpr int kTsThreads = 512;
 constexpr int kTsMaxLv = 8;
+constexpr int kTsU = 2;      // cells per thread whose loads are issued together (sweep, SpMV)
 
 // Unsigned division by a runtime constant as multiply-high + shift (valid for n < 2^31):
 // the tail's index decoding was instruction-bound on IMAD/IABS division sequences.
@@ -71,11 +72,12 @@ struct TsArgs {
   long long* iters;     // [MSS_MAX_LEVELS]
   long long* calls;
   int* flags;
+  int* ev;              // level-tree event log (kernels.cuh ev_push), null = off
+  int ev_cap;
   long long* phase_cyc; // optional [16] per-phase clock64 totals (CTA 0 thread 0), null = off
   int o_rfull;          // replicated full r_L (NL doubles)
   int o_red;            // reduction scratch (40 doubles)
   int smem_doubles;
-  int nbsync;           // 1: non-dot half-sweeps end with a neighbour-only sync (MSS_TAIL_NBSYNC)
   TsLevel lv[kTsMaxLv]; // index = level - L0
 };
 
@@ -89,11 +91,8 @@ struct TailSm {
   int rank, cs;
   int phase;
   long long tmark;
-  unsigned* nbf;    // [0]: phase counter written by CTA rank-1, [1]: by CTA rank+1
-  unsigned nbph;    // neighbour-sync phases completed (thread 0)
 
-  __device__ TailSm(const TsArgs* a, double* s, unsigned* nb)
-      : A(a), cl(cg::this_cluster()), sm(s), phase(0), nbf(nb), nbph(0) {
+  __device__ TailSm(const TsArgs* a, double* s) : A(a), cl(cg::this_cluster()), sm(s), phase(0) {
     rank = (int)cl.block_rank();
     cs = (int)cl.num_blocks();
     sm_lo = rank > 0 ? cl.map_shared_rank(sm, rank - 1) : nullptr;
@@ -110,33 +109,6 @@ struct TailSm {
     }
   }
   __device__ __forceinline__ void sync() { cl.sync(); }
-  // A half-sweep reads only the boundary slices of CTAs rank-1 and rank+1, so its end needs
-  // ordering with those two only: after the CTA barrier, thread 0 publishes the phase number
-  // into both neighbours' counters (release, cluster scope) and waits until both neighbours
-  // have published it into its own (acquire).  Counters, not mbarrier parities: a neighbour
-  // may already be one phase ahead (it needs this CTA's store to get further).
-  __device__ __forceinline__ void nb_sync() {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      ++nbph;
-      if (rank > 0) {
-        unsigned* p = cl.map_shared_rank(nbf + 1, rank - 1);
-        asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(p), "r"(nbph) : "memory");
-      }
-      if (rank < cs - 1) {
-        unsigned* p = cl.map_shared_rank(nbf, rank + 1);
-        asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(p), "r"(nbph) : "memory");
-      }
-      for (int side = 0; side < 2; ++side) {
-        if (side == 0 ? rank == 0 : rank == cs - 1) continue;
-        unsigned v;
-        do {
-          asm volatile("ld.acquire.cluster.u32 %0, [%1];" : "=r"(v) : "l"(nbf + side) : "memory");
-        } while (v < nbph);
-      }
-    }
-    __syncthreads();
-  }
   __device__ __forceinline__ const TsLevel& lvl(int q) const { return A->lv[q - A->L0]; }
   __device__ __forceinline__ int olo(const TsLevel& l) const { return min(l.no, rank * l.ppc); }
   __device__ __forceinline__ int ohi(const TsLevel& l) const { return min(l.no, (rank + 1) * l.ppc); }
@@ -149,30 +121,25 @@ struct TailSm {
     return own == rank ? p : cl.map_shared_rank(p, own);
   }
 
-  // cluster-wide sum, identical bits in every CTA
+  // cluster-wide sum, identical bits in every CTA (and every thread): per-warp butterfly,
+  // warp partials combined by a butterfly in every warp, CTA partials likewise after the
+  // cluster barrier (the xor butterfly leaves identical bits in all lanes)
   __device__ double sum(double v) {
     double* red_w = sm + A->o_red;
     double* slot = red_w + 32;
-    double* bc = red_w + 34;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nw = (int)(blockDim.x >> 5);
     v = warp_sum(v);
     if (lane == 0) red_w[w] = v;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red_w[i];
-      slot[phase] = s;
-    }
+    double s = (lane < nw) ? red_w[lane] : 0.0;
+    s = warp_sum(s);
+    if (threadIdx.x == 0) slot[phase] = s;
     sync();
-    if (w == 0) {
-      double pv = (lane < cs) ? *cl.map_shared_rank(&slot[phase], lane) : 0.0;
-      pv = warp_sum(pv);
-      if (lane == 0) *bc = pv;
-    }
-    __syncthreads();
-    const double t = *bc;
+    double pv = (lane < cs) ? *cl.map_shared_rank(&slot[phase], lane) : 0.0;
+    pv = warp_sum(pv);
     phase ^= 1;
-    return t;
+    return pv;
   }
 
   __device__ __forceinline__ void decode(const TsLevel& l, int t, int o0, int& i, int& j, int& k) {
@@ -269,8 +236,42 @@ struct TailSm {
     return s;
   }
 
+  // 3-D form of nbr() without branches (the tail is issue-bound on its per-cell instruction
+  // count, ncu r01j / r02): boundary neighbours are selected to 0 after a load from a clamped
+  // index, a z neighbour in another CTA is read through a selected generic (DSMEM) pointer,
+  // and the expression tree is nbr()'s, so the bits are the same.  kk = k - o0, nloc = o1 - o0.
+  __device__ __forceinline__ double nbr3(const TsLevel& l, int off, int t, int i, int j, int k, int kk, int nloc) {
+    const double* v = sm + off;
+    const double* tx = sm + l.o_tx;
+    const double* ty = sm + l.o_ty;
+    const double* tz = sm + l.o_tz;
+    const int tin = t - kk * l.P;
+    const bool hxl = i > 0, hxh = i < l.nx - 1, hyl = j > 0, hyh = j < l.ny - 1;
+    const bool hzl = k > 0, hzh = k < l.nz - 1;
+    const bool inl = kk > 0, inh = kk < nloc - 1;
+    const double* pzl = inl ? v + t - l.P : (sm_lo ? sm_lo + off + (l.ppc - 1) * l.P + tin : v + t);
+    const double* pzh = inh ? v + t + l.P : (sm_hi ? sm_hi + off + tin : v + t);
+    const double zl0 = *pzl, zh0 = *pzh;
+    const double xl0 = v[hxl ? t - 1 : t], xh0 = v[hxh ? t + 1 : t];
+    const double yl0 = v[hyl ? t - l.nx : t], yh0 = v[hyh ? t + l.nx : t];
+    const double txl = tx[t], txh0 = tx[hxh ? t + 1 : t];
+    const double tyl = ty[t], tyh0 = ty[hyh ? t + l.nx : t];
+    const double tzl = tz[t], tzh0 = inh ? tz[t + l.P] : sm[l.o_tup + tin];
+    const double xl = hxl ? xl0 : 0.0, xh = hxh ? xh0 : 0.0;
+    const double yl = hyl ? yl0 : 0.0, yh = hyh ? yh0 : 0.0;
+    const double zl = hzl ? zl0 : 0.0, zh = hzh ? zh0 : 0.0;
+    const double txh = hxh ? txh0 : 0.0, tyh = hyh ? tyh0 : 0.0, tzh = hzh ? tzh0 : 0.0;
+    double s = txl * xl + txh * xh + tyl * yl + tyh * yh;
+    s += tzl * zl + tzh * zh;
+    return s;
+  }
+
   // ---------------------------------------------------------------- passes
-  // half-sweep of colour col; dot: returns r.z over all local cells (cluster-summed)
+  // half-sweep of colour col; dot: returns r.z over all local cells (cluster-summed).
+  // Each thread takes kTsU pair units per batch and issues every load of the batch before
+  // the first division: a unit reads only cells of the other colour (and its own r, diag),
+  // so no store of the batch feeds a load of it, and the loads overlap (the tail is latency-
+  // bound: ncu r01j).  Per-cell expressions and the per-thread sum order are unchanged.
   __device__ double sweep(int q, int col, bool first, bool dot) {
     const TsLevel l = lvl(q);   // by value: smem stores below cannot alias it
     const int o0 = olo(l), o1 = ohi(l);
@@ -280,31 +281,57 @@ struct TailSm {
     double acc = 0.0;
     double* z = sm + l.o_z;
     const double* r = sm + l.o_r;
-    for (int u = threadIdx.x; u < n; u += blockDim.x) {
-      const int rw = (int)l.f_hx.div((uint32_t)u), mm = u - rw * hx;
-      int j, k;
-      if (NDIM == 3) {
-        const int kk = (int)l.f_ny.div((uint32_t)rw);
-        j = rw - kk * l.ny;
-        k = o0 + kk;
-      } else {
-        j = o0 + rw;
-        k = 0;
+    const int nt = blockDim.x;
+    for (int u0 = threadIdx.x; u0 < n; u0 += kTsU * nt) {
+      double a[kTsU], dg[kTsU], rv[kTsU], ox[kTsU];
+      int tt[kTsU];
+#pragma unroll
+      for (int e = 0; e < kTsU; ++e) {
+        const int u = u0 + e * nt;
+        tt[e] = -1;
+        ox[e] = 0.0;
+        if (u < n) {
+          const int rw = (int)l.f_hx.div((uint32_t)u), mm = u - rw * hx;
+          int j, k;
+          if (NDIM == 3) {
+            const int kk = (int)l.f_ny.div((uint32_t)rw);
+            j = rw - kk * l.ny;
+            k = o0 + kk;
+          } else {
+            j = o0 + rw;
+            k = 0;
+          }
+          const int par = (j + k + col) & 1;
+          const int i = 2 * mm + par;
+          const int base = rw * l.nx;
+          if (NDIM == 3) {
+            // every load unconditional (a clamped cell when i == nx on an odd row): no branch
+            const int ic = min(i, l.nx - 1), t = base + ic;
+            tt[e] = (i < l.nx) ? t : -1;
+            rv[e] = r[t];
+            a[e] = first ? 0.0 : nbr3(l, l.o_z, t, ic, j, k, k - o0, o1 - o0);
+            dg[e] = sm[l.o_dg + t];
+          } else if (i < l.nx) {
+            const int t = base + i;
+            tt[e] = t;
+            rv[e] = r[t];
+            a[e] = first ? 0.0 : nbr(l, l.o_z, t, i, j, k, o0, o1);
+            dg[e] = sm[l.o_dg + t];
+          }
+          if (dot) {
+            const int ip = 2 * mm + 1 - par;
+            if (ip < l.nx) ox[e] = r[base + ip] * z[base + ip];
+          }
+        }
       }
-      const int par = (j + k + col) & 1;
-      const int i = 2 * mm + par;
-      const int base = rw * l.nx;
-      if (i < l.nx) {
-        const int t = base + i;
-        double a = r[t];
-        if (!first) a += nbr(l, l.o_z, t, i, j, k, o0, o1);
-        const double zn = a / sm[l.o_dg + t];
-        z[t] = zn;
-        if (dot) acc += r[t] * zn;
-      }
-      if (dot) {
-        const int ip = 2 * mm + 1 - par;
-        if (ip < l.nx) acc += r[base + ip] * z[base + ip];
+#pragma unroll
+      for (int e = 0; e < kTsU; ++e) {
+        if (tt[e] >= 0) {
+          const double zn = (first ? rv[e] : rv[e] + a[e]) / dg[e];
+          z[tt[e]] = zn;
+          if (dot) acc += rv[e] * zn;
+        }
+        if (dot) acc += ox[e];
       }
     }
     if (dot) {
@@ -312,10 +339,7 @@ struct TailSm {
       mark(0);
       return d;
     }
-    if (A->nbsync)
-      nb_sync();
-    else
-      sync();
+    sync();
     mark(0);
     return 0.0;
   }
@@ -346,7 +370,8 @@ struct TailSm {
         int i, j, k;
         decode(f, t, o0, i, j, k);
         if (((i + j + k) & 1) == 0) continue;
-        sm[f.o_q + t] = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nbr(f, f.o_z, t, i, j, k, o0, o1));
+        const double nb = (NDIM == 3) ? nbr3(f, f.o_z, t, i, j, k, k - o0, o1 - o0) : nbr(f, f.o_z, t, i, j, k, o0, o1);
+        sm[f.o_q + t] = sm[f.o_r + t] - (sm[f.o_dg + t] * sm[f.o_z + t] - nb);
       }
       __syncthreads();
     }
@@ -481,16 +506,19 @@ struct TailSm {
       rf[g] = *at(c.o_r, c.P, c, o, in);
     }
     __syncthreads();
-    const int o0 = olo(c), o1 = ohi(c);
-    const int nl = (o1 - o0) * c.P;
+    // rows are spread evenly over all CTAs (not by plane ownership: the coarsest level
+    // may have fewer planes than the cluster has CTAs); each result goes to its owner
+    const int g0 = (int)(((int64_t)n * rank) / cs), g1 = (int)(((int64_t)n * (rank + 1)) / cs);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int t = w; t < nl; t += nw) {
-      const int row = o0 * c.P + t;
+    for (int row = g0 + w; row < g1; row += nw) {
       const double* a = A->Ainv + (int64_t)row * n;
       double acc = 0.0;
       for (int qq = lane; qq < n; qq += 32) acc += __ldg(a + qq) * rf[qq];
       acc = warp_sum(acc);
-      if (lane == 0) sm[c.o_x + t] = acc;
+      if (lane == 0) {
+        const int o = (int)c.f_P.div((uint32_t)row);
+        *at(c.o_x, c.P, c, o, row - o * c.P) = acc;
+      }
     }
     sync();
     mark(4);
@@ -498,6 +526,9 @@ struct TailSm {
 
   __device__ void count(long long* arr, int k, long long v) {
     if (rank == 0 && threadIdx.x == 0) arr[k] += v;
+  }
+  __device__ void ev(int k, int leave, long long it) {
+    if (rank == 0 && threadIdx.x == 0) ev_push(A->ev, A->ev_cap, k, leave, it);
   }
 
   template <int D>
@@ -530,13 +561,17 @@ struct TailSm {
     double* z = sm + l.o_z;
     double* qv = sm + l.o_q;
     count(A->calls, q, 1);
+    ev(q, 0, 0);
     double acc = 0.0;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       x[t] = 0.0;
       acc += r[t] * r[t];
     }
     double rr = sum(acc);
-    if (rr < l.thr) return true;
+    if (rr < l.thr) {
+      ev(q, 1, 0);
+      return true;
+    }
     long long it = 0;
     double rho_prev = 1.0;
     int cur = 0;
@@ -552,13 +587,29 @@ struct TailSm {
       for (int t = threadIdx.x; t < n; t += blockDim.x) po[t] = (it == 0) ? z[t] : z[t] + beta * pi[t];
       sync();
       mark(6);
-      for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        int i, j, k;
-        decode(l, t, o0, i, j, k);
-        const double pc = po[t];
-        const double qc = sm[l.o_dg + t] * pc - nbr(l, off_out, t, i, j, k, o0, o1);
-        qv[t] = qc;
-        acc += pc * qc;
+      // batched like sweep(): all loads of kTsU cells before their stores
+      for (int t0 = threadIdx.x; t0 < n; t0 += kTsU * (int)blockDim.x) {
+        double pcv[kTsU], dgv[kTsU], nbv[kTsU];
+#pragma unroll
+        for (int e = 0; e < kTsU; ++e) {
+          const int t = t0 + e * (int)blockDim.x;
+          if (t < n) {
+            int i, j, k;
+            decode(l, t, o0, i, j, k);
+            pcv[e] = po[t];
+            dgv[e] = sm[l.o_dg + t];
+            nbv[e] = (NDIM == 3) ? nbr3(l, off_out, t, i, j, k, k - o0, o1 - o0) : nbr(l, off_out, t, i, j, k, o0, o1);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < kTsU; ++e) {
+          const int t = t0 + e * (int)blockDim.x;
+          if (t < n) {
+            const double qc = dgv[e] * pcv[e] - nbv[e];
+            qv[t] = qc;
+            acc += pcv[e] * qc;
+          }
+        }
       }
       const double pq = sum(acc);
       mark(7);
@@ -566,6 +617,7 @@ struct TailSm {
       if (!(rho > 0.0) || !(pq > 0.0)) {
         count(A->iters, q, it + 1);
         if (rank == 0 && threadIdx.x == 0) A->flags[1] = q + 1;
+        ev(q, 1, it + 1);
         return false;
       }
       const double alpha = rho / pq;
@@ -587,6 +639,7 @@ struct TailSm {
       }
     }
     count(A->iters, q, it);
+    ev(q, 1, it);
     return true;
   }
 };
@@ -614,9 +667,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
     __syncthreads();
   }
   const TsArgs* A = &As;
-  __shared__ unsigned nbflag[2];
-  if (threadIdx.x < 2) nbflag[threadIdx.x] = 0u;   // published by the cluster barrier below
-  TailSm<NDIM> T(A, sm_dyn, nbflag);
+  TailSm<NDIM> T(A, sm_dyn);
   // stage faces and weight tables of every PCG level, and the top level's residual
   for (int q = A->L0; q < A->L; ++q) T.stage(q);
   {
@@ -687,7 +738,6 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
   a.s = ctx->prm.scale;
   a.interp = ctx->prm.interp;
   a.max_iter = ctx->prm.max_iter;
-  a.nbsync = ctx->kn.tail_nbsync ? 1 : 0;
   a.NL = ctx->NL;
   a.Ainv = ctx->Ainv;
   for (int q = L0; q <= ctx->L; ++q) {
@@ -820,6 +870,8 @@ static int tailsm_upload(mss_ctx* ctx, int k) {
     a.iters = ctx->tail_cnt;
     a.calls = ctx->tail_cnt + MSS_MAX_LEVELS;
     a.flags = ctx->tail_flags;
+    a.ev = ctx->d_ev;
+    a.ev_cap = ctx->ev_cap;
     if (cudaMemcpyAsync(ctx->tsm_d, &a, sizeof(a), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) return MSS_ECUDA;
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return MSS_ECUDA;
     ctx->tsm_dirty = false;

@@ -50,6 +50,7 @@ class Params(ctypes.Structure):
         ("dims_mode", ctypes.c_int),
         ("n_level_dims", ctypes.c_int),
         ("level_dims", (ctypes.c_int64 * 3) * MAX_LEVELS),
+        ("log_events", ctypes.c_int),
     ]
 
 METHODS = {"multiscale": 0, "tatebe": 1, "polynomial": 2, "multigrid": 3}
@@ -100,6 +101,7 @@ SIGNATURES = [
     ("mss_solve_host", ctypes.c_int, [P, P, P, ctypes.c_double, I64P, DP]),
     ("mss_solve_host_batch", ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_double, I64P, DP]),
     ("mss_get_info", ctypes.c_int, [P, ctypes.POINTER(Info)]),
+    ("mss_level_events", ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("mss_get_faces", ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P]),
     ("mss_apply_A", ctypes.c_int, [P, ctypes.c_int, P, P]),
     ("mss_dot", ctypes.c_int, [P, ctypes.c_int, P, P, DP]),
@@ -279,6 +281,7 @@ class Solver:
         self.n_global = (nx, ny, nz)
         depth_arg = -1 if depth is None else int(depth)
         prm = default_params(**(params or {}))
+        self.ev_cap = int(prm.log_events)
         self.z_range = (0, nz)
         if comm is not None:
             rank = comm[2] if comm[0] == "loop" else comm[1]
@@ -340,6 +343,20 @@ class Solver:
     def level_N(self, level: int) -> int:
         d = self.level_dims(level)
         return d[0] * d[1] * d[2]
+
+    def level_events(self):
+        """mss_level_events: the last solve's level tree as the oracle logs it,
+        [(k, "enter"), ..., (k, "leave", iterations), ...] (needs params log_events > 0)."""
+        n = ctypes.c_int()
+        _check(self.lib.mss_level_events(self.ctx, None, 0, ctypes.byref(n)), "mss_level_events", allow_nc=False)
+        cap = min(n.value, self.ev_cap)   # the log keeps the first ev_cap events
+        buf = (ctypes.c_int * (2 * max(cap, 1)))()
+        _check(self.lib.mss_level_events(self.ctx, buf, cap, ctypes.byref(n)), "mss_level_events", allow_nc=False)
+        out = []
+        for i in range(min(cap, n.value)):
+            code, it = buf[2 * i], buf[2 * i + 1]
+            out.append((code >> 1, "enter") if (code & 1) == 0 else (code >> 1, "leave", it))
+        return out, n.value
 
     def info(self) -> SolveReport:
         inf = Info()

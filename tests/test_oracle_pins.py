@@ -742,3 +742,101 @@ def test_P12_solve_matches_dense_non_integer(ndim, n, depth):
         if lv.N <= 600:
             Ad = dense_from_oracle(lv.T, lv.shape)
             assert np.linalg.eigvalsh(Ad).min() > 0
+
+
+# ---------------------------------------------------------------- P14 automatic semi-coarsening
+# Reading A1 of "the coarsening strategy aimed for cells with an aspect ratio of 1",
+# with anisotropic K as the equivalent stretched cells.
+@pytest.mark.parametrize("n,kd", [((16, 8, 4), (1.0, 4.0, 9.0)), ((24, 6, 1), (2.0, 0.5, None))])
+def test_P14_effective_lengths_closed_form(n, kd):
+    """Uniform diagonal K: T_d = K_d V / h_d^2 exactly, so e_d = h_d / sqrt(K_d)."""
+    ndim = 3 if n[2] > 1 else 2
+    shape = O.shape_of(ndim, n)
+    K = np.stack([np.full(shape, kd[d]) for d in range(ndim)])
+    bc = bc_table(ndim, {"x-": (DIRICHLET, 1.0)})
+    T = O.assemble_faces(ndim, n, K, bc)
+    e = O.effective_lengths(ndim, n, T)
+    for d in range(ndim):
+        assert abs(e[d] - (1.0 / n[d]) / math.sqrt(kd[d])) <= 1e-14 * e[d]
+
+
+def test_P14_isotropic_chain_is_the_uniform_chain():
+    """Equal effective lengths: every axis is coarsened by s, the O8 chain (C2, C5 recipes:
+    random isotropic log-normal K, e_d equal to ~1e-3)."""
+    for cfg, n in (("C2", None), ("C5", 64), ("C1", None)):
+        w = make_workload(cfg, n=n)
+        K = np.asarray(w.K)
+        K = K[None] if K.ndim == w.ndim else K
+        e = O.effective_lengths(w.ndim, w.n, O.assemble_faces(w.ndim, w.n, K, w.bc))
+        assert O.aspect_hierarchy_dims(w.n, w.ndim, e, 4, w.depth) == O.hierarchy_dims(w.n, w.ndim, 4, w.depth)
+
+
+def test_P14_anisotropic_chain():
+    """K_x = K_y = 16 K_z: e_x = e_y = e_z / 4, so x and y are coarsened first (by s = 4), z
+    not at all; the coarse cells are then isotropic and the rule coarsens uniformly.  A
+    non-square grid with isotropic K behaves the same way (the cell lengths differ)."""
+    n = (64, 64, 64)
+    shape = O.shape_of(3, n)
+    K = np.stack([np.full(shape, 16.0), np.full(shape, 16.0), np.ones(shape)])
+    bc = bc_table(3, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})
+    e = O.effective_lengths(3, n, O.assemble_faces(3, n, K, bc))
+    assert O.aspect_hierarchy_dims(n, 3, e, 4) == [(64, 64, 64), (16, 16, 64), (4, 4, 16)]
+    n2 = (512, 128, 1)
+    K2 = np.ones(O.shape_of(2, n2))
+    bc2 = bc_table(2, {"x-": (DIRICHLET, 1.0)})
+    e2 = O.effective_lengths(2, n2, O.assemble_faces(2, n2, K2[None], bc2))
+    assert O.aspect_hierarchy_dims(n2, 2, e2, 4) == [(512, 128, 1), (128, 128, 1), (32, 32, 1), (8, 8, 1)]
+
+
+def test_P14_table2_x_chain_from_its_y_chain():
+    """Table 2: a 2000 x 500 grid of 10:1 cells, equivalently square
+    cells with K_yy / K_xx = 100; on our unit box (cells 4:1 the other way) the
+    same e_x / e_y = 10 needs K_yy = 1600 K_xx.  Given the paper's chain on the short axis
+    (500, 147, 44, 13, 4), the rule "coarsen the other axis to the same effective length"
+    (non-integer) reproduces its long-axis chain 2000, 2000, 1760, 520, 160."""
+    rows = [r for r in _read("table2.csv") if r[0] != "total"]
+    rows = sorted(rows, key=lambda r: int(r[0]))
+    nx_p = [int(r[1]) for r in rows]
+    ny_p = [int(r[2]) for r in rows]
+    n = (nx_p[0], ny_p[0], 1)
+    shape = O.shape_of(2, n)
+    K = np.stack([np.ones(shape), np.full(shape, 1600.0)])
+    bc = bc_table(2, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})
+    e = O.effective_lengths(2, n, O.assemble_faces(2, n, K, bc))
+    assert abs(e[0] / e[1] - 10.0) < 1e-12
+    cur = n
+    chain = [cur[0]]
+    for y in ny_p[1:]:
+        E = e[1] * cur[1] / y             # the short axis' next effective length
+        cur, e = O.aspect_step(cur, e, E, 2, 4, integer=False)
+        assert cur[1] == y
+        chain.append(cur[0])
+    assert chain == nx_p == [2000, 2000, 1760, 520, 160]
+
+
+def test_P14_integer_rule_picks_log_nearest_divisor():
+    cur, e = O.aspect_step((128, 128, 128), [1.0, 1.0, 3.17], 4.0, 3, 4)
+    assert cur == (32, 32, 128)
+    cur, e = O.aspect_step(cur, e, 4.0 * 3.17, 3, 4)     # targets 3.17 (x, y) and 4 (z)
+    assert cur == (8, 8, 32)
+    cur, _ = O.aspect_step((36, 7, 1), [1.0, 1.5, math.inf], 4.0, 2, 4)   # 7: no divisor but 1
+    assert cur == (9, 7, 1)                                               # t_y = 2.67 -> 1
+
+
+def test_P14_aspect_solve_matches_dense():
+    """A semi-coarsened hierarchy is still a preconditioner of the same A: the solve
+    converges to the dense solution (strongly anisotropic K on 16 x 16 x 8)."""
+    rng = np.random.default_rng(3)
+    n = (16, 16, 8)
+    shape = O.shape_of(3, n)
+    g = rng.standard_normal(shape)
+    K = np.stack([16.0 * np.exp(g), 16.0 * np.exp(g), np.exp(g)])
+    bc = bc_table(3, {"x-": (DIRICHLET, 1.0), "x+": (DIRICHLET, 0.0)})
+    f = rng.uniform(-1, 1, shape)
+    o = O.MultiScaleOracle(3, n, K, bc, dims_mode="aspect", coarse_min=16)
+    assert o.dims[1] == (4, 4, 8)
+    x, info = o.solve(f, 1e-10)
+    A = o.dense_operator(0)
+    b = O.rhs(3, n, o.levels[0].T, f, bc)
+    xd = np.linalg.solve(A, b.ravel())
+    assert np.linalg.norm(x.ravel() - xd) <= 1e-8 * np.linalg.norm(xd)
