@@ -1101,7 +1101,10 @@ static bool graph_eligible(const mss_ctx* ctx) {
   if (ctx->graph_knob == 0 || ctx->graph_failed || ctx->prof_on || ctx->L < 1) return false;
   if (ctx->prm.method != 0 || ctx->prm.splitting != 0) return false;
   if (ctx->loop_group) return false;                                    // host-barrier transport
-  if (ctx->comm && ctx->comm->size > 1 && ctx->graph_knob < 2) return false;
+  // NCCL z-slab contexts capture their collectives with the rest (every rank captures the
+  // same sequence and takes the same device-side decisions: the CG scalars are allgathered
+  // and summed in a fixed order, identical bits on every rank); a failed capture falls back
+  // to the host loop.  MSS_GRAPH=0 forces the host loop.
   return true;
 }
 

@@ -21,6 +21,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -75,6 +76,8 @@ struct TsArgs {
   int* ev;              // level-tree event log (kernels.cuh ev_push), null = off
   int ev_cap;
   long long* phase_cyc; // optional [16] per-phase clock64 totals (CTA 0 thread 0), null = off
+  int ct;               // 3-D top level with compile-time dims (sweep_ct): 0 none, 1 = 32x32 with
+                        // 2 planes per CTA, 2 = 16x16 x 1, 3 = 16x16 x 2
   int o_rfull;          // replicated full r_L (NL doubles)
   int o_red;            // reduction scratch (40 doubles)
   int smem_doubles;
@@ -266,6 +269,174 @@ struct TailSm {
     return s;
   }
 
+  // ------------------------------------------------ compile-time-dims passes (top tail level)
+  // The tail is issue-bound (ncu r02e: 38 % issue-active, >50 % of the instructions integer
+  // address arithmetic).  For the top tail level of the common 3-D shapes the x-y dims and
+  // the planes per CTA are template parameters: thread <-> cell-pair position (mm, j) of
+  // every local plane, neighbour offsets are immediates, nothing is decoded per pass.  Same
+  // per-cell expressions as nbr() / sweep(); the per-thread order of the dot partials is the
+  // pair-major one of this mapping.
+  template <int NX, int NY>
+  __device__ __forceinline__ double nbr_ct(const TsLevel& l, const double* v, const double* vlo, const double* vhi,
+                                           int t, int tin, int i, int j, int k, int kk, int nloc) {
+    constexpr int P = NX * NY;
+    const double* tx = sm + l.o_tx;
+    const double* ty = sm + l.o_ty;
+    const double* tz = sm + l.o_tz;
+    const bool hxl = i > 0, hxh = i < NX - 1, hyl = j > 0, hyh = j < NY - 1;
+    const bool hzl = k > 0, hzh = k < l.nz - 1;
+    const bool inh = kk < nloc - 1;
+    const double* pzl = (kk > 0) ? v + t - P : (vlo ? vlo + tin : v + t);
+    const double* pzh = inh ? v + t + P : (vhi ? vhi + tin : v + t);
+    const double zl0 = *pzl, zh0 = *pzh;
+    const double xl0 = v[t - 1], xh0 = v[t + 1], yl0 = v[t - NX], yh0 = v[t + NX];
+    const double txl = tx[t], txh0 = tx[t + 1], tyl = ty[t], tyh0 = ty[t + NX], tzl = tz[t];
+    const double tzh0 = inh ? tz[t + P] : sm[l.o_tup + tin];
+    const double xl = hxl ? xl0 : 0.0, xh = hxh ? xh0 : 0.0;
+    const double yl = hyl ? yl0 : 0.0, yh = hyh ? yh0 : 0.0;
+    const double zl = hzl ? zl0 : 0.0, zh = hzh ? zh0 : 0.0;
+    const double txh = hxh ? txh0 : 0.0, tyh = hyh ? tyh0 : 0.0, tzh = hzh ? tzh0 : 0.0;
+    double s = txl * xl + txh * xh + tyl * yl + tyh * yh;
+    s += tzl * zl + tzh * zh;
+    return s;
+  }
+
+  // half-sweep of colour col (optionally from z = 0 / with the r.z partial); returns the
+  // thread's partial of r.z (DOT)
+  template <int NX, int NY, int PPC, bool FIRST, bool DOT>
+  __device__ double sweep_ct(const TsLevel& l, int col) {
+    constexpr int HX = NX / 2, P = NX * NY, U = HX * NY;
+    const int o0 = olo(l), nloc = ohi(l) - o0;
+    double* z = sm + l.o_z;
+    const double* r = sm + l.o_r;
+    const double* dg = sm + l.o_dg;
+    const double* zlo = sm_lo ? sm_lo + l.o_z + (l.ppc - 1) * P : nullptr;
+    const double* zhi = sm_hi ? sm_hi + l.o_z : nullptr;
+    double acc = 0.0;
+    for (int pos = threadIdx.x; pos < U; pos += blockDim.x) {
+      const int j = pos / HX, mm = pos - (pos / HX) * HX;
+      double a[PPC], rv[PPC], dv[PPC], ox[PPC];
+#pragma unroll
+      for (int kk = 0; kk < PPC; ++kk) {
+        a[kk] = rv[kk] = ox[kk] = 0.0;
+        dv[kk] = 1.0;
+        if (kk < nloc) {
+          const int k = o0 + kk, par = (j + k + col) & 1, i = 2 * mm + par;
+          const int tin = j * NX + i, t = kk * P + tin;
+          rv[kk] = r[t];
+          dv[kk] = dg[t];
+          if (!FIRST) a[kk] = nbr_ct<NX, NY>(l, z, zlo, zhi, t, tin, i, j, k, kk, nloc);
+          if (DOT) {
+            const int tp = t + 1 - 2 * par;   // the pair's other cell (not updated here)
+            ox[kk] = r[tp] * z[tp];
+          }
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < PPC; ++kk) {
+        if (kk < nloc) {
+          const int k = o0 + kk, par = (j + k + col) & 1;
+          const int t = kk * P + j * NX + 2 * mm + par;
+          const double zn = (FIRST ? rv[kk] : rv[kk] + a[kk]) / dv[kk];
+          z[t] = zn;
+          if (DOT) {
+            acc += rv[kk] * zn;
+            acc += ox[kk];
+          }
+        }
+      }
+    }
+    return acc;
+  }
+
+  // q = A p on the local planes (both cells of every pair); returns the thread's p.q partial
+  template <int NX, int NY, int PPC>
+  __device__ double spmv_ct(const TsLevel& l, int off_p, double* qv) {
+    constexpr int HX = NX / 2, P = NX * NY, U = HX * NY;
+    const int o0 = olo(l), nloc = ohi(l) - o0;
+    const double* p = sm + off_p;
+    const double* dg = sm + l.o_dg;
+    const double* plo = sm_lo ? sm_lo + off_p + (l.ppc - 1) * P : nullptr;
+    const double* phi = sm_hi ? sm_hi + off_p : nullptr;
+    double acc = 0.0;
+    for (int pos = threadIdx.x; pos < U; pos += blockDim.x) {
+      const int j = pos / HX, mm = pos - (pos / HX) * HX;
+      double pc[PPC][2], dv[PPC][2], nb[PPC][2];
+#pragma unroll
+      for (int kk = 0; kk < PPC; ++kk) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          pc[kk][b] = dv[kk][b] = nb[kk][b] = 0.0;
+          if (kk < nloc) {
+            const int i = 2 * mm + b, tin = j * NX + i, t = kk * P + tin;
+            pc[kk][b] = p[t];
+            dv[kk][b] = dg[t];
+            nb[kk][b] = nbr_ct<NX, NY>(l, p, plo, phi, t, tin, i, j, o0 + kk, kk, nloc);
+          }
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < PPC; ++kk) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          if (kk < nloc) {
+            const int t = kk * P + j * NX + 2 * mm + b;
+            const double qc = dv[kk][b] * pc[kk][b] - nb[kk][b];
+            qv[t] = qc;
+            acc += pc[kk][b] * qc;
+          }
+        }
+      }
+    }
+    return acc;
+  }
+
+  // black residual s = r - A z into q (resid_restrict pass A0)
+  template <int NX, int NY, int PPC>
+  __device__ void resid_ct(const TsLevel& l) {
+    constexpr int HX = NX / 2, P = NX * NY, U = HX * NY;
+    const int o0 = olo(l), nloc = ohi(l) - o0;
+    const double* z = sm + l.o_z;
+    const double* zlo = sm_lo ? sm_lo + l.o_z + (l.ppc - 1) * P : nullptr;
+    const double* zhi = sm_hi ? sm_hi + l.o_z : nullptr;
+    for (int pos = threadIdx.x; pos < U; pos += blockDim.x) {
+      const int j = pos / HX, mm = pos - (pos / HX) * HX;
+      double res[PPC];
+#pragma unroll
+      for (int kk = 0; kk < PPC; ++kk) {
+        res[kk] = 0.0;
+        if (kk < nloc) {
+          const int k = o0 + kk, par = (j + k + 1) & 1, i = 2 * mm + par;
+          const int tin = j * NX + i, t = kk * P + tin;
+          const double nbv = nbr_ct<NX, NY>(l, z, zlo, zhi, t, tin, i, j, k, kk, nloc);
+          res[kk] = sm[l.o_r + t] - (sm[l.o_dg + t] * z[t] - nbv);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < PPC; ++kk)
+        if (kk < nloc) {
+          const int k = o0 + kk, par = (j + k + 1) & 1;
+          sm[l.o_q + kk * P + j * NX + 2 * mm + par] = res[kk];
+        }
+    }
+  }
+
+  // dispatch on TsArgs::ct (the top tail level only)
+  template <class F>
+  __device__ __forceinline__ bool with_ct(int q, F&& f) {
+    if constexpr (NDIM == 3) {
+      if (q == A->L0) {
+        switch (A->ct) {
+          case 1: f(std::integral_constant<int, 32>(), std::integral_constant<int, 32>(), std::integral_constant<int, 2>()); return true;
+          case 2: f(std::integral_constant<int, 16>(), std::integral_constant<int, 16>(), std::integral_constant<int, 1>()); return true;
+          case 3: f(std::integral_constant<int, 16>(), std::integral_constant<int, 16>(), std::integral_constant<int, 2>()); return true;
+          default: break;
+        }
+      }
+    }
+    return false;
+  }
+
   // ---------------------------------------------------------------- passes
   // half-sweep of colour col; dot: returns r.z over all local cells (cluster-summed).
   // Each thread takes kTsU pair units per batch and issues every load of the batch before
@@ -273,6 +444,26 @@ struct TailSm {
   // so no store of the batch feeds a load of it, and the loads overlap (the tail is latency-
   // bound: ncu r01j).  Per-cell expressions and the per-thread sum order are unchanged.
   __device__ double sweep(int q, int col, bool first, bool dot) {
+    {
+      double acc = 0.0;
+      const bool done = with_ct(q, [&](auto nx_, auto ny_, auto ppc_) {
+        constexpr int X = decltype(nx_)::value, Y = decltype(ny_)::value, Z = decltype(ppc_)::value;
+        const TsLevel& lc = lvl(q);
+        if (first) acc = sweep_ct<X, Y, Z, true, false>(lc, col);
+        else if (dot) acc = sweep_ct<X, Y, Z, false, true>(lc, col);
+        else acc = sweep_ct<X, Y, Z, false, false>(lc, col);
+      });
+      if (done) {
+        if (dot) {
+          const double d = sum(acc);
+          mark(0);
+          return d;
+        }
+        sync();
+        mark(0);
+        return 0.0;
+      }
+    }
     const TsLevel l = lvl(q);   // by value: smem stores below cannot alias it
     const int o0 = olo(l), o1 = ohi(l);
     const int hx = l.hx;
@@ -365,7 +556,9 @@ struct TailSm {
     {
       // pass A0: the black residual of every local cell, once, into the level's q array
       // (dead during the preconditioner); the x-windows below overlap 3-fold
-      const int nl = (o1 - o0) * f.P;
+      const int nl = with_ct(q, [&](auto nx_, auto ny_, auto ppc_) {
+        resid_ct<decltype(nx_)::value, decltype(ny_)::value, decltype(ppc_)::value>(lvl(q));
+      }) ? 0 : (o1 - o0) * f.P;
       for (int t = threadIdx.x; t < nl; t += blockDim.x) {
         int i, j, k;
         decode(f, t, o0, i, j, k);
@@ -588,7 +781,10 @@ struct TailSm {
       sync();
       mark(6);
       // batched like sweep(): all loads of kTsU cells before their stores
-      for (int t0 = threadIdx.x; t0 < n; t0 += kTsU * (int)blockDim.x) {
+      const int nsp = with_ct(q, [&](auto nx_, auto ny_, auto ppc_) {
+        acc = spmv_ct<decltype(nx_)::value, decltype(ny_)::value, decltype(ppc_)::value>(lvl(q), off_out, qv);
+      }) ? 0 : n;
+      for (int t0 = threadIdx.x; t0 < nsp; t0 += kTsU * (int)blockDim.x) {
         double pcv[kTsU], dgv[kTsU], nbv[kTsU];
 #pragma unroll
         for (int e = 0; e < kTsU; ++e) {
@@ -779,6 +975,14 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
       t.gwx = t.gwy = t.gwz = nullptr;
       t.t1_slice = t.t2_slice = 0;
     }
+  }
+  a.ct = 0;
+  if (nd == 3 && L0 < ctx->L) {
+    const TsLevel& t0 = a.lv[0];
+    if (t0.nx == 32 && t0.ny == 32 && t0.ppc == 2) a.ct = 1;
+    else if (t0.nx == 16 && t0.ny == 16 && t0.ppc == 1) a.ct = 2;
+    else if (t0.nx == 16 && t0.ny == 16 && t0.ppc == 2) a.ct = 3;
+    if (getenv("MSS_TAIL_CT") && atoi(getenv("MSS_TAIL_CT")) == 0) a.ct = 0;
   }
   a.o_rfull = off; off += ctx->NL;
   a.o_red = off; off += 40;
