@@ -177,16 +177,17 @@ struct TailSm {
         t4 = l.Tz[c];
         t5 = l.Tz[c + (int64_t)l.P];
       }
-      sm[l.o_tx + t] = t0;
-      sm[l.o_ty + t] = t2;
-      sm[l.o_tz + t] = t4;
+      const int ts = store_idx(q, l, t, o0);
+      sm[l.o_tx + ts] = t0;
+      sm[l.o_ty + ts] = t2;
+      sm[l.o_tz + ts] = t4;
       // the top local slice's upper faces along the outer axis (z in 3-D, y in 2-D): read
       // from HBM once here instead of from the next CTA's shared memory in every pass
       const int o = (NDIM == 3) ? k : j;
-      if (o == o1 - 1) sm[l.o_tup + t - (o1 - 1 - o0) * l.P] = (NDIM == 3) ? t5 : t3;
+      if (o == o1 - 1) sm[l.o_tup + ts - (o1 - 1 - o0) * l.P] = (NDIM == 3) ? t5 : t3;
       double d = t0 + t1 + t2 + t3;
       if (NDIM == 3) d += t4 + t5;
-      sm[l.o_dg + t] = d;
+      sm[l.o_dg + ts] = d;
     }
     // 1-D transfer weight tables
     W1* wx = reinterpret_cast<W1*>(sm + l.o_wx);
@@ -271,27 +272,41 @@ struct TailSm {
 
   // ------------------------------------------------ compile-time-dims passes (top tail level)
   // The tail is issue-bound (ncu r02e: 38 % issue-active, >50 % of the instructions integer
-  // address arithmetic).  For the top tail level of the common 3-D shapes the x-y dims and
-  // the planes per CTA are template parameters: thread <-> cell-pair position (mm, j) of
-  // every local plane, neighbour offsets are immediates, nothing is decoded per pass.  Same
+  // address arithmetic) and shared-memory-bound (a colour's cells at stride 2 move twice the
+  // wavefronts they use).  For the top tail level of the common 3-D shapes (followed directly
+  // by the coarsest level) the x-y dims and the planes per CTA are template parameters and the
+  // level's shared arrays are colour-split by row: row (j, k) holds its colour-0 cells, then its
+  // colour-1 cells, cell i at column (i >> 1) of its colour's half (sidx).  Thread <-> cell-pair
+  // column m of row j of every local plane; every neighbour of a colour-c cell is a colour-(1-c)
+  // cell at column m (y, z) or m - 1 + par, m + par (x), so warp loads are contiguous.  Same
   // per-cell expressions as nbr() / sweep(); the per-thread order of the dot partials is the
   // pair-major one of this mapping.
+  // sum_f T_f v_nbr for the colour-c cell at column m, row j, plane k (local kk); par = its
+  // x parity (i = 2m + par); v / vlo / vhi: the array and the neighbour CTAs' copies of it
   template <int NX, int NY>
   __device__ __forceinline__ double nbr_ct(const TsLevel& l, const double* v, const double* vlo, const double* vhi,
-                                           int t, int tin, int i, int j, int k, int kk, int nloc) {
-    constexpr int P = NX * NY;
+                                           int m, int par, int c, int j, int k, int kk, int nloc) {
+    constexpr int HX = NX / 2, P = NX * NY;
+    const int row = kk * P + j * NX;
+    const int own = row + c * HX + m;                 // the cell itself
+    const int oth = row + (c ^ 1) * HX;               // its row's other colour
+    const int i = 2 * m + par;
     const double* tx = sm + l.o_tx;
     const double* ty = sm + l.o_ty;
     const double* tz = sm + l.o_tz;
     const bool hxl = i > 0, hxh = i < NX - 1, hyl = j > 0, hyh = j < NY - 1;
     const bool hzl = k > 0, hzh = k < l.nz - 1;
     const bool inh = kk < nloc - 1;
-    const double* pzl = (kk > 0) ? v + t - P : (vlo ? vlo + tin : v + t);
-    const double* pzh = inh ? v + t + P : (vhi ? vhi + tin : v + t);
+    const int tin = own - kk * P;                     // in-plane index of the cell
+    const int oin = oth - kk * P + m;                 // in-plane index of the other colour, column m
+    const double* pzl = (kk > 0) ? v + oth + m - P : (vlo ? vlo + oin : v + own);
+    const double* pzh = inh ? v + oth + m + P : (vhi ? vhi + oin : v + own);
     const double zl0 = *pzl, zh0 = *pzh;
-    const double xl0 = v[t - 1], xh0 = v[t + 1], yl0 = v[t - NX], yh0 = v[t + NX];
-    const double txl = tx[t], txh0 = tx[t + 1], tyl = ty[t], tyh0 = ty[t + NX], tzl = tz[t];
-    const double tzh0 = inh ? tz[t + P] : sm[l.o_tup + tin];
+    const double xl0 = v[hxl ? oth + m - 1 + par : own], xh0 = v[hxh ? oth + m + par : own];
+    const double yl0 = v[hyl ? oth + m - NX : own], yh0 = v[hyh ? oth + m + NX : own];
+    const double txl = tx[own], txh0 = tx[hxh ? oth + m + par : own];
+    const double tyl = ty[own], tyh0 = ty[hyh ? oth + m + NX : own];
+    const double tzl = tz[own], tzh0 = inh ? tz[oth + m + P] : sm[l.o_tup + tin];
     const double xl = hxl ? xl0 : 0.0, xh = hxh ? xh0 : 0.0;
     const double yl = hyl ? yl0 : 0.0, yh = hyh ? yh0 : 0.0;
     const double zl = hzl ? zl0 : 0.0, zh = hzh ? zh0 : 0.0;
@@ -312,22 +327,23 @@ struct TailSm {
     const double* dg = sm + l.o_dg;
     const double* zlo = sm_lo ? sm_lo + l.o_z + (l.ppc - 1) * P : nullptr;
     const double* zhi = sm_hi ? sm_hi + l.o_z : nullptr;
+    const int co = col ^ 1;
     double acc = 0.0;
     for (int pos = threadIdx.x; pos < U; pos += blockDim.x) {
-      const int j = pos / HX, mm = pos - (pos / HX) * HX;
+      const int j = pos / HX, m = pos - (pos / HX) * HX;
       double a[PPC], rv[PPC], dv[PPC], ox[PPC];
 #pragma unroll
       for (int kk = 0; kk < PPC; ++kk) {
         a[kk] = rv[kk] = ox[kk] = 0.0;
         dv[kk] = 1.0;
         if (kk < nloc) {
-          const int k = o0 + kk, par = (j + k + col) & 1, i = 2 * mm + par;
-          const int tin = j * NX + i, t = kk * P + tin;
+          const int k = o0 + kk, par = (j + k + col) & 1;
+          const int t = kk * P + j * NX + col * HX + m;
           rv[kk] = r[t];
           dv[kk] = dg[t];
-          if (!FIRST) a[kk] = nbr_ct<NX, NY>(l, z, zlo, zhi, t, tin, i, j, k, kk, nloc);
+          if (!FIRST) a[kk] = nbr_ct<NX, NY>(l, z, zlo, zhi, m, par, col, j, k, kk, nloc);
           if (DOT) {
-            const int tp = t + 1 - 2 * par;   // the pair's other cell (not updated here)
+            const int tp = kk * P + j * NX + co * HX + m;   // the pair's other cell (not updated here)
             ox[kk] = r[tp] * z[tp];
           }
         }
@@ -335,8 +351,7 @@ struct TailSm {
 #pragma unroll
       for (int kk = 0; kk < PPC; ++kk) {
         if (kk < nloc) {
-          const int k = o0 + kk, par = (j + k + col) & 1;
-          const int t = kk * P + j * NX + 2 * mm + par;
+          const int t = kk * P + j * NX + col * HX + m;
           const double zn = (FIRST ? rv[kk] : rv[kk] + a[kk]) / dv[kk];
           z[t] = zn;
           if (DOT) {
@@ -360,30 +375,31 @@ struct TailSm {
     const double* phi = sm_hi ? sm_hi + off_p : nullptr;
     double acc = 0.0;
     for (int pos = threadIdx.x; pos < U; pos += blockDim.x) {
-      const int j = pos / HX, mm = pos - (pos / HX) * HX;
+      const int j = pos / HX, m = pos - (pos / HX) * HX;
       double pc[PPC][2], dv[PPC][2], nb[PPC][2];
 #pragma unroll
       for (int kk = 0; kk < PPC; ++kk) {
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          pc[kk][b] = dv[kk][b] = nb[kk][b] = 0.0;
+        for (int c = 0; c < 2; ++c) {
+          pc[kk][c] = dv[kk][c] = nb[kk][c] = 0.0;
           if (kk < nloc) {
-            const int i = 2 * mm + b, tin = j * NX + i, t = kk * P + tin;
-            pc[kk][b] = p[t];
-            dv[kk][b] = dg[t];
-            nb[kk][b] = nbr_ct<NX, NY>(l, p, plo, phi, t, tin, i, j, o0 + kk, kk, nloc);
+            const int k = o0 + kk, par = (j + k + c) & 1;
+            const int t = kk * P + j * NX + c * HX + m;
+            pc[kk][c] = p[t];
+            dv[kk][c] = dg[t];
+            nb[kk][c] = nbr_ct<NX, NY>(l, p, plo, phi, m, par, c, j, k, kk, nloc);
           }
         }
       }
 #pragma unroll
       for (int kk = 0; kk < PPC; ++kk) {
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
+        for (int c = 0; c < 2; ++c) {
           if (kk < nloc) {
-            const int t = kk * P + j * NX + 2 * mm + b;
-            const double qc = dv[kk][b] * pc[kk][b] - nb[kk][b];
+            const int t = kk * P + j * NX + c * HX + m;
+            const double qc = dv[kk][c] * pc[kk][c] - nb[kk][c];
             qv[t] = qc;
-            acc += pc[kk][b] * qc;
+            acc += pc[kk][c] * qc;
           }
         }
       }
@@ -400,25 +416,36 @@ struct TailSm {
     const double* zlo = sm_lo ? sm_lo + l.o_z + (l.ppc - 1) * P : nullptr;
     const double* zhi = sm_hi ? sm_hi + l.o_z : nullptr;
     for (int pos = threadIdx.x; pos < U; pos += blockDim.x) {
-      const int j = pos / HX, mm = pos - (pos / HX) * HX;
+      const int j = pos / HX, m = pos - (pos / HX) * HX;
       double res[PPC];
 #pragma unroll
       for (int kk = 0; kk < PPC; ++kk) {
         res[kk] = 0.0;
         if (kk < nloc) {
-          const int k = o0 + kk, par = (j + k + 1) & 1, i = 2 * mm + par;
-          const int tin = j * NX + i, t = kk * P + tin;
-          const double nbv = nbr_ct<NX, NY>(l, z, zlo, zhi, t, tin, i, j, k, kk, nloc);
+          const int k = o0 + kk, par = (j + k + 1) & 1;
+          const int t = kk * P + j * NX + HX + m;
+          const double nbv = nbr_ct<NX, NY>(l, z, zlo, zhi, m, par, 1, j, k, kk, nloc);
           res[kk] = sm[l.o_r + t] - (sm[l.o_dg + t] * z[t] - nbv);
         }
       }
 #pragma unroll
       for (int kk = 0; kk < PPC; ++kk)
-        if (kk < nloc) {
-          const int k = o0 + kk, par = (j + k + 1) & 1;
-          sm[l.o_q + kk * P + j * NX + 2 * mm + par] = res[kk];
-        }
+        if (kk < nloc) sm[l.o_q + kk * P + j * NX + HX + m] = res[kk];
     }
+  }
+
+  // local cell index of the natural layout -> the level's storage index (colour-split on
+  // the compile-time-dims level, identity elsewhere)
+  __device__ __forceinline__ int store_idx(int q, const TsLevel& l, int t, int o0) {
+    if constexpr (NDIM == 3) {
+      if (q == A->L0 && A->ct) {
+        int i, j, k;
+        decode(l, t, o0, i, j, k);
+        const int kk = k - o0;
+        return kk * l.P + j * l.nx + (((i + j + k) & 1) ? (l.nx >> 1) : 0) + (i >> 1);
+      }
+    }
+    return t;
   }
 
   // dispatch on TsArgs::ct (the top tail level only)
@@ -569,7 +596,9 @@ struct TailSm {
       __syncthreads();
     }
     {
-      // pass A: t1[I, j, (k)] on local outer slices
+      // pass A: t1[I, j, (k)] on local outer slices (the black residuals of a colour-split
+      // level sit in the black half of their row)
+      const bool split = NDIM == 3 && q == A->L0 && A->ct;
       const int per_slice = f.t1_slice;
       const int n = (o1 - o0) * per_slice;
       for (int u = threadIdx.x; u < n; u += blockDim.x) {
@@ -592,7 +621,7 @@ struct TailSm {
           const W1 w1 = wx[i];
           const double w = (w1.I0 == I ? w1.w0 : 0.0) + (w1.I1 == I ? w1.w1 : 0.0);
           if (w == 0.0) continue;
-          acc += w * sm[f.o_q + base + i];
+          acc += w * sm[f.o_q + base + (split ? (f.nx >> 1) + (i >> 1) : i)];
         }
         sm[f.o_t1 + u] = acc;
       }
@@ -683,7 +712,9 @@ struct TailSm {
         acc = ay.w0 * (ax.w0 * Yv(ax.I0, ay.I0) + ax.w1 * Yv(ax.I1, ay.I0)) +
               ay.w1 * (ax.w0 * Yv(ax.I0, ay.I1) + ax.w1 * Yv(ax.I1, ay.I1));
       }
-      sm[f.o_z + rw * f.nx + i] += acc;
+      // colour-split storage on the compile-time-dims level: black half, column i >> 1
+      const int ts = (NDIM == 3 && q == A->L0 && A->ct) ? rw * f.nx + (f.nx >> 1) + (i >> 1) : rw * f.nx + i;
+      sm[f.o_z + ts] += acc;
     }
     sync();
     mark(5);
@@ -870,7 +901,8 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
     const TsLevel& l = T.lvl(A->L0);
     const int o0 = T.olo(l), o1 = T.ohi(l);
     const int n = (o1 - o0) * l.P;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) sm_dyn[l.o_r + t] = A->r_in[(int64_t)o0 * l.P + t];
+    for (int t = threadIdx.x; t < n; t += blockDim.x)
+      sm_dyn[l.o_r + T.store_idx(A->L0, l, t, o0)] = A->r_in[(int64_t)o0 * l.P + t];
   }
   T.sync();
   const bool ok = T.template pcg<D>(A->L0);
@@ -879,7 +911,8 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tailsm(const TsArgs* __restri
     const TsLevel& l = T.lvl(A->L0);
     const int o0 = T.olo(l), o1 = T.ohi(l);
     const int n = (o1 - o0) * l.P;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) A->x_out[(int64_t)o0 * l.P + t] = sm_dyn[l.o_x + t];
+    for (int t = threadIdx.x; t < n; t += blockDim.x)
+      A->x_out[(int64_t)o0 * l.P + t] = sm_dyn[l.o_x + T.store_idx(A->L0, l, t, o0)];
   }
   T.sync();   // keep every CTA's shared memory alive until remote readers are done
 }
@@ -977,7 +1010,7 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
     }
   }
   a.ct = 0;
-  if (nd == 3 && L0 < ctx->L) {
+  if (nd == 3 && L0 + 1 == ctx->L) {   // colour-split storage: the next level is the coarsest
     const TsLevel& t0 = a.lv[0];
     if (t0.nx == 32 && t0.ny == 32 && t0.ppc == 2) a.ct = 1;
     else if (t0.nx == 16 && t0.ny == 16 && t0.ppc == 1) a.ct = 2;
