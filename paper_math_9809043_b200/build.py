@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "--split-compile", "0",  # one translation unit: let nvcc optimise its kernels in parallel
            "-I", os.path.join(ROOT, "include")]
     inc, lib = _nccl_paths()
     if inc:
