@@ -66,6 +66,7 @@ struct Level {
   double *x = nullptr, *r = nullptr, *z = nullptr, *q = nullptr, *b = nullptr, *s = nullptr;
   double *p[2] = {nullptr, nullptr};
   double *t1 = nullptr, *t2 = nullptr;   // restriction temporaries (to level+1); t2 has 2 ghost planes
+  bool w4 = false;                       // the tables have the scale-4 two-neighbour structure on all axes (k_restrict_black_xyz)
   void* w[3] = {nullptr, nullptr, nullptr};  // 1-D transfer weight tables (mss::W1) per axis, to level+1
   int pcur = 0;
   double thr = 0;                          // N_k f^k eps^2 for the current solve
@@ -159,6 +160,8 @@ struct mss_ctx {
     bool spmv_tma = true;     // MSS_SPMV_TMA
     int spmv_nch = 0;         // MSS_SPMV_NCH: 0 cost model
     bool fused_resid = true;  // MSS_FUSED_RESID
+    bool restrict_xyz = true; // MSS_RESTRICT_XYZ: x, y, z restriction of the stored black residual in one pass
+    int rxyz_kc = 0;          // MSS_RXYZ_KC: coarse planes per CTA of that pass (0 = 16)
     bool prolong_pairs = true;// MSS_PROLONG_PAIRS
     bool fused_prolong = false;// MSS_FUSED_PROLONG: a8 inside the first post-smoothing TMA pair
   } kn;

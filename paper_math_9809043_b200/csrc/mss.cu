@@ -363,6 +363,8 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.spmv_tma = geti("MSS_SPMV_TMA", 1) != 0;
   ctx->kn.spmv_nch = geti("MSS_SPMV_NCH", 0);
   ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
+  ctx->kn.restrict_xyz = geti("MSS_RESTRICT_XYZ", 1) != 0;
+  ctx->kn.rxyz_kc = geti("MSS_RXYZ_KC", 0);
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
   ctx->kn.fused_prolong = geti("MSS_FUSED_PROLONG", 0) != 0;
   ctx->graph_knob = geti("MSS_GRAPH", 1);
@@ -809,6 +811,22 @@ static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
     std::swap(l.z, l.s);
     ctx->nswap++;
     tail_mark_dirty(ctx);
+  }
+  if (l.w4 && ctx->kn.restrict_xyz && l.nx / 2 <= 512 && l.w[1] && l.w[2] && c.ny <= 65535) {
+    // x, y and z in one pass over the stored black residual
+    ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.N);
+    int kc = ctx->kn.rxyz_kc > 0 ? ctx->kn.rxyz_kc : 16;
+    kc = std::max(1, std::min(std::min(kc, mss::kRxyzMaxKc), c.nz));
+    const int bt = (l.nx / 2 + 31) / 32 * 32;
+    const dim3 xg(c.ny, (c.nz + kc - 1) / kc);
+    const W1 *w0 = reinterpret_cast<const W1*>(l.w[0]), *w1 = reinterpret_cast<const W1*>(l.w[1]),
+             *w2 = reinterpret_cast<const W1*>(l.w[2]);
+    if (bt <= 256)
+      k_restrict_black_xyz<256><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+    else
+      k_restrict_black_xyz<512><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+    ctx->launches++;
+    return MSS_OK;
   }
   {
     ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.nx * l.ny * l.nz);
@@ -1670,12 +1688,17 @@ static int setup_impl(mss_ctx* ctx, const int64_t n[3], const double* K, int k_c
     Level& f = ctx->lv[k];
     Level& c = ctx->lv[k + 1];
     const int nf[3] = {f.nx, f.ny, f.nz}, ncs[3] = {c.nx, c.ny, c.nz};
+    f.w4 = ndim == 3;
     for (int d = 0; d < ndim; ++d) {
       std::vector<W1> tab(nf[d]);
+      if (nf[d] != 4 * ncs[d]) f.w4 = false;
       for (int i = 0; i < nf[d]; ++i) {
         W1& e = tab[i];
         interp_host(i, ncs[d], (double)nf[d] / ncs[d], ctx->prm.interp, e.I0, e.w0, e.I1, e.w1);
         if (e.I1 == e.I0) e.w1 = 0.0;
+        // fine index 4m+o only reaches coarse {m-1, m} (o < 2) or {m, m+1} (o >= 2)
+        const int m = i >> 2, lo = (i & 3) < 2 ? m - 1 : m;
+        if (e.I0 < lo || e.I0 > lo + 1 || (e.I1 != e.I0 && (e.I1 < lo || e.I1 > lo + 1))) f.w4 = false;
       }
       TRY(dalloc(ctx, &f.w[d], sizeof(W1) * tab.size()));
       CK(cudaMemcpy(f.w[d], tab.data(), sizeof(W1) * tab.size(), cudaMemcpyHostToDevice));

@@ -393,6 +393,139 @@ __global__ void __launch_bounds__(128) k_restrict_x_black(LevelDev L, const doub
   }
 }
 
+// a6 after the fused sweep, all three axes in one pass (scale factor 4, R = E^T):
+// coarse[I, J, K] = sum_{i,j,k} wx(i->I) wy(j->J) wz(k->K) resB[pair(i), j, k] over the black
+// cells.  One CTA per coarse row J and chunk of coarse planes; a thread owns one cell pair q
+// of the fine rows and streams the 8 fine rows of J's window plane by plane (coalesced 8 B
+// loads, no shared staging).  The restriction is separable and linear, so y and z are
+// contracted first, per thread, into three rolling coarse-plane accumulators per colour of
+// the pair (plane 4m+o only reaches coarse planes m-1, m, m+1); x is contracted last, once
+// per finished coarse plane: each pair's value times its weight to its own coarse cell
+// q>>1 (a) and to the neighbouring one (b), combined with three shuffles (the warp edges
+// through shared memory).  Fixed summation order, no atomics.  Host-checked precondition
+// (Level::w4): every axis has n = 4 n_c and each fine index 4m+o only has weights to
+// {m-1, m} (o < 2) or {m, m+1} (o >= 2) — true for the linear and the constant E.
+constexpr int kRxyzMaxKc = 32;   // coarse planes per CTA (shared z-weight table)
+template <int BT>
+__global__ void __launch_bounds__(BT, (BT <= 256) ? 3 : 1)
+    k_restrict_black_xyz(LevelDev L, const double* __restrict__ resB, double* __restrict__ coarse, int ncx, int ncy,
+                         int ncz, const W1* __restrict__ wx, const W1* __restrict__ wy, const W1* __restrict__ wz,
+                         int kc) {
+  __shared__ double edgeL[2][32], edgeR[2][32];
+  __shared__ double wys[8];
+  __shared__ int jrs[8];
+  __shared__ double wzs[4 * kRxyzMaxKc + 4][3];   // per fine plane of the chunk: weight to m-1, m, m+1
+  const int hx = L.nx >> 1, ny = L.ny, nz = L.nz;
+  const int q = threadIdx.x, lane = q & 31, wid = q >> 5, nw = (blockDim.x + 31) >> 5;
+  const bool live = q < hx;
+  const int J = blockIdx.x;
+  const int Ka = blockIdx.y * kc, Kb = min(ncz, Ka + kc);
+  const int kbeg = max(0, 4 * Ka - 2), kend = min(nz, 4 * Kb + 2);
+  const int jlo = 4 * J - 2;   // even
+  // y weights of the 8 rows of J's window (0 outside the domain; the row index is clamped)
+  if (q < 8) {
+    const int j = jlo + q;
+    double w = 0.0;
+    if (j >= 0 && j < ny) {
+      const W1 e = wy[j];
+      if (e.I0 == J) w += e.w0;
+      if (e.I1 == J && e.I1 != e.I0) w += e.w1;
+    }
+    wys[q] = w;
+    jrs[q] = hx * min(max(j, 0), ny - 1);   // row offset in pairs
+  }
+  for (int k = kbeg + q; k < kend; k += blockDim.x) {
+    const int m = k >> 2;
+    const W1 e = wz[k];
+    double wp = 0.0, wc = 0.0, wn = 0.0;
+    if (e.I0 == m - 1) wp += e.w0;
+    else if (e.I0 == m) wc += e.w0;
+    else if (e.I0 == m + 1) wn += e.w0;
+    if (e.I1 != e.I0) {
+      if (e.I1 == m - 1) wp += e.w1;
+      else if (e.I1 == m) wc += e.w1;
+      else if (e.I1 == m + 1) wn += e.w1;
+    }
+    wzs[k - kbeg][0] = wp, wzs[k - kbeg][1] = wc, wzs[k - kbeg][2] = wn;
+  }
+  // x weights of this pair's two cells: to the own coarse cell (a) and to the other one (b)
+  const int Iown = q >> 1, Ioth = (q & 1) ? Iown + 1 : Iown - 1;
+  double a[2] = {0.0, 0.0}, b[2] = {0.0, 0.0};
+  if (live) {
+#pragma unroll
+    for (int pb = 0; pb < 2; ++pb) {
+      const W1 e = wx[2 * q + pb];
+      if (e.I0 == Iown) a[pb] += e.w0;
+      if (e.I0 == Ioth) b[pb] += e.w0;
+      if (e.I1 != e.I0) {
+        if (e.I1 == Iown) a[pb] += e.w1;
+        if (e.I1 == Ioth) b[pb] += e.w1;
+      }
+    }
+  }
+  __syncthreads();
+  double accP[2] = {0.0, 0.0}, accC[2] = {0.0, 0.0}, accN[2] = {0.0, 0.0};
+  int mcur = kbeg >> 2, nemit = 0;
+  const int64_t pstride = (int64_t)hx * ny;
+  const double* pl = resB + pstride * kbeg + (live ? q : 0);
+
+  auto emit = [&](const double (&v)[2], int K) {
+    double A = a[0] * v[0] + a[1] * v[1];
+    double B = b[0] * v[0] + b[1] * v[1];
+    if (!live) A = 0.0, B = 0.0;
+    const int eb = nemit & 1;
+    ++nemit;
+    if (lane == 0) edgeL[eb][wid] = B;
+    if (lane == 31) edgeR[eb][wid] = B;
+    __syncthreads();
+    const double up = __shfl_up_sync(0xffffffffu, B, 1), dn = __shfl_down_sync(0xffffffffu, B, 1);
+    double T = (lane & 1) ? dn : up;   // even lanes: the pair to the left; odd lanes: to the right
+    if (lane == 0) T = (wid > 0) ? edgeR[eb][wid - 1] : 0.0;
+    if (lane == 31) T = (wid + 1 < nw) ? edgeL[eb][wid + 1] : 0.0;
+    const double S = A + T;
+    const double O = S + __shfl_xor_sync(0xffffffffu, S, 1);
+    if (live && !(lane & 1)) coarse[Iown + (int64_t)ncx * (J + (int64_t)ncy * K)] = O;
+  };
+
+  // the next plane's 8 rows are in flight while this plane is accumulated
+  double v[8], vn[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) v[t] = pl[jrs[t]];
+  for (int k = kbeg; k < kend; ++k) {
+    pl += pstride;
+    if (k + 1 < kend) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) vn[t] = pl[jrs[t]];
+    }
+    const int m = k >> 2;
+    if (m != mcur) {   // the window moves up one coarse plane
+      accP[0] = accC[0], accP[1] = accC[1];
+      accC[0] = accN[0], accC[1] = accN[1];
+      accN[0] = 0.0, accN[1] = 0.0;
+      mcur = m;
+    }
+    // rows of one parity hold the same cell of the pair: pb = (j + k + z0 + 1) & 1
+    const int pb0 = (k + L.z0 + 1) & 1;   // cell index in the even window rows (jlo is even)
+    double te = 0.0, to = 0.0;            // even window rows (cell pb0), odd rows (cell 1 - pb0)
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      te += wys[t] * v[t];
+      to += wys[t + 1] * v[t + 1];
+    }
+    const double wp = wzs[k - kbeg][0], wc = wzs[k - kbeg][1], wn = wzs[k - kbeg][2];
+    const double t0 = pb0 ? to : te, t1 = pb0 ? te : to;   // by cell of the pair
+    accP[0] += wp * t0, accP[1] += wp * t1;
+    accC[0] += wc * t0, accC[1] += wc * t1;
+    accN[0] += wn * t0, accN[1] += wn * t1;
+    // coarse plane m-1 is complete after fine plane 4m+1
+    if ((k & 3) == 1 && m - 1 >= Ka && m - 1 < Kb) emit(accP, m - 1);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = vn[t];
+  }
+  // the top coarse plane of the domain never becomes the lower slot
+  if (kend == nz && ncz - 1 >= Ka && ncz - 1 < Kb) emit(accC, ncz - 1);
+}
+
 // ---------------------------------------------------------------------------------------------
 // a10 on TMA: p_out = z + beta p_in, q = A p_out, p_out . q (same per-cell expressions as
 // k_spmv_col; neighbour p values are formed from z and p_in, never from p_out).  Tile: 32 pairs

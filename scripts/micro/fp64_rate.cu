@@ -14,7 +14,17 @@ __global__ void k(double* out, int iters, double a) {
     for (int u = 0; u < 8; ++u) {
       if (OP == 0) v[u] = fma(v[u], a, 1e-9);        // DFMA
       else if (OP == 1) v[u] = a / (v[u] + 1.0);      // IEEE division (+ one add)
-      else v[u] = __drcp_rn(v[u] + 1.0);               // correctly rounded reciprocal (+ add)
+      else if (OP == 2) v[u] = __drcp_rn(v[u] + 1.0);  // correctly rounded reciprocal (+ add)
+      else {                                           // MUFU.RCP64H seed + 2 Newton steps (+ add)
+        const double d = v[u] + 1.0;
+        double x;
+        asm("{.reg .b32 lo, hi; mov.b64 {lo, hi}, %1; rcp.approx.ftz.f64 %0, %1;}" : "=d"(x) : "d"(d));
+        double e = fma(-d, x, 1.0);
+        x = fma(x, e, x);
+        e = fma(-d, x, 1.0);
+        x = fma(x, e, x);
+        v[u] = x;
+      }
     }
   }
   double s = 0;
@@ -33,13 +43,14 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[3] = {"dfma", "ddiv (a/(v+1))", "drcp_rn (1/(v+1))"};
-  for (int op = 0; op < 3; ++op) {
+  const char* names[4] = {"dfma", "ddiv (a/(v+1))", "drcp_rn (1/(v+1))", "rcp.approx + 2 Newton"};
+  for (int op = 0; op < 4; ++op) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
       if (op == 0) k<0><<<blocks, threads>>>(out, iters, 0.999999);
       else if (op == 1) k<1><<<blocks, threads>>>(out, iters, 0.999999);
-      else k<2><<<blocks, threads>>>(out, iters, 0.999999);
+      else if (op == 2) k<2><<<blocks, threads>>>(out, iters, 0.999999);
+      else k<3><<<blocks, threads>>>(out, iters, 0.999999);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms = 0;

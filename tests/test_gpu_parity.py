@@ -561,8 +561,9 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
         z, its = s.precond(0, r, rel_tol=w.rel_tol)
         prof = s.profile_read()
         s.profile(False, 0)
-        # the fused path books its x-restriction as a second restrict-class launch
-        assert prof[("restrict", 0)][0] == (2 if fused == "1" else 1), prof
+        # the fused path's closing red sweep is part of the residual pass: one single
+        # half-sweep (the post-smoothing's) instead of two
+        assert prof[("halfsweep", 0)][0] == (1 if fused == "1" else 2), prof
         x, rep = s.solve(cu(torch, w.f), rel_tol=w.rel_tol)
         out[fused] = (z.cpu().numpy(), list(its), x.cpu().numpy(), list(rep.iters))
         out["r"] = r.cpu().numpy()
@@ -571,6 +572,40 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
     assert ia == ib and ra == rb
     assert rel(zb, za) <= 1e-12
     assert rel(xb, xa) <= 1e-12
+
+
+@pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
+                                     ("3d_ragged", CASES[1][1]), ("tall", lambda: random_problem(3, (72, 40, 136), seed=31))],
+                         ids=["C2", "C5_128", "3d_ragged", "tall"])
+@pytest.mark.parametrize("kc", ["0", "1", "3"])
+def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, monkeypatch):
+    """x, y and z restriction of the stored black residual in one pass (k_restrict_black_xyz,
+    R = E^T) against the three table-driven passes: the coarse right-hand side of one
+    pre-smoothing + restriction agrees to 1e-13 (another summation order), for several
+    coarse-plane chunkings (chunk edges fall inside the domain), and with the oracle's
+    formulas in tests/test_gpu_production_kernels.py."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = mk()
+    K = torch.from_numpy(w.K).cuda()
+    monkeypatch.setenv("MSS_PAIR", "1")
+    monkeypatch.setenv("MSS_RXYZ_KC", kc)
+    rng = np.random.default_rng(19)
+    out = {}
+    r = None
+    for one in ("0", "1"):
+        monkeypatch.setenv("MSS_RESTRICT_XYZ", one)
+        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+        if r is None:
+            r = cu(torch, rng.standard_normal(s.level_N(0)))
+        s.profile(True, 0)
+        z, bc = s.presmooth_restrict(0, r)
+        prof = s.profile_read()
+        s.profile(False, 0)
+        assert prof[("restrict", 0)][0] == (1 if one == "1" else 2), prof
+        out[one] = (z.cpu().numpy(), bc.cpu().numpy())
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert rel(out["1"][1], out["0"][1]) <= 1e-13
 
 
 @pytest.mark.parametrize("ty", ["16", "8"])

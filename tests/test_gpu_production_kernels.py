@@ -150,7 +150,7 @@ def test_presmooth_restrict_and_postsmooth(torch_mod, name, mk, variant, monkeyp
 
 def test_variants_select_the_kernels_they_name(torch_mod, monkeypatch):
     """The pair variants really run pairs and the fused closing sweep + residual on level 0
-    (restrict class booked twice: k_restrict_x_black and the y/z passes)."""
+    (restrict class booked once: the x / y / z restriction is one pass, k_restrict_black_xyz)."""
     torch = torch_mod
     w = CASES[0][1]()
     for variant, npair in (("default", 0), ("pair16", 4)):
@@ -163,7 +163,7 @@ def test_variants_select_the_kernels_they_name(torch_mod, monkeypatch):
         got = prof.get(("pair_sweep", 0), (0,))[0]
         assert got == npair, (variant, prof)
         if npair:
-            assert prof[("residual", 0)][0] == 1 and prof[("restrict", 0)][0] == 2, prof
+            assert prof[("residual", 0)][0] == 1 and prof[("restrict", 0)][0] == 1, prof
 
 
 def test_neumann_flux_rhs_closed_form(torch_mod):
