@@ -310,6 +310,74 @@ __global__ void __launch_bounds__(256) k_prolong_pairs(LevelDev L, int ncx, int 
   }
 }
 
+// a8 for scale factor 4 (Level::w4): one thread per cell pair and coarse plane block m, i.e.
+// the pair's four fine planes 4m .. 4m+3, whose taps all lie in the coarse planes m-1, m, m+1,
+// two coarse rows and two coarse columns: 12 coarse loads serve four black cells (the
+// per-pair kernel above issues 8 per cell) and the four 128-bit z accesses are in flight
+// together.  The per-cell expression, its operands and their order are those of
+// k_prolong_pairs / prolong_item (the table entries are used as they are; a tap the table
+// does not name is never selected).
+template <int BT, int MINB>
+__global__ void __launch_bounds__(BT, MINB) k_prolong_black4(LevelDev L, int ncx, int ncy, int ncz,
+                                                        const double* __restrict__ y, double* __restrict__ z,
+                                                        const W1* __restrict__ wx, const W1* __restrict__ wy,
+                                                        const W1* __restrict__ wz) {
+  const int hx = L.nx >> 1;
+  const int j = blockIdx.x, m = blockIdx.y;
+  const int64_t cp = (int64_t)ncx * ncy;
+  const W1 ay = wy[j];
+  W1 az[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) az[o] = wz[4 * m + o];
+  const int Pm = max(m - 1, 0), Pp = min(m + 1, ncz - 1);
+  const double* y0 = y + (int64_t)ncx * ay.I0;
+  const double* y1 = y + (int64_t)ncx * ay.I1;
+  for (int q = threadIdx.x; q < hx; q += blockDim.x) {
+    const int i0 = 2 * q;
+    const int64_t c0 = i0 + (int64_t)L.nx * (j + (int64_t)L.ny * (4 * m));
+    double2 zc[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) zc[o] = ld2(z + c0 + o * L.plane);
+    const W1 xa = wx[i0], xb = wx[i0 + 1];
+    // both cells' taps lie in the columns lo, lo + 1
+    const int lo = ((i0 & 3) < 2) ? (i0 >> 2) - 1 : (i0 >> 2);
+    const int X0 = max(lo, 0), X1 = min(lo + 1, ncx - 1);
+    // x-y interpolated value of each cell on the three coarse planes
+    double Pa[3], Pb[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int64_t pz = cp * (t == 0 ? Pm : (t == 1 ? m : Pp));
+      const double v00 = __ldg(y0 + pz + X0), v10 = __ldg(y0 + pz + X1);
+      const double v01 = __ldg(y1 + pz + X0), v11 = __ldg(y1 + pz + X1);
+      {
+        const double a00 = (xa.I0 == X0) ? v00 : v10, a10 = (xa.I1 == X0) ? v00 : v10;
+        const double a01 = (xa.I0 == X0) ? v01 : v11, a11 = (xa.I1 == X0) ? v01 : v11;
+        Pa[t] = ay.w0 * (xa.w0 * a00 + xa.w1 * a10) + ay.w1 * (xa.w0 * a01 + xa.w1 * a11);
+      }
+      {
+        const double b00 = (xb.I0 == X0) ? v00 : v10, b10 = (xb.I1 == X0) ? v00 : v10;
+        const double b01 = (xb.I0 == X0) ? v01 : v11, b11 = (xb.I1 == X0) ? v01 : v11;
+        Pb[t] = ay.w0 * (xb.w0 * b00 + xb.w1 * b10) + ay.w1 * (xb.w0 * b01 + xb.w1 * b11);
+      }
+    }
+    const int par0 = (i0 + j + 4 * m + L.z0 + 1) & 1;   // black cell of the pair at plane 4m
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int par = par0 ^ (o & 1);
+      const double c0v = par ? Pb[0] : Pa[0], c1v = par ? Pb[1] : Pa[1], c2v = par ? Pb[2] : Pa[2];
+      const int s0 = az[o].I0 - m + 1, s1 = az[o].I1 - m + 1;   // 0, 1, 2: planes m-1, m, m+1
+      const double p0 = (s0 == 0) ? c0v : ((s0 == 1) ? c1v : c2v);
+      const double p1 = (s1 == 0) ? c0v : ((s1 == 1) ? c1v : c2v);
+      double acc = p0;
+      acc *= az[o].w0;
+      acc += az[o].w1 * p1;
+      if (par) zc[o].y += acc;
+      else zc[o].x += acc;
+      *reinterpret_cast<double2*>(z + c0 + o * L.plane) = zc[o];
+    }
+  }
+}
+
 // a8 column-walk: z_black += (E y)_black, thread per pair walking z.  Per coarse plane Z the
 // x-y interpolated values of both cells of the pair, P_a(Z) and P_b(Z), are formed once and
 // carried (the fine walk revisits each coarse plane ~s times); the black cell then gets

@@ -364,6 +364,7 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.spmv_nch = geti("MSS_SPMV_NCH", 0);
   ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
   ctx->kn.restrict_xyz = geti("MSS_RESTRICT_XYZ", 1) != 0;
+  ctx->kn.prolong4 = geti("MSS_PROLONG4", 1) != 0;
   ctx->kn.rxyz_kc = geti("MSS_RXYZ_KC", 0);
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
   ctx->kn.fused_prolong = geti("MSS_FUSED_PROLONG", 0) != 0;
@@ -748,7 +749,19 @@ static int op_prolong_add(mss_ctx* ctx, int k, const double* y, double* z, int c
     ProfScope ps(ctx, KC_PROLONG, k, cell_bytes(ctx, KC_PROLONG) * f.N + 8.0 * c.N);
     dim3 cgrid;
     int kch = 0;
-    if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && !dist_level(ctx, k) && f.w[0] && f.w[1] && f.w[2] &&
+    if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && !dist_level(ctx, k) && f.w4 && ctx->kn.prolong4 &&
+        c.nz <= 65535 && f.nx / 2 >= 32) {
+      // scale factor 4: one thread per pair and block of four fine planes
+      const int bt = std::min(512, (f.nx / 2 + 31) / 32 * 32);
+      const W1 *w0 = reinterpret_cast<const W1*>(f.w[0]), *w1 = reinterpret_cast<const W1*>(f.w[1]),
+               *w2 = reinterpret_cast<const W1*>(f.w[2]);
+      const dim3 pg(f.ny, c.nz);
+      if (bt <= 256)
+        k_prolong_black4<256, 4><<<pg, bt, 0, ctx->stream>>>(f.dev(), c.nx, c.ny, c.nz, y, z, w0, w1, w2);
+      else
+        k_prolong_black4<512, 1><<<pg, bt, 0, ctx->stream>>>(f.dev(), c.nx, c.ny, c.nz, y, z, w0, w1, w2);
+      ctx->launches++;
+    } else if (colour == 1 && ctx->ndim == 3 && col_ok(ctx, f) && !dist_level(ctx, k) && f.w[0] && f.w[1] && f.w[2] &&
         ctx->kn.prolong_pairs && (int64_t)(f.nx / 2) * f.ny * f.nz < ((int64_t)1 << 32)) {
       const int64_t np = (int64_t)(f.nx / 2) * f.ny * f.nz;
       LAUNCH(k_prolong_pairs, grid_for(np), f.dev(), c.nx, c.ny, y, z, reinterpret_cast<const W1*>(f.w[0]),

@@ -608,6 +608,36 @@ def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, monkeypatch):
     assert rel(out["1"][1], out["0"][1]) <= 1e-13
 
 
+@pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
+                                     ("tall", lambda: random_problem(3, (72, 40, 136), seed=31)),
+                                     ("wide", lambda: random_problem(3, (1032, 8, 8), seed=32))],
+                         ids=["C2", "C5_128", "tall", "wide"])
+def test_prolong_four_planes_per_thread(torch_mod, name, mk, monkeypatch):
+    """a8 with one thread per cell pair and four fine planes (k_prolong_black4, scale factor 4)
+    against the per-pair kernel: z_black += (E y)_black, same taps and operand
+    order, so the results agree to rounding of the contraction (<= 1e-15); red cells untouched."""
+    torch = torch_mod
+    from paper_math_9809043_b200.mss import Solver
+    w = mk()
+    K = torch.from_numpy(w.K).cuda()
+    rng = np.random.default_rng(23)
+    out = {}
+    y = z = None
+    for four in ("0", "1"):
+        monkeypatch.setenv("MSS_PROLONG4", four)
+        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+        if y is None:
+            y = cu(torch, rng.standard_normal(s.level_N(1)))
+            z = cu(torch, rng.standard_normal(s.level_N(0)))
+        out[four] = s.prolong_add(0, y, z.clone(), color=1).cpu().numpy()
+    assert rel(out["1"], out["0"]) <= 1e-15
+    nx, ny, nz = w.n
+    kk, jj, ii = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    red = ((ii + jj + kk) & 1) == 0
+    assert np.array_equal(out["1"].reshape(nz, ny, nx)[red], z.cpu().numpy().reshape(nz, ny, nx)[red])
+    assert not np.array_equal(out["1"], z.cpu().numpy())
+
+
 @pytest.mark.parametrize("ty", ["16", "8"])
 def test_hot_paths_are_bitwise_deterministic(torch_mod, ty, monkeypatch):
     """Race check (compute-sanitizer is closed on this pool): the TMA pair sweeps (both tile
