@@ -78,6 +78,7 @@ struct TsArgs {
   long long* phase_cyc; // optional [16] per-phase clock64 totals (CTA 0 thread 0), null = off
   int ct;               // 3-D top level with compile-time dims (sweep_ct): 0 none, 1 = 32x32 with
                         // 2 planes per CTA, 2 = 16x16 x 1, 3 = 16x16 x 2
+  int ct_smooth;        // 1: the ct level's smoothing keeps the thread's faces and values in registers (smooth_ct)
   int o_rfull;          // replicated full r_L (NL doubles)
   int o_red;            // reduction scratch (40 doubles)
   int smem_doubles;
@@ -364,6 +365,127 @@ struct TailSm {
     return acc;
   }
 
+  // All 2m+1 half-sweeps of one smoothing with the thread's data in registers: a thread owns
+  // the cell pair of column m, row j on every local plane for the whole smoothing, so the six
+  // face weights (masked to 0 where the neighbour is outside the domain), r and the diagonal
+  // of its 2 PPC cells are loaded once instead of once per half-sweep, and two of a cell's
+  // six neighbours are the thread's own values (the pair's other cell; the other local
+  // plane).  Per update that leaves one x and two y neighbours in shared memory and, on a
+  // slab's outer plane, one z neighbour in the neighbour CTA (DSMEM).  Same per-cell
+  // expressions, operand order and dot order as nbr_ct / the generic sweep() (a masked face times a finite
+  // clamped value is the same 0 as a face times a masked value).
+  template <int NX, int NY, int PPC>
+  __device__ double smooth_ct(const TsLevel& l, bool zero, bool dot_last) {
+    constexpr int HX = NX / 2, P = NX * NY, U = HX * NY;
+    static_assert(U <= kTsThreads, "one pair column per thread");
+    const int o0 = olo(l), nloc = ohi(l) - o0;
+    double* z = sm + l.o_z;
+    const double* zlo = sm_lo ? sm_lo + l.o_z + (l.ppc - 1) * P : nullptr;
+    const double* zhi = sm_hi ? sm_hi + l.o_z : nullptr;
+    const int pos = threadIdx.x;
+    const bool act = pos < U;
+    const int j = act ? pos / HX : 0, m = act ? pos - (pos / HX) * HX : 0;
+    // [kk][c]: plane kk, colour c
+    double T[PPC][2][6], zr[PPC][2];
+#pragma unroll
+    for (int kk = 0; kk < PPC; ++kk) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int f = 0; f < 6; ++f) T[kk][c][f] = 0.0;
+        zr[kk][c] = 0.0;
+        if (act && kk < nloc) {
+          const int k = o0 + kk, par = (j + k + c) & 1, i = 2 * m + par;
+          const int row = kk * P + j * NX, own = row + c * HX + m, oth = row + (c ^ 1) * HX;
+          const bool hxl = i > 0, hxh = i < NX - 1, hyl = j > 0, hyh = j < NY - 1;
+          const bool hzl = k > 0, hzh = k < l.nz - 1, inh = kk < nloc - 1;
+          const double* tx = sm + l.o_tx;
+          const double* ty = sm + l.o_ty;
+          const double* tz = sm + l.o_tz;
+          T[kk][c][0] = hxl ? tx[own] : 0.0;
+          T[kk][c][1] = hxh ? tx[oth + m + par] : 0.0;
+          T[kk][c][2] = hyl ? ty[own] : 0.0;
+          T[kk][c][3] = hyh ? ty[oth + m + NX] : 0.0;
+          T[kk][c][4] = hzl ? tz[own] : 0.0;
+          T[kk][c][5] = hzh ? (inh ? tz[oth + m + P] : sm[l.o_tup + own - kk * P]) : 0.0;
+          if (!zero) zr[kk][c] = z[own];
+        }
+      }
+    }
+    const int nh = 2 * A->m + 1;
+    double acc = 0.0;
+    for (int h = 0; h < nh; ++h) {
+      const bool first = zero && h == 0;
+      const bool dot = dot_last && h == nh - 1 && !first;
+      double zn[PPC], rn[PPC];   // new values and their r
+      if (h & 1) {
+#pragma unroll
+        for (int kk = 0; kk < PPC; ++kk) zn[kk] = smooth_ct_cell<NX, NY, PPC, 1>(l, kk, nloc, j, m, o0, first, act, T, zr, z, zlo, zhi, rn[kk]);
+#pragma unroll
+        for (int kk = 0; kk < PPC; ++kk)
+          if (act && kk < nloc) {
+            z[kk * P + j * NX + HX + m] = zn[kk];
+            zr[kk][1] = zn[kk];
+          }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < PPC; ++kk) zn[kk] = smooth_ct_cell<NX, NY, PPC, 0>(l, kk, nloc, j, m, o0, first, act, T, zr, z, zlo, zhi, rn[kk]);
+#pragma unroll
+        for (int kk = 0; kk < PPC; ++kk)
+          if (act && kk < nloc) {
+            z[kk * P + j * NX + m] = zn[kk];
+            zr[kk][0] = zn[kk];
+          }
+      }
+      if (dot) {
+        const int c = h & 1;
+#pragma unroll
+        for (int kk = 0; kk < PPC; ++kk)
+          if (act && kk < nloc) {
+            acc += rn[kk] * zn[kk];
+            acc += sm[l.o_r + kk * P + j * NX + (c ^ 1) * HX + m] * (c ? zr[kk][0] : zr[kk][1]);
+          }
+        const double d = sum(acc);
+        mark(0);
+        return d;
+      }
+      sync();
+      mark(0);
+    }
+    return 0.0;
+  }
+
+  // one cell update of smooth_ct: colour C cell of plane kk (its new value)
+  template <int NX, int NY, int PPC, int C>
+  __device__ __forceinline__ double smooth_ct_cell(const TsLevel& l, int kk, int nloc, int j, int m, int o0, bool first,
+                                                   bool act, const double (&T)[PPC][2][6], const double (&zr)[PPC][2],
+                                                   const double* z, const double* zlo, const double* zhi, double& rcell) {
+    constexpr int HX = NX / 2, P = NX * NY;
+    rcell = 0.0;
+    if (!(act && kk < nloc)) return 0.0;
+    const int k = o0 + kk, par = (j + k + C) & 1;
+    const int row = kk * P + j * NX, own = row + C * HX + m, oth = row + (C ^ 1) * HX;
+    const double rvc = sm[l.o_r + own], dvc = sm[l.o_dg + own];
+    rcell = rvc;
+    if (first) return rvc / dvc;
+    const bool hyl = j > 0, hyh = j < NY - 1;
+    const double pairv = zr[kk][C ^ 1];            // the pair's other cell
+    // the x neighbour in the adjacent pair: par = 0: column m - 1 (the cell is the pair's left
+    // one), par = 1: column m + 1; clamped to the cell itself where that face is masked
+    const int xoi = par ? ((2 * m + 1 < NX - 1) ? oth + m + 1 : own) : ((m > 0) ? oth + m - 1 : own);
+    const double xov = z[xoi];
+    const double xl = par ? pairv : xov, xh = par ? xov : pairv;
+    const double yl = z[hyl ? oth + m - NX : own], yh = z[hyh ? oth + m + NX : own];
+    double zl, zh;
+    if (kk > 0) zl = zr[kk - 1 < 0 ? 0 : kk - 1][C ^ 1];
+    else zl = zlo ? zlo[own - kk * P + (1 - 2 * C) * HX] : z[own];
+    if (kk < PPC - 1 && kk < nloc - 1) zh = zr[kk + 1 > PPC - 1 ? PPC - 1 : kk + 1][C ^ 1];
+    else zh = zhi ? zhi[own - kk * P + (1 - 2 * C) * HX] : z[own];
+    double s = T[kk][C][0] * xl + T[kk][C][1] * xh + T[kk][C][2] * yl + T[kk][C][3] * yh;
+    s += T[kk][C][4] * zl + T[kk][C][5] * zh;
+    return (rvc + s) / dvc;
+  }
+
   // q = A p on the local planes (both cells of every pair); returns the thread's p.q partial
   template <int NX, int NY, int PPC>
   __device__ double spmv_ct(const TsLevel& l, int off_p, double* qv) {
@@ -563,6 +685,13 @@ struct TailSm {
   }
 
   __device__ double smooth(int q, bool zero, bool dot_last) {
+    if (A->ct_smooth) {
+      double d = 0.0;
+      if (with_ct(q, [&](auto nx_, auto ny_, auto ppc_) {
+            d = smooth_ct<decltype(nx_)::value, decltype(ny_)::value, decltype(ppc_)::value>(lvl(q), zero, dot_last);
+          }))
+        return d;
+    }
     const int nh = 2 * A->m + 1;
     double d = 0.0;
     for (int h = 0; h < nh; ++h) {
@@ -1016,6 +1145,7 @@ static bool tailsm_layout(mss_ctx* ctx, int L0, int cs, mss::TsArgs& a) {
     else if (t0.nx == 16 && t0.ny == 16 && t0.ppc == 1) a.ct = 2;
     else if (t0.nx == 16 && t0.ny == 16 && t0.ppc == 2) a.ct = 3;
     if (getenv("MSS_TAIL_CT") && atoi(getenv("MSS_TAIL_CT")) == 0) a.ct = 0;
+    a.ct_smooth = (getenv("MSS_TAIL_SMOOTH_REG") && atoi(getenv("MSS_TAIL_SMOOTH_REG")) == 0) ? 0 : 1;
   }
   a.o_rfull = off; off += ctx->NL;
   a.o_red = off; off += 40;

@@ -24,7 +24,10 @@ ap.add_argument("--params", default="{}")
 ap.add_argument("--stream", action="store_true", help="run on a non-default stream")
 args = ap.parse_args()
 build.build()
-from paper_math_9809043_b200.mss import Solver  # noqa: E402
+from paper_math_9809043_b200.mss import Solver, load_library  # noqa: E402
+
+if os.environ.get("MSS_PROBE_LIB"):   # A/B against another build of the library (same session)
+    load_library(os.path.join(ROOT, os.environ["MSS_PROBE_LIB"]))
 
 if args.stream:
     torch.cuda.set_stream(torch.cuda.Stream())
