@@ -279,8 +279,10 @@ int mss_setup_loopback(mss_ctx** out, void* group, int rank, int ndim, const int
  * Classes: 0 half-sweep (generic), 1 half-sweep from z = 0, 2 residual, 3 restrict,
  * 4 prolong-add, 5 direction+SpMV+dot, 6 axpy+norm, 7 dot, 8 coarsest solve, 9 cluster tail
  * (the whole device-resident PCG of the levels below, bracketed as one launch),
- * 10 fused red+black pair (two half-sweeps in one pass; bytes = one pass's). */
-#define MSS_NUM_KCLASS 11
+ * 10 fused red+black pair (two half-sweeps in one pass; bytes = one pass's),
+ * 11 z-slab halo exchange (bytes = planes sent + received), 12 CG-scalar allreduce and the
+ * gather of the first replicated level (distributed levels only). */
+#define MSS_NUM_KCLASS 13
 int mss_profile(mss_ctx* ctx, int enable, int max_level);      /* enable also resets */
 int mss_profile_read(const mss_ctx* ctx, int kclass, int level, int64_t* count,
                      double* ms, double* bytes);

@@ -181,15 +181,8 @@ static bool col_grid(const void* kern, const Level& l, dim3* grid, int* kchunk) 
 static bool dist_level(const mss_ctx* ctx, int k) {
   return ctx->comm && ctx->comm->size > 1 && k < ctx->ndist;
 }
-static int do_halo(mss_ctx* ctx, int k, double* v, int depth = 1) {
-  if (!dist_level(ctx, k)) return MSS_OK;
-  const Level& l = ctx->lv[k];
-  return ctx->comm->halo(ctx->stream, v, l.plane, l.nz, depth);
-}
-static int do_allred(mss_ctx* ctx, int k, double* dev) {
-  if (!dist_level(ctx, k)) return MSS_OK;
-  return ctx->comm->allreduce_sum(ctx->stream, dev);
-}
+static int do_halo(mss_ctx* ctx, int k, double* v, int depth = 1);
+static int do_allred(mss_ctx* ctx, int k, double* dev);
 static double global_N(const Level& l) { return (double)l.nx * l.ny * (double)(l.nzg ? l.nzg : l.nz); }
 
 // Slab partition of the global planes in units of s^ndist planes (so every distributed
@@ -207,7 +200,7 @@ static void slab_of(int64_t nzg0, int64_t unit, int P, int r, int64_t* z0, int64
   } while (0)
 
 // ============================================================================ live kernel timing
-enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_TAIL, KC_PAIR };
+enum KClass { KC_SWEEP = 0, KC_SWEEP0, KC_RESID, KC_RESTRICT, KC_PROLONG, KC_SPMV, KC_AXPY, KC_DOT, KC_COARSE, KC_TAIL, KC_PAIR, KC_HALO, KC_ALLRED };
 
 static cudaEvent_t ev_get(mss_ctx* ctx) {
   if (!ctx->ev_free.empty()) {
@@ -257,6 +250,18 @@ struct ProfScope {
     if (c->prof_pend.size() > 8192) prof_flush(c);
   }
 };
+
+static int do_halo(mss_ctx* ctx, int k, double* v, int depth) {
+  if (!dist_level(ctx, k)) return MSS_OK;
+  const Level& l = ctx->lv[k];
+  ProfScope ps(ctx, KC_HALO, k, 8.0 * 4 * depth * (double)l.plane);   // up + down, sent + received
+  return ctx->comm->halo(ctx->stream, v, l.plane, l.nz, depth);
+}
+static int do_allred(mss_ctx* ctx, int k, double* dev) {
+  if (!dist_level(ctx, k)) return MSS_OK;
+  ProfScope ps(ctx, KC_ALLRED, k, 0.0);
+  return ctx->comm->allreduce_sum(ctx->stream, dev);
+}
 
 // Algorithmic bytes per cell (fp64 words x 8) of each kernel with the interleaved
 // layout (SURVEY §8(d) "interleaved" column): T = ndim words per cell.
@@ -695,6 +700,7 @@ static int op_restrict_yz(mss_ctx* ctx, int k, double* coarse) {
       off[q] = (z0 / sc) * cplane;
       len[q] = ((z1 - z0) / sc) * cplane;
     }
+    ProfScope ps(ctx, KC_ALLRED, k, 8.0 * c.N);
     TRY(ctx->comm->gather(ctx->stream, coarse, off, len));
   }
   return MSS_OK;

@@ -134,7 +134,7 @@ SIGNATURES = [
 ]
 
 KCLASS = ["halfsweep", "halfsweep_first", "residual", "restrict", "prolong_add", "pdir_spmv_dot",
-          "axpy_norm", "dot", "coarse_solve", "tail", "pair_sweep"]
+          "axpy_norm", "dot", "coarse_solve", "tail", "pair_sweep", "halo", "allreduce_gather"]
 
 _lib = None
 
