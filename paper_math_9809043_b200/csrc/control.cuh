@@ -11,6 +11,12 @@
 
 namespace mss {
 
+// the level's CG scalars into the pinned host copy (see read_scal)
+__global__ void k_scal_to_host(const Scal* __restrict__ d, Scal* __restrict__ h) {
+  *h = *d;
+  __threadfence_system();
+}
+
 // per-level control record (device)
 struct LevelCtl {
   long long calls;   // PCG calls this solve

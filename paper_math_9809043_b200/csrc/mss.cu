@@ -371,6 +371,7 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.restrict_xyz = geti("MSS_RESTRICT_XYZ", 1) != 0;
   ctx->kn.prolong4 = geti("MSS_PROLONG4", 1) != 0;
   ctx->kn.rxyz_kc = geti("MSS_RXYZ_KC", 0);
+  ctx->kn.rxyz_jj = geti("MSS_RXYZ_JJ", 1);
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
   ctx->kn.fused_prolong = geti("MSS_FUSED_PROLONG", 0) != 0;
   ctx->graph_knob = geti("MSS_GRAPH", 1);
@@ -798,8 +799,13 @@ static int op_coarse_solve(mss_ctx* ctx, const double* b, double* x) {
   return MSS_OK;
 }
 
+// The level's device scalars -> the pinned host copy.  A one-thread kernel stores them
+// straight into the pinned (UVA-mapped) host buffer instead of a cudaMemcpyAsync: a copy
+// would queue on the device-to-host copy engine behind whatever is in flight there — in
+// mss_solve_host_batch the previous solve's 1 GiB read-back, which stalled every solve's
+// first threshold read (||b||^2) by the whole transfer (18 ms per step at 512^3).
 static int read_scal(mss_ctx* ctx, int k) {
-  CK(cudaMemcpyAsync(ctx->hscal + k, ctx->dscal + k, sizeof(Scal), cudaMemcpyDeviceToHost, ctx->stream));
+  k_scal_to_host<<<1, 1, 0, ctx->stream>>>(ctx->dscal + k, ctx->hscal + k);
   CK(cudaStreamSynchronize(ctx->stream));
   return MSS_OK;
 }
@@ -837,13 +843,18 @@ static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
     int kc = ctx->kn.rxyz_kc > 0 ? ctx->kn.rxyz_kc : 16;
     kc = std::max(1, std::min(std::min(kc, mss::kRxyzMaxKc), c.nz));
     const int bt = (l.nx / 2 + 31) / 32 * 32;
-    const dim3 xg(c.ny, (c.nz + kc - 1) / kc);
+    const int jj = ctx->kn.rxyz_jj == 2 ? 2 : 1;
+    const dim3 xg((c.ny + jj - 1) / jj, (c.nz + kc - 1) / kc);
     const W1 *w0 = reinterpret_cast<const W1*>(l.w[0]), *w1 = reinterpret_cast<const W1*>(l.w[1]),
              *w2 = reinterpret_cast<const W1*>(l.w[2]);
-    if (bt <= 256)
-      k_restrict_black_xyz<256><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+    if (bt <= 256 && jj == 2)
+      k_restrict_black_xyz<256, 2><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+    else if (bt <= 256)
+      k_restrict_black_xyz<256, 1><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+    else if (jj == 2)
+      k_restrict_black_xyz<512, 2><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
     else
-      k_restrict_black_xyz<512><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+      k_restrict_black_xyz<512, 1><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
     ctx->launches++;
     return MSS_OK;
   }

@@ -406,32 +406,39 @@ __global__ void __launch_bounds__(128) k_restrict_x_black(LevelDev L, const doub
 // (Level::w4): every axis has n = 4 n_c and each fine index 4m+o only has weights to
 // {m-1, m} (o < 2) or {m, m+1} (o >= 2) — true for the linear and the constant E.
 constexpr int kRxyzMaxKc = 32;   // coarse planes per CTA (shared z-weight table)
-template <int BT>
-__global__ void __launch_bounds__(BT, (BT <= 256) ? 3 : 1)
+// JJ coarse rows per CTA: their windows overlap, so JJ = 2 reads 12 fine rows for two coarse
+// rows (1.5x the residual through L2) where JJ = 1 reads 8 for one (2x)
+template <int BT, int JJ>
+__global__ void __launch_bounds__(BT, (BT <= 256) ? (JJ == 1 ? 4 : 2) : 1)
     k_restrict_black_xyz(LevelDev L, const double* __restrict__ resB, double* __restrict__ coarse, int ncx, int ncy,
                          int ncz, const W1* __restrict__ wx, const W1* __restrict__ wy, const W1* __restrict__ wz,
                          int kc) {
-  __shared__ double edgeL[2][32], edgeR[2][32];
-  __shared__ double wys[8];
-  __shared__ int jrs[8];
+  constexpr int NR = 4 * JJ + 4;   // fine rows of the window
+  __shared__ double edgeL[2][JJ][32], edgeR[2][JJ][32];
+  __shared__ double wys[JJ][NR];
+  __shared__ int jrs[NR];
   __shared__ double wzs[4 * kRxyzMaxKc + 4][3];   // per fine plane of the chunk: weight to m-1, m, m+1
   const int hx = L.nx >> 1, ny = L.ny, nz = L.nz;
   const int q = threadIdx.x, lane = q & 31, wid = q >> 5, nw = (blockDim.x + 31) >> 5;
   const bool live = q < hx;
-  const int J = blockIdx.x;
+  const int J0 = blockIdx.x * JJ;
   const int Ka = blockIdx.y * kc, Kb = min(ncz, Ka + kc);
   const int kbeg = max(0, 4 * Ka - 2), kend = min(nz, 4 * Kb + 2);
-  const int jlo = 4 * J - 2;   // even
-  // y weights of the 8 rows of J's window (0 outside the domain; the row index is clamped)
-  if (q < 8) {
+  const int jlo = 4 * J0 - 2;   // even
+  // y weights of the window rows to each coarse row (0 outside the domain / the row's own
+  // window; the row index is clamped)
+  if (q < NR) {
     const int j = jlo + q;
-    double w = 0.0;
-    if (j >= 0 && j < ny) {
-      const W1 e = wy[j];
-      if (e.I0 == J) w += e.w0;
-      if (e.I1 == J && e.I1 != e.I0) w += e.w1;
+#pragma unroll
+    for (int a = 0; a < JJ; ++a) {
+      double w = 0.0;
+      if (j >= 0 && j < ny && J0 + a < ncy) {
+        const W1 e = wy[j];
+        if (e.I0 == J0 + a) w += e.w0;
+        if (e.I1 == J0 + a && e.I1 != e.I0) w += e.w1;
+      }
+      wys[a][q] = w;
     }
-    wys[q] = w;
     jrs[q] = hx * min(max(j, 0), ny - 1);   // row offset in pairs
   }
   for (int k = kbeg + q; k < kend; k += blockDim.x) {
@@ -464,63 +471,78 @@ __global__ void __launch_bounds__(BT, (BT <= 256) ? 3 : 1)
     }
   }
   __syncthreads();
-  double accP[2] = {0.0, 0.0}, accC[2] = {0.0, 0.0}, accN[2] = {0.0, 0.0};
+  double accP[JJ][2], accC[JJ][2], accN[JJ][2];
+#pragma unroll
+  for (int c = 0; c < JJ; ++c) accP[c][0] = accP[c][1] = accC[c][0] = accC[c][1] = accN[c][0] = accN[c][1] = 0.0;
   int mcur = kbeg >> 2, nemit = 0;
   const int64_t pstride = (int64_t)hx * ny;
   const double* pl = resB + pstride * kbeg + (live ? q : 0);
 
-  auto emit = [&](const double (&v)[2], int K) {
-    double A = a[0] * v[0] + a[1] * v[1];
-    double B = b[0] * v[0] + b[1] * v[1];
-    if (!live) A = 0.0, B = 0.0;
+  auto emit = [&](const double (&v)[JJ][2], int K) {
     const int eb = nemit & 1;
     ++nemit;
-    if (lane == 0) edgeL[eb][wid] = B;
-    if (lane == 31) edgeR[eb][wid] = B;
+    double A[JJ], B[JJ];
+#pragma unroll
+    for (int c = 0; c < JJ; ++c) {
+      A[c] = a[0] * v[c][0] + a[1] * v[c][1];
+      B[c] = b[0] * v[c][0] + b[1] * v[c][1];
+      if (!live) A[c] = 0.0, B[c] = 0.0;
+      if (lane == 0) edgeL[eb][c][wid] = B[c];
+      if (lane == 31) edgeR[eb][c][wid] = B[c];
+    }
     __syncthreads();
-    const double up = __shfl_up_sync(0xffffffffu, B, 1), dn = __shfl_down_sync(0xffffffffu, B, 1);
-    double T = (lane & 1) ? dn : up;   // even lanes: the pair to the left; odd lanes: to the right
-    if (lane == 0) T = (wid > 0) ? edgeR[eb][wid - 1] : 0.0;
-    if (lane == 31) T = (wid + 1 < nw) ? edgeL[eb][wid + 1] : 0.0;
-    const double S = A + T;
-    const double O = S + __shfl_xor_sync(0xffffffffu, S, 1);
-    if (live && !(lane & 1)) coarse[Iown + (int64_t)ncx * (J + (int64_t)ncy * K)] = O;
+#pragma unroll
+    for (int c = 0; c < JJ; ++c) {
+      const double up = __shfl_up_sync(0xffffffffu, B[c], 1), dn = __shfl_down_sync(0xffffffffu, B[c], 1);
+      double T = (lane & 1) ? dn : up;   // even lanes: the pair to the left; odd lanes: to the right
+      if (lane == 0) T = (wid > 0) ? edgeR[eb][c][wid - 1] : 0.0;
+      if (lane == 31) T = (wid + 1 < nw) ? edgeL[eb][c][wid + 1] : 0.0;
+      const double S = A[c] + T;
+      const double O = S + __shfl_xor_sync(0xffffffffu, S, 1);
+      if (live && !(lane & 1) && J0 + c < ncy) coarse[Iown + (int64_t)ncx * (J0 + c + (int64_t)ncy * K)] = O;
+    }
   };
 
-  // the next plane's 8 rows are in flight while this plane is accumulated
-  double v[8], vn[8];
+  // the next plane's rows are in flight while this plane is accumulated
+  double v[NR], vn[NR];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) v[t] = pl[jrs[t]];
+  for (int t = 0; t < NR; ++t) v[t] = pl[jrs[t]];
   for (int k = kbeg; k < kend; ++k) {
     pl += pstride;
     if (k + 1 < kend) {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) vn[t] = pl[jrs[t]];
+      for (int t = 0; t < NR; ++t) vn[t] = pl[jrs[t]];
     }
     const int m = k >> 2;
     if (m != mcur) {   // the window moves up one coarse plane
-      accP[0] = accC[0], accP[1] = accC[1];
-      accC[0] = accN[0], accC[1] = accN[1];
-      accN[0] = 0.0, accN[1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < JJ; ++c) {
+        accP[c][0] = accC[c][0], accP[c][1] = accC[c][1];
+        accC[c][0] = accN[c][0], accC[c][1] = accN[c][1];
+        accN[c][0] = 0.0, accN[c][1] = 0.0;
+      }
       mcur = m;
     }
     // rows of one parity hold the same cell of the pair: pb = (j + k + z0 + 1) & 1
     const int pb0 = (k + L.z0 + 1) & 1;   // cell index in the even window rows (jlo is even)
-    double te = 0.0, to = 0.0;            // even window rows (cell pb0), odd rows (cell 1 - pb0)
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      te += wys[t] * v[t];
-      to += wys[t + 1] * v[t + 1];
-    }
     const double wp = wzs[k - kbeg][0], wc = wzs[k - kbeg][1], wn = wzs[k - kbeg][2];
-    const double t0 = pb0 ? to : te, t1 = pb0 ? te : to;   // by cell of the pair
-    accP[0] += wp * t0, accP[1] += wp * t1;
-    accC[0] += wc * t0, accC[1] += wc * t1;
-    accN[0] += wn * t0, accN[1] += wn * t1;
+#pragma unroll
+    for (int c = 0; c < JJ; ++c) {
+      double te = 0.0, to = 0.0;          // even window rows (cell pb0), odd rows (cell 1 - pb0)
+#pragma unroll
+      for (int t = 4 * c; t < 4 * c + 8; t += 2) {   // coarse row c's own window
+        te += wys[c][t] * v[t];
+        to += wys[c][t + 1] * v[t + 1];
+      }
+      const double t0 = pb0 ? to : te, t1 = pb0 ? te : to;   // by cell of the pair
+      accP[c][0] += wp * t0, accP[c][1] += wp * t1;
+      accC[c][0] += wc * t0, accC[c][1] += wc * t1;
+      accN[c][0] += wn * t0, accN[c][1] += wn * t1;
+    }
     // coarse plane m-1 is complete after fine plane 4m+1
     if ((k & 3) == 1 && m - 1 >= Ka && m - 1 < Kb) emit(accP, m - 1);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) v[t] = vn[t];
+    for (int t = 0; t < NR; ++t) v[t] = vn[t];
   }
   // the top coarse plane of the domain never becomes the lower slot
   if (kend == nz && ncz - 1 >= Ka && ncz - 1 < Kb) emit(accC, ncz - 1);

@@ -577,8 +577,8 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
 @pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
                                      ("3d_ragged", CASES[1][1]), ("tall", lambda: random_problem(3, (72, 40, 136), seed=31))],
                          ids=["C2", "C5_128", "3d_ragged", "tall"])
-@pytest.mark.parametrize("kc", ["0", "1", "3"])
-def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, monkeypatch):
+@pytest.mark.parametrize("kc,jj", [("0", "2"), ("1", "2"), ("3", "1"), ("0", "1")])
+def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, monkeypatch):
     """x, y and z restriction of the stored black residual in one pass (k_restrict_black_xyz,
     R = E^T) against the three table-driven passes: the coarse right-hand side of one
     pre-smoothing + restriction agrees to 1e-13 (another summation order), for several
@@ -590,6 +590,7 @@ def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, monkeypatch):
     K = torch.from_numpy(w.K).cuda()
     monkeypatch.setenv("MSS_PAIR", "1")
     monkeypatch.setenv("MSS_RXYZ_KC", kc)
+    monkeypatch.setenv("MSS_RXYZ_JJ", jj)      # coarse rows per CTA (the ragged cases have odd n_cy)
     rng = np.random.default_rng(19)
     out = {}
     r = None
