@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(kColX * kColY, MINB) k_spmv_col(LevelDev L, co
 // (the red residual is zero after the closing red sweep); the x-weighted
 // contributions meet in shared memory and thread I sums the pairs of coarse cell I in
 // a fixed order (deterministic).  t1 has dims (ncx, ny, nz).
-template <int MINB>
+// STORE: the black residual is stored per cell pair instead (t1 = resB, N / 2 doubles; no
+// shared exchange, no barrier) and k_restrict_black_xyz contracts it in one pass.
+template <int MINB, bool STORE = false>
 __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, const double* __restrict__ r,
                                                                   const double* __restrict__ z,
                                                                   double* __restrict__ t1, int ncx, int s, int kind,
@@ -255,23 +257,29 @@ __global__ void __launch_bounds__(512, MINB) k_resid_restrict_col(LevelDev L, co
       const double yn = hasN ? sel(ld2(z + c + nx), par) : 0.0;
       const double nb = txl * xl + txh * xh + t2 * ys + t3 * yn + t4 * sel(zdn, par) + t5 * sel(zup, par);
       const double res = sel(rr, par) - ((txl + txh + t2 + t3 + t4 + t5) * sel(zc, par) - nb);
-      shc[2 * m] = (par ? wb0 : wa0) * res;
-      shc[2 * m + 1] = (par ? wb1 : wa1) * res;
-      shi[2 * m] = par ? Ib0 : Ia0;
-      shi[2 * m + 1] = par ? Ib1 : Ia1;
-    }
-    __syncthreads();
-    const int64_t obase = (int64_t)ncx * (j + (int64_t)ny * k);
-    for (int I = threadIdx.x; I < ncx; I += blockDim.x) {
-      const int mlo = max(0, (s * (I - 1)) >> 1), mhi = min(hx, (s * (I + 2) + 1) >> 1);
-      double acc = 0.0;
-      for (int q = mlo; q < mhi; ++q) {
-        if (shi[2 * q] == I) acc += shc[2 * q];
-        if (shi[2 * q + 1] == I) acc += shc[2 * q + 1];
+      if constexpr (STORE) {
+        t1[row * hx + m] = res;
+      } else {
+        shc[2 * m] = (par ? wb0 : wa0) * res;
+        shc[2 * m + 1] = (par ? wb1 : wa1) * res;
+        shi[2 * m] = par ? Ib0 : Ia0;
+        shi[2 * m + 1] = par ? Ib1 : Ia1;
       }
-      t1[obase + I] = acc;
     }
-    __syncthreads();
+    if constexpr (!STORE) {
+      __syncthreads();
+      const int64_t obase = (int64_t)ncx * (j + (int64_t)ny * k);
+      for (int I = threadIdx.x; I < ncx; I += blockDim.x) {
+        const int mlo = max(0, (s * (I - 1)) >> 1), mhi = min(hx, (s * (I + 2) + 1) >> 1);
+        double acc = 0.0;
+        for (int q = mlo; q < mhi; ++q) {
+          if (shi[2 * q] == I) acc += shc[2 * q];
+          if (shi[2 * q + 1] == I) acc += shc[2 * q + 1];
+        }
+        t1[obase + I] = acc;
+      }
+      __syncthreads();
+    }
     zdn = zc;
     zc = zup;
     tzl = tzu;

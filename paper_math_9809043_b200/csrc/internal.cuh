@@ -161,6 +161,7 @@ struct mss_ctx {
     int spmv_nch = 0;         // MSS_SPMV_NCH: 0 cost model
     bool fused_resid = true;  // MSS_FUSED_RESID
     bool restrict_xyz = true; // MSS_RESTRICT_XYZ: x, y, z restriction of the stored black residual in one pass
+    bool resid_store = true;  // MSS_RESID_STORE: column-walk levels store the black residual and restrict it in one pass
     bool prolong4 = true;     // MSS_PROLONG4: a8 with one thread per pair and four fine planes (scale 4)
     int rxyz_jj = 1;          // MSS_RXYZ_JJ: coarse rows per CTA of that pass (1 or 2)
     int rxyz_kc = 0;          // MSS_RXYZ_KC: coarse planes per CTA of that pass (0 = 16)

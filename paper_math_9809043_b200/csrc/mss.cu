@@ -370,6 +370,7 @@ static void read_knobs(mss_ctx* ctx) {
   ctx->kn.fused_resid = geti("MSS_FUSED_RESID", 1) != 0;
   ctx->kn.restrict_xyz = geti("MSS_RESTRICT_XYZ", 1) != 0;
   ctx->kn.prolong4 = geti("MSS_PROLONG4", 1) != 0;
+  ctx->kn.resid_store = geti("MSS_RESID_STORE", 1) != 0;
   ctx->kn.rxyz_kc = geti("MSS_RXYZ_KC", 0);
   ctx->kn.rxyz_jj = geti("MSS_RXYZ_JJ", 1);
   ctx->kn.prolong_pairs = geti("MSS_PROLONG_PAIRS", 1) != 0;
@@ -707,10 +708,44 @@ static int op_restrict_yz(mss_ctx* ctx, int k, double* coarse) {
   return MSS_OK;
 }
 
+// x, y and z restriction of the stored black residual (level k's resb) in one pass
+static bool restrict_xyz_ok(const mss_ctx* ctx, int k) {
+  const Level& l = ctx->lv[k];
+  const Level& c = ctx->lv[k + 1];
+  return l.w4 && ctx->kn.restrict_xyz && l.resb && l.nx / 2 <= 512 && l.w[0] && l.w[1] && l.w[2] && c.ny <= 65535 &&
+         !dist_level(ctx, k);
+}
+static int op_restrict_xyz(mss_ctx* ctx, int k) {
+  Level& l = ctx->lv[k];
+  Level& c = ctx->lv[k + 1];
+  ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.N);
+  const int bt = (l.nx / 2 + 31) / 32 * 32;
+  // coarse planes per CTA: 16 on big levels (6 % of the planes read twice), fewer on small
+  // ones so that the grid still fills the GPU (about 1024 threads per SM)
+  int kc = ctx->kn.rxyz_kc > 0 ? ctx->kn.rxyz_kc
+                               : (int)std::min<int64_t>(16, (int64_t)c.ny * c.nz * bt / ((int64_t)kSMs * 1024));
+  kc = std::max(1, std::min(std::min(kc, mss::kRxyzMaxKc), c.nz));
+  const int jj = ctx->kn.rxyz_jj == 2 ? 2 : 1;
+  const dim3 xg((c.ny + jj - 1) / jj, (c.nz + kc - 1) / kc);
+  const W1 *w0 = reinterpret_cast<const W1*>(l.w[0]), *w1 = reinterpret_cast<const W1*>(l.w[1]),
+           *w2 = reinterpret_cast<const W1*>(l.w[2]);
+  if (bt <= 256 && jj == 2)
+    k_restrict_black_xyz<256, 2><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+  else if (bt <= 256)
+    k_restrict_black_xyz<256, 1><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+  else if (jj == 2)
+    k_restrict_black_xyz<512, 2><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+  else
+    k_restrict_black_xyz<512, 1><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
+  ctx->launches++;
+  return MSS_OK;
+}
+
 // coarse = R (r - A z): residual fused with the x-pass of the restriction (a6).
 static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double* z, double* coarse, int black_only) {
   Level& f = ctx->lv[k];
   Level& c = ctx->lv[k + 1];
+  bool store = false;
   {
     const double by = 8.0 * (ctx->ndim + 2) * f.N + 8.0 * c.nx * f.ny * f.nz;
     ProfScope ps(ctx, KC_RESID, k, by);
@@ -721,14 +756,23 @@ static int op_resid_restrict(mss_ctx* ctx, int k, const double* r, const double*
       if ((int64_t)nch * f.ny < 2 * kSMs * 4) nch = std::min<int>(f.nz, (2 * kSMs * 4 + f.ny - 1) / f.ny);
       const int kch = (f.nz + nch - 1) / nch;
       nch = (f.nz + kch - 1) / kch;
+      if (coarse == c.r && restrict_xyz_ok(ctx, k) && ctx->kn.resid_store) {
+        // the black residual per cell pair (no shared exchange), then x / y / z in one pass
+        k_resid_restrict_col<2, true><<<dim3(f.ny, nch), bt, 0, ctx->stream>>>(f.dev(), r, z, f.resb, c.nx,
+                                                                                 ctx->prm.scale, ctx->prm.interp, kch);
+        ctx->launches++;
+        store = true;
+      } else {
       const size_t shm = (size_t)bt * 2 * (sizeof(double) + sizeof(int));
       k_resid_restrict_col<2><<<dim3(f.ny, nch), bt, shm, ctx->stream>>>(f.dev(), r, z, f.t1, c.nx, ctx->prm.scale,
                                                                             ctx->prm.interp, kch);
       ctx->launches++;
+      }
     } else
     DISPATCH(ctx->ndim, k_resid_restrict_x, grid_for((int64_t)c.nx * f.ny * f.nz), f.dev(), r, z, f.t1, c.nx,
              ctx->prm.scale, ctx->prm.interp, black_only);
   }
+  if (store) return op_restrict_xyz(ctx, k);
   return op_restrict_yz(ctx, k, coarse);
 }
 
@@ -837,27 +881,7 @@ static int presmooth_restrict(mss_ctx* ctx, int k, int nh, int sgs) {
     ctx->nswap++;
     tail_mark_dirty(ctx);
   }
-  if (l.w4 && ctx->kn.restrict_xyz && l.nx / 2 <= 512 && l.w[1] && l.w[2] && c.ny <= 65535) {
-    // x, y and z in one pass over the stored black residual
-    ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.N);
-    int kc = ctx->kn.rxyz_kc > 0 ? ctx->kn.rxyz_kc : 16;
-    kc = std::max(1, std::min(std::min(kc, mss::kRxyzMaxKc), c.nz));
-    const int bt = (l.nx / 2 + 31) / 32 * 32;
-    const int jj = ctx->kn.rxyz_jj == 2 ? 2 : 1;
-    const dim3 xg((c.ny + jj - 1) / jj, (c.nz + kc - 1) / kc);
-    const W1 *w0 = reinterpret_cast<const W1*>(l.w[0]), *w1 = reinterpret_cast<const W1*>(l.w[1]),
-             *w2 = reinterpret_cast<const W1*>(l.w[2]);
-    if (bt <= 256 && jj == 2)
-      k_restrict_black_xyz<256, 2><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
-    else if (bt <= 256)
-      k_restrict_black_xyz<256, 1><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
-    else if (jj == 2)
-      k_restrict_black_xyz<512, 2><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
-    else
-      k_restrict_black_xyz<512, 1><<<xg, bt, 0, ctx->stream>>>(l.dev(), l.resb, c.r, c.nx, c.ny, c.nz, w0, w1, w2, kc);
-    ctx->launches++;
-    return MSS_OK;
-  }
+  if (restrict_xyz_ok(ctx, k)) return op_restrict_xyz(ctx, k);   // x, y and z in one pass
   {
     ProfScope ps(ctx, KC_RESTRICT, k, 4.0 * l.N + 8.0 * c.nx * l.ny * l.nz);
     const int kper = 16;

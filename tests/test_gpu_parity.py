@@ -577,18 +577,20 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
 @pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
                                      ("3d_ragged", CASES[1][1]), ("tall", lambda: random_problem(3, (72, 40, 136), seed=31))],
                          ids=["C2", "C5_128", "3d_ragged", "tall"])
-@pytest.mark.parametrize("kc,jj", [("0", "2"), ("1", "2"), ("3", "1"), ("0", "1")])
-def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, monkeypatch):
+@pytest.mark.parametrize("kc,jj,pair", [("0", "2", "1"), ("1", "2", "1"), ("3", "1", "1"), ("0", "1", "1"),
+                                        ("0", "1", "0"), ("2", "2", "0")])
+def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, pair, monkeypatch):
     """x, y and z restriction of the stored black residual in one pass (k_restrict_black_xyz,
     R = E^T) against the three table-driven passes: the coarse right-hand side of one
     pre-smoothing + restriction agrees to 1e-13 (another summation order), for several
     coarse-plane chunkings (chunk edges fall inside the domain), and with the oracle's
-    formulas in tests/test_gpu_production_kernels.py."""
+    formulas in tests/test_gpu_production_kernels.py.  pair = 0: the column-walk levels' path
+    (k_resid_restrict_col storing the black residual, then the same single pass)."""
     torch = torch_mod
     from paper_math_9809043_b200.mss import Solver
     w = mk()
     K = torch.from_numpy(w.K).cuda()
-    monkeypatch.setenv("MSS_PAIR", "1")
+    monkeypatch.setenv("MSS_PAIR", pair)
     monkeypatch.setenv("MSS_RXYZ_KC", kc)
     monkeypatch.setenv("MSS_RXYZ_JJ", jj)      # coarse rows per CTA (the ragged cases have odd n_cy)
     rng = np.random.default_rng(19)
@@ -603,7 +605,7 @@ def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, monkeypatch):
         z, bc = s.presmooth_restrict(0, r)
         prof = s.profile_read()
         s.profile(False, 0)
-        assert prof[("restrict", 0)][0] == (1 if one == "1" else 2), prof
+        assert prof[("restrict", 0)][0] == (1 if one == "1" or pair == "0" else 2), prof
         out[one] = (z.cpu().numpy(), bc.cpu().numpy())
     assert np.array_equal(out["0"][0], out["1"][0])
     assert rel(out["1"][1], out["0"][1]) <= 1e-13
