@@ -22,7 +22,7 @@ if [ "${NCU:-launch}" = "launch" ]; then
 elif [ "${NCU}" = "full" ]; then
   timeout 600 $CMD > gpurun_out/plain2.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on \
-      -k regex:"k_sweep2t_col|k_spmv_tma|k_restrict_x_black|k_prolong_pairs|k_axpy_norm|k_sweep_col|k_restrict_axis|k_tailsm" -s 0 -c 16 \
+      -k regex:"k_sweep2t_col|k_spmv_tma|k_restrict_black_xyz|k_prolong_black4|k_axpy_norm|k_sweep_col|k_resid_restrict_col|k_tailsm" -s 0 -c 40 \
       -o gpurun_out/prof_${TAG} $CMD > gpurun_out/ncu_full.log 2>&1
   echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
 fi
