@@ -222,7 +222,7 @@ def main():
         uid = D.nccl_id_for_group()
         z0, z1 = slab_range(w.n, rank, world, depth=w.depth)
         comm = ("nccl", rank, world, uid)
-    K = torch.from_numpy(np.ascontiguousarray(w.K[:, z0:z1])).to(dev)
+    K = torch.from_numpy(np.ascontiguousarray(w.K[:, z0:z1] if w.ndim == 3 else w.K)).to(dev)
     f_np = np.ascontiguousarray(w.f[z0:z1]).ravel() if w.ndim == 3 else w.f.ravel()
     f = torch.from_numpy(f_np).to(dev)
     torch.cuda.synchronize()
