@@ -575,8 +575,9 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
 
 
 @pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
-                                     ("3d_ragged", CASES[1][1]), ("tall", lambda: random_problem(3, (72, 40, 136), seed=31))],
-                         ids=["C2", "C5_128", "3d_ragged", "tall"])
+                                     ("3d_ragged", CASES[1][1]), ("tall", lambda: random_problem(3, (72, 40, 136), seed=31)),
+                                     ("C5_128_constE", lambda: make_workload("C5", n=128))],
+                         ids=["C2", "C5_128", "3d_ragged", "tall", "C5_128_constE"])
 @pytest.mark.parametrize("kc,jj,pair", [("0", "2", "1"), ("1", "2", "1"), ("3", "1", "1"), ("0", "1", "1"),
                                         ("0", "1", "0"), ("2", "2", "0")])
 def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, pair, monkeypatch):
@@ -596,9 +597,10 @@ def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, pair, monkeypatch
     rng = np.random.default_rng(19)
     out = {}
     r = None
+    prm = {"interp": 1} if name.endswith("constE") else None   # piecewise-constant E: I1 == I0 taps
     for one in ("0", "1"):
         monkeypatch.setenv("MSS_RESTRICT_XYZ", one)
-        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=prm)
         if r is None:
             r = cu(torch, rng.standard_normal(s.level_N(0)))
         s.profile(True, 0)
@@ -613,8 +615,9 @@ def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, pair, monkeypatch
 
 @pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
                                      ("tall", lambda: random_problem(3, (72, 40, 136), seed=31)),
-                                     ("wide", lambda: random_problem(3, (1032, 8, 8), seed=32))],
-                         ids=["C2", "C5_128", "tall", "wide"])
+                                     ("wide", lambda: random_problem(3, (1032, 8, 8), seed=32)),
+                                     ("C5_128_constE", lambda: make_workload("C5", n=128))],
+                         ids=["C2", "C5_128", "tall", "wide", "C5_128_constE"])
 def test_prolong_four_planes_per_thread(torch_mod, name, mk, monkeypatch):
     """a8 with one thread per cell pair and four fine planes (k_prolong_black4, scale factor 4)
     against the per-pair kernel: z_black += (E y)_black, same taps and operand
@@ -626,9 +629,10 @@ def test_prolong_four_planes_per_thread(torch_mod, name, mk, monkeypatch):
     rng = np.random.default_rng(23)
     out = {}
     y = z = None
+    prm = {"interp": 1} if name.endswith("constE") else None   # piecewise-constant E
     for four in ("0", "1"):
         monkeypatch.setenv("MSS_PROLONG4", four)
-        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth)
+        s = Solver(w.ndim, w.n, K, w.bc, depth=w.depth, params=prm)
         if y is None:
             y = cu(torch, rng.standard_normal(s.level_N(1)))
             z = cu(torch, rng.standard_normal(s.level_N(0)))

@@ -66,14 +66,15 @@ VARIANTS = {"default": {}, "pair16": {"MSS_PAIR": "1", "MSS_PAIR_TY": "16"},
             "pair8": {"MSS_PAIR": "1", "MSS_PAIR_TY": "8"}}
 
 
-def setup_pair(torch, w, variant, monkeypatch):
+def setup_pair(torch, w, variant, monkeypatch, interp="linear"):
     from paper_math_9809043_b200.mss import Solver
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
-    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth)
+    s = Solver(w.ndim, w.n, torch.from_numpy(w.K).cuda(), w.bc, depth=w.depth,
+               params={"interp": 1 if interp == "constant" else 0})
     for k in VARIANTS[variant]:
         monkeypatch.delenv(k)
-    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth)
+    o = O.MultiScaleOracle(w.ndim, w.n, w.K, w.bc, depth=w.depth, interp=interp)
     assert s.levels == o.L + 1
     return s, o
 
@@ -146,6 +147,30 @@ def test_presmooth_restrict_and_postsmooth(torch_mod, name, mk, variant, monkeyp
         assert rel(zg.cpu().numpy(), zo) <= KTOL, k
         rho = float(np.dot(r.ravel(), zo.ravel()))
         assert abs(rhog - rho) <= KTOL * np.linalg.norm(r) * np.linalg.norm(zo), (k, rhog, rho)
+
+
+@pytest.mark.parametrize("variant", ["default", "pair16"])
+def test_transfer_kernels_piecewise_constant_E(torch_mod, variant, monkeypatch):
+    """The single-pass restriction and the 4-plane prolongation with the piecewise-constant
+    E (every fine cell has one tap, I1 == I0 in the weight tables) against the oracle,
+    on the ragged 100 x 52 x 24 case (odd coarse dims) in both kernel families."""
+    torch = torch_mod
+    w = CASES[0][1]()
+    s, o = setup_pair(torch, w, variant, monkeypatch, interp="constant")
+    rng = np.random.default_rng(24)
+    nh = 2 * o.m + 1
+    lv, lc = o.levels[0], o.levels[1]
+    r = rng.standard_normal(lv.shape)
+    zg, cbg = s.presmooth_restrict(0, cu(torch, r))
+    zo = np.zeros(lv.shape)
+    o.smooth(0, r, zo, nh)
+    cbo = O.restrict(r - O.apply_A(lv.T, zo), o.E[0])
+    assert rel(zg.cpu().numpy(), zo) <= KTOL
+    assert rel(cbg.cpu().numpy(), cbo) <= KTOL
+    y = rng.standard_normal(lc.shape)
+    z0 = rng.standard_normal(lv.shape)
+    zb = s.prolong_add(0, cu(torch, y), cu(torch, z0), color=1).cpu().numpy()
+    assert rel(zb, np.where(lv.black, z0 + O.prolong(y, o.E[0]), z0)) <= KTOL
 
 
 def test_variants_select_the_kernels_they_name(torch_mod, monkeypatch):
