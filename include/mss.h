@@ -235,7 +235,9 @@ int mss_residual(mss_ctx* ctx, int level, const double* b, const double* x, doub
  * alternating half-sweeps from z = 0 starting red (O12), then
  * coarse_b = R (r - A_k z) on level+1 (R = E^T).  Under SGS the residual is taken on black
  * cells only (after the closing red sweep the red residual is zero up to rounding); on TMA
- * pair levels the closing red sweep and the black residual are one fused pass.  z: device
+ * pair levels the closing red sweep and the black residual are one fused pass; with scale
+ * factor 4 the stored black residual is restricted along x, y and z in one pass
+ * (k_restrict_black_xyz; column-walk levels store it from their residual kernel).  z: device
  * out, N_k; coarse_b: device out, N_{k+1}. */
 int mss_presmooth_restrict(mss_ctx* ctx, int level, const double* r, double* z, double* coarse_b);
 /* a8 + a9 exactly as the preconditioner runs them (Eq. 2.10): z += E y

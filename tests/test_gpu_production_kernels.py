@@ -7,11 +7,12 @@ formulas at the north_star kernel gate (1e-12 relative L2) on ragged shapes:
   * mss_cg_update: a11, x += alpha p, r -= alpha q, ||r||^2 (P:440-452);
   * mss_residual: a4 / O15, r = b - A x, ||r||^2 (TMA SpMV residual mode on padded levels);
   * mss_presmooth_restrict: a5 + a6, 2m+1 half-sweeps from zero then R (r - A z) (black
-    residual; column-walk k_resid_restrict_col, or on pair levels the TMA pairs, the fused
-    closing sweep + black residual, k_restrict_x_black and the y/z weight-table passes;
-    Eq. 2.10, P:267-271, P:412);
-  * mss_prolong_postsmooth: a8 + a9, z += E y then 2m+1 half-sweeps with rho = r.z fused
-    into the closing one (Eq. 2.10).
+    residual; column-walk k_resid_restrict_col storing it, or on pair levels the TMA pairs
+    and the fused closing sweep + black residual, then the single x / y / z restriction pass
+    k_restrict_black_xyz (the x-from-shared + y/z weight-table passes where the scale factor
+    is not 4); Eq. 2.10, P:267-271, P:412);
+  * mss_prolong_postsmooth: a8 + a9, z += E y (k_prolong_black4 with scale factor 4) then
+    2m+1 half-sweeps with rho = r.z fused into the closing one (Eq. 2.10).
 
 Kernel families are selected the way the solver selects them (environment knobs read at
 setup): "default" (single half-sweeps; the column walk on 3-D levels with even n_x and
