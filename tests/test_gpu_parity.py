@@ -576,8 +576,9 @@ def test_fused_closing_sweep_residual(torch_mod, name, mk, monkeypatch):
 
 @pytest.mark.parametrize("name,mk", [("C2", lambda: make_workload("C2")), ("C5_128", lambda: make_workload("C5", n=128)),
                                      ("3d_ragged", CASES[1][1]), ("tall", lambda: random_problem(3, (72, 40, 136), seed=31)),
-                                     ("C5_128_constE", lambda: make_workload("C5", n=128))],
-                         ids=["C2", "C5_128", "3d_ragged", "tall", "C5_128_constE"])
+                                     ("C5_128_constE", lambda: make_workload("C5", n=128)),
+                                     ("wide1024", lambda: random_problem(3, (1024, 16, 8), seed=33))],
+                         ids=["C2", "C5_128", "3d_ragged", "tall", "C5_128_constE", "wide1024"])
 @pytest.mark.parametrize("kc,jj,pair", [("0", "2", "1"), ("1", "2", "1"), ("3", "1", "1"), ("0", "1", "1"),
                                         ("0", "1", "0"), ("2", "2", "0")])
 def test_restrict_xyz_single_pass(torch_mod, name, mk, kc, jj, pair, monkeypatch):
